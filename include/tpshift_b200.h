@@ -1,0 +1,156 @@
+/*
+ * tpshift_b200.h -- C ABI of libtpshift_b200.so, the B200 (sm_100a) execution
+ * engine behind PAT's generation hot path (arXiv 2605.23945).
+ *
+ * The reference (`tpshift`, /root/reference/pkg) is a pure-Python simulator: it
+ * has no FFI. Its hot path crosses two seams that this library implements for
+ * real, and a Python host mirror (paper_2605_23945_b200) binds them with ctypes:
+ *
+ *   (1) the decode-step seam  oracle_decode_latency(hw, tp, B, T0 + B*arange(n))
+ *       tpshift/latency.py:111-133, called at tpshift/engine.py:291-293; its
+ *       HBM/compute terms (latency.py:123-124) are the projections below, its
+ *       KV term is tps_paged_attention, its TP comm term (latency.py:125-126) is
+ *       tps_reduce_push + the waiting tps_add_norm.
+ *   (2) the switch seam       _commit_switch, tpshift/engine.py:206-269, and the
+ *       plans it executes, plan_weight_reshard / plan_kv_migration
+ *       (tpshift/reshard.py:80-151): tps_copy_items, tps_barrier; the
+ *       communication-group pool (tpshift/switchcost.py:76-104) is the IPC set.
+ *
+ * Conventions: every entry point takes raw device pointers, integer sizes and a
+ * cudaStream_t passed as void*; calls are stream-ordered and asynchronous; the
+ * library never allocates on the hot path (PyTorch owns every buffer). Return
+ * value 0 = OK; TPS_EINVAL maps to tpshift ConfigError (tpshift/errors.py:8),
+ * TPS_EPLAN to PlanVerificationError (tpshift/errors.py:36), TPS_ECUDA to a
+ * RuntimeError carrying tps_last_error().
+ *
+ * bf16 tensors are passed as void*; fp32 as float*; all matrices row-major.
+ */
+#ifndef TPSHIFT_B200_H_
+#define TPSHIFT_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TPS_OK 0
+#define TPS_EINVAL (-22)
+#define TPS_EPLAN (-1001)
+#define TPS_ECUDA (-1002)
+
+/* Completion-counter wait: spin until *ctr >= (*epoch) * mult + add
+ * (epoch may be NULL -> target = add). NULL spec = no wait. */
+typedef struct tps_wait {
+  const uint64_t* ctr;
+  const uint64_t* epoch;
+  uint64_t mult;
+  uint64_t add;
+} tps_wait;
+
+/* One contiguous chunk of a reshard / migration copy (32 bytes, device array). */
+typedef struct tps_copy_item {
+  const void* src;
+  void* dst;
+  uint64_t bytes;
+  uint64_t reserved;
+} tps_copy_item;
+
+/* ---------------------------------------------------------------- setup --- */
+/* Library/ABI version string. */
+const char* tps_version(void);
+/* Last error text of the calling thread (valid until the next failing call). */
+const char* tps_last_error(void);
+/* Bind the calling thread to `device`, report its SM count; checks sm_100. */
+int tps_init(int device, int* sm_count);
+
+/* ------------------------------------------------ decode step (seam 1) --- */
+/* Split-K count tps_linear will use for an [n x k] weight at batch b. */
+int tps_linear_splits(int64_t n, int64_t k, int64_t b);
+
+/* Column/row-parallel projection on tcgen05 tensor cores:
+ *   out[s][i][j] = sum_{kk in split s} W[j][kk] * X[i][kk],  i < b, j < n
+ * W: bf16 [n][ldw], X: bf16 [x_rows][ldx] (rows >= b are ignored), out: fp32
+ * [splits][b][n]. Replaces the weight-traffic/compute term of
+ * oracle_decode_latency (tpshift/latency.py:123-124). */
+int tps_linear(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,
+               int64_t x_rows, int64_t ldx, float* out, int splits, void* stream);
+
+/* resid[b] = E[history[slot][pos_by_slot[slot]]] (slot = row_slot[b]). */
+int tps_embed(const int* row_slot, const int* pos_by_slot, const int* history, int hist_ld,
+              const void* table, int H, int B, float* resid, void* stream);
+
+/* resid[b] += sum_i srcs[i][b] (list order), then out[b] = bf16(RMSNorm(resid[b]) * w).
+ * srcs: host array of nsrc device pointers, each fp32 [B][H]. This is the
+ * consumer of the O/down projections and of the TP allreduce receive slots. */
+int tps_add_norm(float* resid, const float* const* srcs, int nsrc, const tps_wait* wait, const void* w,
+                 float eps, int H, int B, void* out, int ldo, void* stream);
+
+/* One-shot TP allreduce, push half (reference comm term, tpshift/latency.py:125-126):
+ * r = sum_i srcs[i] (fp32, n elements), stored to every dsts[d] (this rank's slot
+ * in each TP peer's receive area, NVLink P2P stores), then +1 on every sig_ctrs[]
+ * (issued once per launch by the last CTA; `done` is that launch site's CTA counter). */
+int tps_reduce_push(const float* const* srcs, int nsrc, float* const* dsts, int ndst, int64_t n,
+                    uint64_t* const* sig_ctrs, int nsig, unsigned int* done, void* stream);
+
+/* QKV: sum split partials [s][B][(nq+2nkv)*D] + bias, rotate-half RoPE (fp32
+ * cos/sin tables [pos][D/2]), q -> bf16 [B][nq][D], k/v appended at each
+ * row's position into the paged cache [page][nkv][64][D]. */
+int tps_qkv_rope_append(const float* const* srcs, int nsrc, const void* bias, const int* row_slot,
+                        const int* pos_by_slot, const int* page_table, int max_pages, const float* cos_t,
+                        const float* sin_t, int B, int nq, int nkv, int D, int page_size, void* q_out,
+                        void* k_cache, void* v_cache, void* stream);
+
+/* Split count for tps_paged_attention. */
+int tps_attn_splits(int B, int nkv, int max_pages);
+
+/* Paged GQA decode attention over ctx = pos+1 tokens per row, split-KV with a
+ * log-sum-exp merge; out bf16 [B][nq][D]. part_m/part_l: fp32 [B][nq][nsplit],
+ * part_o: fp32 [B][nq][nsplit][D] scratch. KV term of tpshift/latency.py:123. */
+int tps_paged_attention(const void* q, const void* k_cache, const void* v_cache, const int* row_slot,
+                        const int* pos_by_slot, const int* page_table, int max_pages, int B, int nq,
+                        int nkv, int D, int nsplit, float* part_m, float* part_l, float* part_o, void* out,
+                        void* stream);
+
+/* act[b][f] = bf16(silu(g) * u) from split partials [s][B][2F] = [gate | up]. */
+int tps_silu_mul(const float* const* srcs, int nsrc, int B, int F, void* out, int ldo, void* stream);
+
+/* Vocab-parallel greedy argmax, stage 1: per-(row, chunk) (max, smallest global
+ * index) candidates from LM-head split partials [s][B][V]; signals sig_ctrs. */
+int tps_argmax_stage1(const float* const* srcs, int nsrc, int B, int V, int vocab_offset, int nchunk,
+                      void* cand, uint64_t* const* sig_ctrs, int nsig, unsigned int* done, void* stream);
+
+/* Stage 2: reduce candidates of all TP ranks (list = rank order), append the
+ * token to history[slot][pos+1] unless pos+1 is still inside the prompt
+ * (prompt_len may be NULL), advance pos_by_slot[slot]. out_tok may be NULL. */
+int tps_argmax_finalize(const void* const* cands, int ncand, int nchunk, const tps_wait* wait, int B,
+                        const int* row_slot, int* pos_by_slot, const int* prompt_len, int* history,
+                        int hist_ld, int* out_tok, void* stream);
+
+/* *epoch += 1 (end of a decode step; drives graph-replay-safe counter waits). */
+int tps_epoch_advance(uint64_t* epoch, void* stream);
+
+/* out[i] = sum_s srcs[s][i] for i < n (fp32). */
+int tps_sum_partials(const float* const* srcs, int nsrc, int64_t n, float* out, void* stream);
+
+/* --------------------------------------------------- switch (seam 2) ----- */
+/* Execute n copy items (device array of tps_copy_item). mode 0 = LSU vector
+ * copy, 1 = TMA bulk (cp.async.bulk) staged copy. grid <= 0 -> 2 x SMs.
+ * Replaces the All-Gather + Slice of tpshift/reshard.py:80-151. */
+int tps_copy_items(const tps_copy_item* items, int n, int mode, int grid, void* stream);
+
+/* Device barrier over a communication group: +1 on each peer counter, then wait
+ * until *my_ctr >= target. */
+int tps_barrier(uint64_t* const* peer_ctrs, int npeers, uint64_t* my_ctr, uint64_t target, void* stream);
+
+/* CUDA IPC for the Cache Manager's per-(tp, dp) peer tables
+ * (CommGroupPool, tpshift/switchcost.py:76-104). handle: 64 bytes. */
+int tps_ipc_get_handle(const void* ptr, void* handle_out, int64_t* offset_out);
+int tps_ipc_open(const void* handle, void** base_out);
+int tps_ipc_close(void* base);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TPSHIFT_B200_H_ */

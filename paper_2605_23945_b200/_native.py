@@ -1,0 +1,132 @@
+"""ctypes binding of libtpshift_b200.so (the C ABI in include/tpshift_b200.h).
+
+The CUDA engine is the only execution path: if the library is missing or the
+device is not sm_100, every runtime entry point raises. There is no CPU or
+eager-PyTorch fallback for the hot path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import ConfigError, PlanVerificationError
+
+LIB_NAME = "libtpshift_b200.so"
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+
+TPS_OK = 0
+TPS_EINVAL = -22
+TPS_EPLAN = -1001
+TPS_ECUDA = -1002
+
+# Every entry point declared in include/tpshift_b200.h, with its ctypes signature.
+_vp = ctypes.c_void_p
+_i32 = ctypes.c_int
+_i64 = ctypes.c_int64
+_f32 = ctypes.c_float
+_pp = ctypes.c_void_p  # pointer to a host array of device pointers
+
+SIGNATURES = {
+    "tps_version": (ctypes.c_char_p, []),
+    "tps_last_error": (ctypes.c_char_p, []),
+    "tps_init": (_i32, [_i32, ctypes.POINTER(_i32)]),
+    "tps_linear_splits": (_i32, [_i64, _i64, _i64]),
+    "tps_linear": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _vp, _i32, _vp]),
+    "tps_embed": (_i32, [_vp, _vp, _vp, _i32, _vp, _i32, _i32, _vp, _vp]),
+    "tps_add_norm": (_i32, [_vp, _pp, _i32, _vp, _vp, _f32, _i32, _i32, _vp, _i32, _vp]),
+    "tps_reduce_push": (_i32, [_pp, _i32, _pp, _i32, _i64, _pp, _i32, _vp, _vp]),
+    "tps_qkv_rope_append": (_i32, [_pp, _i32, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _i32, _i32, _i32,
+                                   _i32, _i32, _vp, _vp, _vp, _vp]),
+    "tps_attn_splits": (_i32, [_i32, _i32, _i32]),
+    "tps_paged_attention": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32,
+                                   _vp, _vp, _vp, _vp, _vp]),
+    "tps_silu_mul": (_i32, [_pp, _i32, _i32, _i32, _vp, _i32, _vp]),
+    "tps_argmax_stage1": (_i32, [_pp, _i32, _i32, _i32, _i32, _i32, _vp, _pp, _i32, _vp, _vp]),
+    "tps_argmax_finalize": (_i32, [_pp, _i32, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _i32, _vp, _vp]),
+    "tps_epoch_advance": (_i32, [_vp, _vp]),
+    "tps_sum_partials": (_i32, [_pp, _i32, _i64, _vp, _vp]),
+    "tps_copy_items": (_i32, [_vp, _i32, _i32, _i32, _vp]),
+    "tps_barrier": (_i32, [_pp, _i32, _vp, ctypes.c_uint64, _vp]),
+    "tps_ipc_get_handle": (_i32, [_vp, _vp, ctypes.POINTER(_i64)]),
+    "tps_ipc_open": (_i32, [_vp, ctypes.POINTER(_vp)]),
+    "tps_ipc_close": (_i32, [_vp]),
+}
+
+
+class TpsWait(ctypes.Structure):
+    _fields_ = [("ctr", ctypes.c_void_p), ("epoch", ctypes.c_void_p),
+                ("mult", ctypes.c_uint64), ("add", ctypes.c_uint64)]
+
+
+COPY_ITEM_BYTES = 32
+
+_lock = threading.Lock()
+_lib = None
+
+
+class NativeUnavailable(RuntimeError):
+    """The CUDA engine library could not be loaded."""
+
+
+def load_library(path: str = LIB_PATH):
+    """Load the library and bind every declared symbol (raises if any is absent)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise NativeUnavailable(
+                f"{path} is missing: build it with `make` (or __graft_entry__.build()); "
+                "the B200 engine has no fallback path")
+        lib = ctypes.CDLL(path)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)  # AttributeError if the ABI is incomplete
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def lib():
+    return _lib if _lib is not None else load_library()
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == TPS_OK:
+        return
+    msg = lib().tps_last_error().decode(errors="replace")
+    text = f"{what}: {msg}" if what else msg
+    if rc == TPS_EINVAL:
+        raise ConfigError(text)
+    if rc == TPS_EPLAN:
+        raise PlanVerificationError(text)
+    raise RuntimeError(f"libtpshift_b200 error {rc}: {text}")
+
+
+def ptr_array(ptrs) -> ctypes.Array:
+    """Host array of device pointers (kept alive by the caller for the call)."""
+    arr = (ctypes.c_void_p * max(1, len(ptrs)))()
+    for i, p in enumerate(ptrs):
+        arr[i] = int(p)
+    return arr
+
+
+def wait_spec(ctr: int | None, epoch: int | None = None, mult: int = 0, add: int = 0):
+    if not ctr:
+        return None
+    return ctypes.byref(TpsWait(ctypes.c_void_p(int(ctr)),
+                                ctypes.c_void_p(int(epoch)) if epoch else None,
+                                int(mult), int(add)))
+
+
+_initialized_devices: set[int] = set()
+
+
+def init_device(device: int) -> int:
+    """tps_init: bind + verify sm_100; returns the SM count."""
+    sm = ctypes.c_int(0)
+    check(lib().tps_init(int(device), ctypes.byref(sm)), "tps_init")
+    _initialized_devices.add(int(device))
+    return sm.value

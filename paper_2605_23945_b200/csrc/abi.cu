@@ -1,0 +1,227 @@
+// extern "C" entry points of libtpshift_b200.so (declared in include/tpshift_b200.h).
+// Each one validates its arguments, packs host pointer lists into by-value
+// kernel parameter structs and forwards to the kernel launchers.
+#include <stdio.h>
+
+#include <string>
+
+#include "../../include/tpshift_b200.h"
+#include "common.cuh"
+#include "decode_ops.cuh"
+
+namespace tps {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+// launchers (defined in the kernel translation units)
+int linear_splits(int64_t n, int64_t k, int64_t b);
+int linear(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
+           int64_t ldx, float* out, int splits, cudaStream_t stream);
+int embed(const int*, const int*, const int*, int, const void*, int, int, float*, cudaStream_t);
+int add_norm(float*, const SrcList&, const WaitSpec&, const void*, float, int, int, void*, int, cudaStream_t);
+int reduce_push(const SrcList&, const DstList&, int64_t, const SignalSpec&, cudaStream_t);
+int qkv_rope_append(const SrcList&, const void*, const int*, const int*, const int*, int, const float*,
+                    const float*, int, int, int, int, int, void*, void*, void*, cudaStream_t);
+int silu_mul(const SrcList&, int, int, void*, int, cudaStream_t);
+int argmax_stage1(const SrcList&, int, int, int, int, void*, const SignalSpec&, cudaStream_t);
+int argmax_finalize(const CandList&, int, const WaitSpec&, int, const int*, int*, const int*, int*, int, int*,
+                    cudaStream_t);
+int epoch_advance(uint64_t*, cudaStream_t);
+int sum_src(const SrcList&, int64_t, float*, cudaStream_t);
+int attn_splits(int B, int nkv, int max_pages);
+int paged_attention(const void*, const void*, const void*, const int*, const int*, const int*, int, int, int,
+                    int, int, int, float*, float*, float*, void*, cudaStream_t);
+int copy_items(const void*, int, int, int, cudaStream_t);
+int configure_gemm();
+int configure_attention();
+int configure_copy();
+int barrier(uint64_t* const*, int, uint64_t*, uint64_t, cudaStream_t);
+int ipc_get_handle(const void*, void*, int64_t*);
+int ipc_open(const void*, void**);
+int ipc_close(void*);
+
+static int make_src(const float* const* srcs, int nsrc, SrcList* out) {
+  if (nsrc < 0 || nsrc > kMaxSrc) return fail(kInvalid, "source list longer than 64 entries");
+  if (nsrc > 0 && !srcs) return fail(kInvalid, "null source list");
+  out->n = nsrc;
+  for (int i = 0; i < nsrc; ++i) {
+    if (!srcs[i]) return fail(kInvalid, "null source pointer");
+    out->p[i] = srcs[i];
+  }
+  return kOk;
+}
+
+static int make_sig(uint64_t* const* ctrs, int n, unsigned int* done, SignalSpec* out) {
+  if (n < 0 || n > kMaxPeers) return fail(kInvalid, "signal list longer than 8 entries");
+  if (n > 0 && !done) return fail(kInvalid, "signal list needs a done counter");
+  out->n = n;
+  out->done = done;
+  for (int i = 0; i < n; ++i) out->ctr[i] = ctrs[i];
+  return kOk;
+}
+
+static WaitSpec make_wait(const tps_wait* w) {
+  WaitSpec s{};
+  if (w) {
+    s.ctr = w->ctr;
+    s.epoch = w->epoch;
+    s.mult = w->mult;
+    s.add = w->add;
+  }
+  return s;
+}
+
+static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+}  // namespace tps
+
+using namespace tps;
+
+extern "C" {
+
+const char* tps_version(void) { return "tpshift_b200 1.0 (sm_100a; tcgen05 GEMM, paged GQA decode, P2P switch)"; }
+
+const char* tps_last_error(void) { return g_last_error.c_str(); }
+
+int tps_init(int device, int* sm_count) {
+  TPS_CUDA_TRY(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  TPS_CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  if (sm_count) *sm_count = prop.multiProcessorCount;
+  if (prop.major != 10)
+    return fail(kUnsupported, std::string("libtpshift_b200 is built for sm_100a; device is sm_") +
+                                  std::to_string(prop.major) + std::to_string(prop.minor));
+  // kernel attributes (dynamic smem opt-in) are set once here, outside any stream capture
+  int rc = configure_gemm();
+  if (!rc) rc = configure_attention();
+  if (!rc) rc = configure_copy();
+  return rc;
+}
+
+int tps_linear_splits(int64_t n, int64_t k, int64_t b) { return linear_splits(n, k, b); }
+
+int tps_linear(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
+               int64_t ldx, float* out, int splits, void* stream) {
+  return linear(w, n, k, ldw, x, b, x_rows, ldx, out, splits, S(stream));
+}
+
+int tps_embed(const int* row_slot, const int* pos_by_slot, const int* history, int hist_ld, const void* table,
+              int H, int B, float* resid, void* stream) {
+  TPS_CHECK_ARG(row_slot && pos_by_slot && history && table && resid, "embed: null pointer");
+  return embed(row_slot, pos_by_slot, history, hist_ld, table, H, B, resid, S(stream));
+}
+
+int tps_add_norm(float* resid, const float* const* srcs, int nsrc, const tps_wait* wait, const void* w,
+                 float eps, int H, int B, void* out, int ldo, void* stream) {
+  TPS_CHECK_ARG(resid && w && out, "add_norm: null pointer");
+  SrcList sl;
+  int rc = make_src(srcs, nsrc, &sl);
+  if (rc) return rc;
+  return add_norm(resid, sl, make_wait(wait), w, eps, H, B, out, ldo, S(stream));
+}
+
+int tps_reduce_push(const float* const* srcs, int nsrc, float* const* dsts, int ndst, int64_t n,
+                    uint64_t* const* sig_ctrs, int nsig, unsigned int* done, void* stream) {
+  SrcList sl;
+  int rc = make_src(srcs, nsrc, &sl);
+  if (rc) return rc;
+  TPS_CHECK_ARG(ndst >= 1 && ndst <= kMaxPeers && dsts, "reduce_push: 1..8 destinations");
+  DstList dl;
+  dl.n = ndst;
+  for (int i = 0; i < ndst; ++i) dl.p[i] = dsts[i];
+  SignalSpec sg;
+  rc = make_sig(sig_ctrs, nsig, done, &sg);
+  if (rc) return rc;
+  return reduce_push(sl, dl, n, sg, S(stream));
+}
+
+int tps_qkv_rope_append(const float* const* srcs, int nsrc, const void* bias, const int* row_slot,
+                        const int* pos_by_slot, const int* page_table, int max_pages, const float* cos_t,
+                        const float* sin_t, int B, int nq, int nkv, int D, int page_size, void* q_out,
+                        void* k_cache, void* v_cache, void* stream) {
+  TPS_CHECK_ARG(page_size == 64, "qkv_rope_append: page_size must be 64");
+  TPS_CHECK_ARG(row_slot && pos_by_slot && page_table && cos_t && sin_t && q_out && k_cache && v_cache,
+                "qkv_rope_append: null pointer");
+  SrcList sl;
+  int rc = make_src(srcs, nsrc, &sl);
+  if (rc) return rc;
+  return qkv_rope_append(sl, bias, row_slot, pos_by_slot, page_table, max_pages, cos_t, sin_t, B, nq, nkv, D,
+                         page_size, q_out, k_cache, v_cache, S(stream));
+}
+
+int tps_attn_splits(int B, int nkv, int max_pages) { return attn_splits(B, nkv, max_pages); }
+
+int tps_paged_attention(const void* q, const void* k_cache, const void* v_cache, const int* row_slot,
+                        const int* pos_by_slot, const int* page_table, int max_pages, int B, int nq, int nkv,
+                        int D, int nsplit, float* part_m, float* part_l, float* part_o, void* out,
+                        void* stream) {
+  TPS_CHECK_ARG(q && k_cache && v_cache && row_slot && pos_by_slot && page_table && part_m && part_l &&
+                    part_o && out,
+                "paged_attention: null pointer");
+  return paged_attention(q, k_cache, v_cache, row_slot, pos_by_slot, page_table, max_pages, B, nq, nkv, D,
+                         nsplit, part_m, part_l, part_o, out, S(stream));
+}
+
+int tps_silu_mul(const float* const* srcs, int nsrc, int B, int F, void* out, int ldo, void* stream) {
+  SrcList sl;
+  int rc = make_src(srcs, nsrc, &sl);
+  if (rc) return rc;
+  return silu_mul(sl, B, F, out, ldo, S(stream));
+}
+
+int tps_argmax_stage1(const float* const* srcs, int nsrc, int B, int V, int vocab_offset, int nchunk,
+                      void* cand, uint64_t* const* sig_ctrs, int nsig, unsigned int* done, void* stream) {
+  SrcList sl;
+  int rc = make_src(srcs, nsrc, &sl);
+  if (rc) return rc;
+  SignalSpec sg;
+  rc = make_sig(sig_ctrs, nsig, done, &sg);
+  if (rc) return rc;
+  return argmax_stage1(sl, B, V, vocab_offset, nchunk, cand, sg, S(stream));
+}
+
+int tps_argmax_finalize(const void* const* cands, int ncand, int nchunk, const tps_wait* wait, int B,
+                        const int* row_slot, int* pos_by_slot, const int* prompt_len, int* history, int hist_ld,
+                        int* out_tok, void* stream) {
+  TPS_CHECK_ARG(ncand >= 1 && ncand <= kMaxPeers && cands, "argmax_finalize: 1..8 candidate arrays");
+  CandList cl;
+  cl.n = ncand;
+  for (int i = 0; i < ncand; ++i) cl.p[i] = reinterpret_cast<const ArgmaxCand*>(cands[i]);
+  return argmax_finalize(cl, nchunk, make_wait(wait), B, row_slot, pos_by_slot, prompt_len, history, hist_ld,
+                         out_tok, S(stream));
+}
+
+int tps_epoch_advance(uint64_t* epoch, void* stream) {
+  TPS_CHECK_ARG(epoch, "epoch_advance: null pointer");
+  return epoch_advance(epoch, S(stream));
+}
+
+int tps_sum_partials(const float* const* srcs, int nsrc, int64_t n, float* out, void* stream) {
+  SrcList sl;
+  int rc = make_src(srcs, nsrc, &sl);
+  if (rc) return rc;
+  return sum_src(sl, n, out, S(stream));
+}
+
+int tps_copy_items(const tps_copy_item* items, int n, int mode, int grid, void* stream) {
+  static_assert(sizeof(tps_copy_item) == 32, "copy item layout");
+  return copy_items(items, n, mode, grid, S(stream));
+}
+
+int tps_barrier(uint64_t* const* peer_ctrs, int npeers, uint64_t* my_ctr, uint64_t target, void* stream) {
+  return barrier(peer_ctrs, npeers, my_ctr, target, S(stream));
+}
+
+int tps_ipc_get_handle(const void* ptr, void* handle_out, int64_t* offset_out) {
+  return ipc_get_handle(ptr, handle_out, offset_out);
+}
+int tps_ipc_open(const void* handle, void** base_out) { return ipc_open(handle, base_out); }
+int tps_ipc_close(void* base) { return ipc_close(base); }
+
+}  // extern "C"

@@ -1,0 +1,199 @@
+// Switch Executor data movement: batched peer pulls for weight reshard and
+// KV-page migration, plus the device barrier and CUDA-IPC plumbing.
+//
+// Replaces the layer-wise All-Gather + Slice the reference plans
+// (plan_weight_reshard / plan_kv_migration, tpshift/reshard.py:80-151) with
+// one-sided pulls: every target rank reads exactly the canonical slices it
+// owns from whichever rank holds them (local HBM when the slice is already
+// resident, an NVLink peer otherwise). Copies are byte-exact by construction.
+//
+// Work items are 1-D contiguous chunks (host-side planner splits 2-D slices
+// into rows / <=64 KB pieces). Two engines:
+//   mode 0: LSU copy, 4 x 16 B loads in flight per thread, persistent grid;
+//   mode 1: TMA-staged copy, cp.async.bulk global->smem->global through a
+//           4-deep ring of 32 KB buffers per CTA (no register round trip).
+#include "common.cuh"
+
+namespace tps {
+
+struct CopyItem {
+  const uint8_t* src;
+  uint8_t* dst;
+  uint64_t bytes;
+  uint64_t reserved;
+};
+
+constexpr int kCopyThreads = 256;
+
+__global__ void __launch_bounds__(kCopyThreads) copy_items_lsu_kernel(const CopyItem* __restrict__ items,
+                                                                      int n) {
+  for (int it = blockIdx.x; it < n; it += gridDim.x) {
+    const CopyItem ci = items[it];
+    const bool aligned = ((reinterpret_cast<uintptr_t>(ci.src) | reinterpret_cast<uintptr_t>(ci.dst)) & 15u) == 0;
+    const uint64_t nvec = aligned ? ci.bytes / 16 : 0;
+    const int4* s = reinterpret_cast<const int4*>(ci.src);
+    int4* d = reinterpret_cast<int4*>(ci.dst);
+    uint64_t i = threadIdx.x;
+    for (; i + 3 * kCopyThreads < nvec; i += 4 * kCopyThreads) {
+      int4 v0 = s[i], v1 = s[i + kCopyThreads], v2 = s[i + 2 * kCopyThreads], v3 = s[i + 3 * kCopyThreads];
+      d[i] = v0;
+      d[i + kCopyThreads] = v1;
+      d[i + 2 * kCopyThreads] = v2;
+      d[i + 3 * kCopyThreads] = v3;
+    }
+    for (; i < nvec; i += kCopyThreads) d[i] = s[i];
+    for (uint64_t j = nvec * 16 + threadIdx.x; j < ci.bytes; j += kCopyThreads) ci.dst[j] = ci.src[j];
+  }
+}
+
+constexpr int kBulkBuf = 32 * 1024;
+constexpr int kBulkDepth = 4;
+
+// One elected thread per CTA drives a kBulkDepth-deep ring: loads of chunks
+// k+1..k+depth-1 are in flight while chunk k is being stored.
+__global__ void __launch_bounds__(32) copy_items_tma_kernel(const CopyItem* __restrict__ items, int n) {
+  extern __shared__ __align__(128) uint8_t sbuf[];
+  __shared__ __align__(8) uint64_t bars[kBulkDepth];
+  if (threadIdx.x != 0) return;
+  for (int i = 0; i < kBulkDepth; ++i) mbar_init(&bars[i], 1);
+  fence_barrier_init();
+  int git = blockIdx.x;
+  uint64_t goff = 0;
+  auto next = [&](const uint8_t*& s, uint8_t*& d, uint32_t& len) -> bool {
+    while (git < n) {
+      const CopyItem ci = items[git];
+      if (goff < ci.bytes) {
+        const uint64_t rem = ci.bytes - goff;
+        len = (uint32_t)(rem < (uint64_t)kBulkBuf ? rem : (uint64_t)kBulkBuf);
+        s = ci.src + goff;
+        d = ci.dst + goff;
+        goff += len;
+        return true;
+      }
+      git += gridDim.x;
+      goff = 0;
+    }
+    return false;
+  };
+  uint8_t* dsts[kBulkDepth];
+  uint32_t lens[kBulkDepth];
+  uint32_t phases = 0;
+  int head = 0, tail = 0;
+  const uint8_t* s;
+  uint8_t* d;
+  uint32_t len;
+  while (tail < kBulkDepth && next(s, d, len)) {
+    const int sl = tail % kBulkDepth;
+    mbar_arrive_expect_tx(&bars[sl], len);
+    bulk_g2s(sbuf + sl * kBulkBuf, s, len, &bars[sl]);
+    dsts[sl] = d;
+    lens[sl] = len;
+    ++tail;
+  }
+  while (head < tail) {
+    const int sl = head % kBulkDepth;
+    mbar_wait(&bars[sl], (phases >> sl) & 1u);
+    phases ^= (1u << sl);
+    bulk_s2g(dsts[sl], sbuf + sl * kBulkBuf, lens[sl]);
+    bulk_commit();
+    ++head;
+    if (next(s, d, len)) {
+      bulk_wait_read<0>();  // the store just issued has read its smem slot
+      const int sl2 = tail % kBulkDepth;
+      mbar_arrive_expect_tx(&bars[sl2], len);
+      bulk_g2s(sbuf + sl2 * kBulkBuf, s, len, &bars[sl2]);
+      dsts[sl2] = d;
+      lens[sl2] = len;
+      ++tail;
+    }
+  }
+  bulk_wait<0>();
+}
+
+int configure_copy() {
+  TPS_CUDA_TRY(cudaFuncSetAttribute(copy_items_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kBulkBuf * kBulkDepth));
+  return kOk;
+}
+
+int copy_items(const void* items, int n, int mode, int grid, cudaStream_t st) {
+  TPS_CHECK_ARG(n >= 0, "copy_items: n >= 0");
+  if (n == 0) return kOk;
+  if (grid <= 0) grid = 2 * kNumSMs;
+  if (grid > n) grid = n;
+  if (mode == 0) {
+    copy_items_lsu_kernel<<<grid, kCopyThreads, 0, st>>>(reinterpret_cast<const CopyItem*>(items), n);
+  } else if (mode == 1) {
+    const int smem = kBulkBuf * kBulkDepth;
+    copy_items_tma_kernel<<<grid, 32, smem, st>>>(reinterpret_cast<const CopyItem*>(items), n);
+  } else {
+    return fail(kInvalid, "copy_items: mode must be 0 (LSU) or 1 (TMA bulk)");
+  }
+  TPS_LAUNCH_CHECK();
+  return kOk;
+}
+
+// ------------------------------------------------------ device barrier ----
+// Every rank adds 1 to each peer's counter, then waits for its own counter to
+// reach target (= epoch * (nranks - 1) for a full barrier). Stream ordered.
+constexpr int kMaxPeerArgs = 16;
+struct PeerPtrs {
+  uint64_t* p[kMaxPeerArgs];
+};
+
+__global__ void barrier_kernel_v(PeerPtrs peers, int npeers, uint64_t* my_ctr, uint64_t target) {
+  if (threadIdx.x != 0) return;
+  __threadfence_system();
+  for (int i = 0; i < npeers; ++i) red_release_sys_add(peers.p[i], 1ull);
+  wait_counter_geq(my_ctr, target);
+  __threadfence_system();
+}
+
+int barrier(uint64_t* const* peer_ctrs, int npeers, uint64_t* my_ctr, uint64_t target, cudaStream_t st) {
+  TPS_CHECK_ARG(npeers >= 0 && npeers <= kMaxPeerArgs && my_ctr, "barrier: bad args");
+  PeerPtrs pp{};
+  for (int i = 0; i < npeers; ++i) pp.p[i] = peer_ctrs[i];
+  barrier_kernel_v<<<1, 32, 0, st>>>(pp, npeers, my_ctr, target);
+  TPS_LAUNCH_CHECK();
+  return kOk;
+}
+
+// ------------------------------------------------------------------ IPC ---
+typedef CUresult (*GetAddrRangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+int ipc_get_handle(const void* ptr, void* handle_out, int64_t* offset_out) {
+  TPS_CHECK_ARG(ptr && handle_out && offset_out, "ipc_get_handle: null argument");
+  static GetAddrRangeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return fail(kCuda, "cuMemGetAddressRange entry point unavailable");
+    fn = reinterpret_cast<GetAddrRangeFn>(p);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (fn(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS)
+    return fail(kCuda, "cuMemGetAddressRange failed");
+  cudaIpcMemHandle_t h;
+  TPS_CUDA_TRY(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  memcpy(handle_out, &h, sizeof(h));
+  *offset_out = (int64_t)(reinterpret_cast<uintptr_t>(ptr) - (uintptr_t)base);
+  return kOk;
+}
+
+int ipc_open(const void* handle, void** base_out) {
+  TPS_CHECK_ARG(handle && base_out, "ipc_open: null argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  TPS_CUDA_TRY(cudaIpcOpenMemHandle(base_out, h, cudaIpcMemLazyEnablePeerAccess));
+  return kOk;
+}
+
+int ipc_close(void* base) {
+  TPS_CUDA_TRY(cudaIpcCloseMemHandle(base));
+  return kOk;
+}
+
+}  // namespace tps

@@ -1,0 +1,362 @@
+// Skinny decode GEMM on 5th-gen tensor cores (tcgen05 + TMA + TMEM), sm_100a.
+//
+//   out[split][b][n] = sum_{k in split} W[n][k] * X[b][k]        (fp32 partials)
+//
+// This is the Infer Executor's column-/row-parallel projection (QKV, O, gate/up,
+// down, LM head) for a decode step, i.e. the work the reference prices with the
+// HBM/compute terms of oracle_decode_latency (tpshift/latency.py:123-124).
+// Decode is weight-streaming bound (batch B <= 256 << the bf16 ridge), so the
+// kernel is built to keep HBM busy:
+//   * swap-AB: the weight tile is the 128-row UMMA "M" operand, the B tokens are
+//     the UMMA "N" operand (N = BN, padded to a multiple of 16), so one MMA
+//     shape serves every batch from 1 to 256;
+//   * persistent grid (<= 148 CTAs, one per SM) walking (tile, k-split) units;
+//     k-splits fill the machine when N/128 tiles alone would not;
+//   * warp-specialised: warp0 = TMA producer (weights EVICT_FIRST, activations
+//     EVICT_LAST), warp1 = single-thread tcgen05.mma issuer, warp2 = TMEM
+//     allocator, warps4-7 = epilogue (tcgen05.ld -> fp32 partials);
+//   * a 4-8 stage smem ring (SWIZZLE_128B) and two TMEM accumulators so the
+//     epilogue of unit i overlaps the MMAs of unit i+1.
+// Split partials are reduced, in fixed split order, by the consumer kernels
+// (norm / rope / silu / argmax), which keeps results deterministic.
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "common.cuh"
+
+namespace tps {
+
+constexpr int kBM = 128;  // weight rows per tile == UMMA M
+constexpr int kBK = 64;   // K elements per stage == one 128-byte swizzle row
+constexpr int kGemmThreads = 256;
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int kABytes = kBM * kBK * 2;
+  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStagesRaw = (200 * 1024) / kStageBytes;
+  static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
+  static constexpr int kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
+  static constexpr int kBarBytes = 256;
+  static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kBarBytes;
+  static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128 must be 16..256, %16");
+  static_assert(kStages >= 3, "need at least 3 stages");
+};
+
+// UMMA shared-memory descriptor, K-major operand in the canonical SWIZZLE_128B layout
+// (8-row x 128-byte atoms; SBO = 1024 B between atoms; version 1 for sm_100).
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((1024u >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1u << 46;
+  d |= (uint64_t)2u << 61;
+  return d;
+}
+
+__device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_swapab_kernel(const __grid_constant__ CUtensorMap tmap_w,
+                       const __grid_constant__ CUtensorMap tmap_x, float* __restrict__ out, int N,
+                       int B, int num_tiles, int splits, int chunks) {
+  using Cfg = GemmCfg<BN>;
+  constexpr int S = Cfg::kStages;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem + S * Cfg::kABytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + S;
+  uint64_t* tmem_full = bars + 2 * S;
+  uint64_t* tmem_empty = bars + 2 * S + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int units = num_tiles * splits;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tmem_full[a], 1);
+      mbar_init(&tmem_empty[a], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmap_w);
+    prefetch_tmap(&tmap_x);
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(Cfg::kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      const uint64_t pol_w = policy_evict_first();
+      const uint64_t pol_x = policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int tile = u / splits, split = u % splits;
+        const int c0 = (int)((long long)split * chunks / splits);
+        const int c1 = (int)((long long)(split + 1) * chunks / splits);
+        for (int c = c0; c < c1; ++c) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
+          tma_load_2d(smem_a + stage * Cfg::kABytes, &tmap_w, &full[stage], c * kBK, tile * kBM, pol_w);
+          tma_load_2d(smem_b + stage * Cfg::kBBytes, &tmap_x, &full[stage], c * kBK, 0, pol_x);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer (single thread) ----------------
+      constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                                 ((uint32_t)(kBM >> 4) << 24);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int split = u % splits;
+        const int c0 = (int)((long long)split * chunks / splits);
+        const int c1 = (int)((long long)(split + 1) * chunks / splits);
+        mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+        for (int c = c0; c < c1; ++c) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t a0 = umma_desc_sw128(smem_u32(smem_a + stage * Cfg::kABytes));
+          const uint64_t b0 = umma_desc_sw128(smem_u32(smem_b + stage * Cfg::kBBytes));
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            // advance 16 bf16 = 32 bytes along K inside the 128-byte swizzle row
+            umma_bf16(d_tmem, a0 + (uint64_t)(2 * k), b0 + (uint64_t)(2 * k), idesc,
+                      (c > c0 || k > 0) ? 1u : 0u);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tmem_full[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue: TMEM -> fp32 partials ----------------
+    const int q = warp & 3;  // TMEM lane quadrant owned by this warp
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int tile = u / splits, split = u % splits;
+      mbar_wait(&tmem_full[acc], acc_phase);
+      tc_fence_after();
+      const int n = tile * kBM + q * 32 + lane;
+      float* dst = out + (size_t)split * (size_t)B * (size_t)N + (size_t)n;
+      for (int j0 = 0; j0 < BN && j0 < B; j0 += 16) {
+        uint32_t r[16];
+        tmem_ld16(tmem_base + (uint32_t)(acc * BN + j0) + ((uint32_t)(q * 32) << 16), r);
+        if (n < N) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (j0 + j < B) dst[(size_t)(j0 + j) * N] = __uint_as_float(r[j]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tmem_empty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "n"(Cfg::kTmemCols));
+  }
+}
+
+// ------------------------------------------------------------------ host ---
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// 2-D bf16 tensor [rows][cols] with row pitch ld (elements), box [box_rows][64], SWIZZLE_128B.
+int make_tmap_bf16(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int64_t ld,
+                   int box_rows) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int64_t, int64_t, int64_t, int>, CUtensorMap> cache;
+  auto key = std::make_tuple(ptr, rows, cols, ld, box_rows);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *map = it->second;
+    return kOk;
+  }
+  EncodeTiledFn fn = get_encode_fn();
+  if (!fn) return fail(kCuda, "cuTensorMapEncodeTiled entry point unavailable");
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) != 0 || (ld * 2) % 16 != 0)
+    return fail(kInvalid, "tensor map: base must be 16B aligned and row pitch a multiple of 16B");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(kCuda, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  if (cache.size() > 4096) cache.clear();
+  cache[key] = *map;
+  return kOk;
+}
+
+static int pick_bn(int64_t b) {
+  if (b <= 16) return 16;
+  if (b <= 32) return 32;
+  if (b <= 64) return 64;
+  if (b <= 128) return 128;
+  return 256;
+}
+
+// Split-K choice: minimise (waves x chunks-per-unit) for a 148-SM persistent grid,
+// plus a small charge for the fp32 partial traffic the consumer has to reduce.
+int linear_splits(int64_t n, int64_t k, int64_t b) {
+  const int64_t tiles = (n + kBM - 1) / kBM;
+  const int64_t chunks = (k + kBK - 1) / kBK;
+  int best = 1;
+  double best_cost = 1e30;
+  const int max_s = (int)(chunks < 32 ? chunks : 32);
+  for (int s = 1; s <= max_s; ++s) {
+    const int64_t units = tiles * s;
+    const int64_t waves = (units + kNumSMs - 1) / kNumSMs;
+    const int64_t cpu = (chunks + s - 1) / s;
+    const double weight_cost = (double)waves * (double)cpu * (kBM * kBK * 2);
+    const double partial_cost = 0.25 * (double)s * (double)b * (double)n * 8.0 / kNumSMs;
+    const double cost = weight_cost + partial_cost;
+    if (cost < best_cost * 0.999) {
+      best_cost = cost;
+      best = s;
+    }
+  }
+  return best;
+}
+
+template <int BN>
+static int launch_gemm(const CUtensorMap& mw, const CUtensorMap& mx, float* out, int n, int b,
+                       int tiles, int splits, int chunks, cudaStream_t stream) {
+  using Cfg = GemmCfg<BN>;
+  const int units = tiles * splits;
+  const int grid = units < kNumSMs ? units : kNumSMs;
+  gemm_swapab_kernel<BN><<<grid, kGemmThreads, Cfg::kSmemBytes, stream>>>(mw, mx, out, n, b, tiles, splits,
+                                                                         chunks);
+  TPS_LAUNCH_CHECK();
+  return kOk;
+}
+
+template <int BN>
+static int configure_one() {
+  TPS_CUDA_TRY(cudaFuncSetAttribute(gemm_swapab_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    GemmCfg<BN>::kSmemBytes));
+  return kOk;
+}
+
+// Called from tps_init (never during stream capture).
+int configure_gemm() {
+  int rc = configure_one<16>();
+  if (!rc) rc = configure_one<32>();
+  if (!rc) rc = configure_one<64>();
+  if (!rc) rc = configure_one<128>();
+  if (!rc) rc = configure_one<256>();
+  return rc;
+}
+
+int linear(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,
+           int64_t x_rows, int64_t ldx, float* out, int splits, cudaStream_t stream) {
+  TPS_CHECK_ARG(w && x && out, "linear: null pointer");
+  TPS_CHECK_ARG(n > 0 && k > 0 && b > 0 && b <= 256, "linear: need n,k > 0 and 1 <= b <= 256");
+  TPS_CHECK_ARG(x_rows >= b && ldw >= k && ldx >= k, "linear: bad leading dimensions");
+  const int64_t chunks = (k + kBK - 1) / kBK;
+  TPS_CHECK_ARG(splits >= 1 && splits <= chunks, "linear: splits must be in [1, ceil(k/64)]");
+  const int bn = pick_bn(b);
+  CUtensorMap mw, mx;
+  int rc = make_tmap_bf16(&mw, w, n, k, ldw, kBM);
+  if (rc) return rc;
+  rc = make_tmap_bf16(&mx, x, x_rows, k, ldx, bn);
+  if (rc) return rc;
+  const int tiles = (int)((n + kBM - 1) / kBM);
+  switch (bn) {
+    case 16: return launch_gemm<16>(mw, mx, out, (int)n, (int)b, tiles, splits, (int)chunks, stream);
+    case 32: return launch_gemm<32>(mw, mx, out, (int)n, (int)b, tiles, splits, (int)chunks, stream);
+    case 64: return launch_gemm<64>(mw, mx, out, (int)n, (int)b, tiles, splits, (int)chunks, stream);
+    case 128: return launch_gemm<128>(mw, mx, out, (int)n, (int)b, tiles, splits, (int)chunks, stream);
+    default: return launch_gemm<256>(mw, mx, out, (int)n, (int)b, tiles, splits, (int)chunks, stream);
+  }
+}
+
+}  // namespace tps

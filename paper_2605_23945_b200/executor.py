@@ -1,0 +1,354 @@
+"""Infer Executor: one TP rank's decode step on the sm_100a engine.
+
+Replaces the reference's per-round latency oracle (the n-round block at
+tpshift/engine.py:287-300 prices `oracle_decode_latency(hw, tp, B, T)`,
+tpshift/latency.py:111-133) with the real step:
+
+  embed -> [ RMSNorm -> QKV (tcgen05) -> bias+RoPE+KV-append -> paged attention
+             -> O (tcgen05) -> TP allreduce -> add+RMSNorm -> gate/up (tcgen05)
+             -> SiLU*up -> down (tcgen05) -> TP allreduce -> add+RMSNorm ] x L
+        -> LM head (tcgen05, vocab-parallel) -> argmax (+ cross-rank reduce)
+
+A step is written once as a *program* (a Python generator that issues the
+rank's launches and yields at every point where it would wait for TP peers).
+One process per GPU runs its own program straight through (peers are NVLink
+mappings and device counters do the waiting); a single-GPU "virtual group"
+advances the programs of all ranks in lock-step, so the same kernels and the
+same counter protocol run on one device. Each (bucket) program is captured
+once into a CUDA graph and replayed for every round of a block.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _native as nat
+from .kvcache import PAGE, KVPool, SlotTable
+from .models import DecoderGeometry, RankShard, rope_tables
+from .shards import RankWeights
+
+BUCKETS = (1, 2, 4, 8, 16, 24, 32, 48, 64, 96, 128, 192, 256)
+
+
+def bucket_for(b: int, max_batch: int) -> int:
+    for x in BUCKETS:
+        if x >= b:
+            return min(x, max_batch) if x > max_batch else x
+    return max_batch
+
+
+def argmax_chunks(B: int) -> int:
+    return max(1, min(64, 296 // max(1, B)))
+
+
+class GroupComm:
+    """Communication state of one TP group as held by one rank.
+
+    recv[parity][src_rank] : fp32 [max_batch][H] receive slots (one-shot allreduce)
+    cand                   : per-(row, chunk) argmax candidates (8 B each)
+    ctr[phase]             : arrival counters, +1 per peer per phase per step
+    done[phase]            : last-CTA detectors of this rank's signalling launches
+    epoch                  : step counter; waits target epoch * tp
+    """
+
+    def __init__(self, tp: int, rank: int, max_batch: int, hidden: int, n_phases: int,
+                 device: torch.device):
+        self.tp = tp
+        self.rank = rank
+        self.max_batch = max_batch
+        self.hidden = hidden
+        self.n_phases = n_phases
+        self.recv = torch.zeros((2, tp, max_batch, hidden), dtype=torch.float32, device=device)
+        self.cand = torch.zeros((max_batch, 64, 2), dtype=torch.int32, device=device)
+        self.ctr = torch.zeros(n_phases, dtype=torch.int64, device=device)
+        self.done = torch.zeros(n_phases, dtype=torch.int32, device=device)
+        self.epoch = torch.ones(1, dtype=torch.int64, device=device)
+        # peer pointer table, rank order (filled by connect / the Cache Manager)
+        self.peer_recv: list[int] = []
+        self.peer_ctr: list[int] = []
+        self.peer_cand: list[int] = []
+
+    # local export for peers
+    def export(self) -> dict:
+        return {"recv": self.recv.data_ptr(), "ctr": self.ctr.data_ptr(), "cand": self.cand.data_ptr()}
+
+    def connect(self, tables: list[dict]) -> None:
+        assert len(tables) == self.tp
+        self.peer_recv = [t["recv"] for t in tables]
+        self.peer_ctr = [t["ctr"] for t in tables]
+        self.peer_cand = [t["cand"] for t in tables]
+
+    def recv_slot(self, base: int, parity: int, src_rank: int) -> int:
+        return base + ((parity * self.tp + src_rank) * self.max_batch * self.hidden) * 4
+
+    def reset(self) -> None:
+        self.ctr.zero_()
+        self.done.zero_()
+        self.epoch.fill_(1)
+
+
+@dataclass
+class LaunchStats:
+    kernels: int = 0
+    by_kind: dict = field(default_factory=dict)
+
+    def add(self, kind: str, n: int = 1) -> None:
+        self.kernels += n
+        self.by_kind[kind] = self.by_kind.get(kind, 0) + n
+
+
+class InferExecutor:
+    """Decode-step engine of one TP rank (the per-GPU Infer Executor)."""
+
+    def __init__(self, geom: DecoderGeometry, shard: RankShard, weights: RankWeights, kv: KVPool,
+                 slots: SlotTable, max_batch: int, device: torch.device | str,
+                 comm: GroupComm | None = None, stream: torch.cuda.Stream | None = None):
+        self.geom = geom
+        self.shard = shard
+        self.w = weights
+        self.kv = kv
+        self.slots = slots
+        self.max_batch = max_batch
+        self.device = torch.device(device)
+        self.comm = comm
+        self.tp = shard.tp
+        self.rank = shard.rank
+        assert (self.tp == 1) == (comm is None), "TP>1 needs a GroupComm"
+        nat.lib()
+        H, D = geom.hidden, geom.head_dim
+        self.nq, self.nkv = shard.n_q, shard.n_kv
+        self.n_qkv = (self.nq + 2 * self.nkv) * D
+        self.F = shard.ffn_width
+        self.V = shard.vocab_width
+        dev = self.device
+        cos, sin = rope_tables(geom, slots.max_len + 1)
+        self.cos = torch.from_numpy(cos).to(dev)
+        self.sin = torch.from_numpy(sin).to(dev)
+        self.resid = torch.zeros((max_batch, H), dtype=torch.float32, device=dev)
+        self.xn = torch.zeros((max_batch, H), dtype=torch.bfloat16, device=dev)
+        self.q = torch.zeros((max_batch, self.nq, D), dtype=torch.bfloat16, device=dev)
+        self.attn = torch.zeros((max_batch, self.nq * D), dtype=torch.bfloat16, device=dev)
+        self.act = torch.zeros((max_batch, self.F), dtype=torch.bfloat16, device=dev)
+        self.prompt_len = torch.zeros(slots.num_slots, dtype=torch.int32, device=dev)
+        # split-K workspace sized for the worst projection over all buckets
+        ws = 0
+        for B in self.buckets():
+            for n, k in self._proj_shapes():
+                ws = max(ws, nat.lib().tps_linear_splits(n, k, B) * B * n)
+        self.ws = torch.zeros(ws, dtype=torch.float32, device=dev)
+        nsplit = max(nat.lib().tps_attn_splits(B, self.nkv, slots.max_pages) for B in self.buckets())
+        self.att_m = torch.zeros(max_batch * self.nq * nsplit, dtype=torch.float32, device=dev)
+        self.att_l = torch.zeros_like(self.att_m)
+        self.att_o = torch.zeros(max_batch * self.nq * nsplit * D, dtype=torch.float32, device=dev)
+        self.local_cand = torch.zeros((max_batch, 64, 2), dtype=torch.int32, device=dev)
+        self.out_tok = torch.zeros(max_batch, dtype=torch.int32, device=dev)
+        self.row_slot = {B: torch.full((B,), -1, dtype=torch.int32, device=dev) for B in self.buckets()}
+        self.graphs: dict[int, torch.cuda.CUDAGraph] = {}
+        self.launch_stats: dict[int, LaunchStats] = {}
+        self._keep = []  # ctypes arrays alive during capture
+
+    # ------------------------------------------------------------ shapes ---
+    def buckets(self) -> list[int]:
+        out = [b for b in BUCKETS if b <= self.max_batch]
+        if not out or out[-1] != self.max_batch:
+            out.append(self.max_batch)
+        return out
+
+    def bucket(self, b: int) -> int:
+        for x in self.buckets():
+            if x >= b:
+                return x
+        raise ValueError(f"batch {b} exceeds max_batch {self.max_batch}")
+
+    def _proj_shapes(self):
+        g = self.geom
+        return [(self.n_qkv, g.hidden), (g.hidden, self.nq * g.head_dim), (2 * self.F, g.hidden),
+                (g.hidden, self.F), (self.V, g.hidden)]
+
+    # --------------------------------------------------------- primitives ---
+    def _splits(self, n: int, k: int, B: int) -> int:
+        return nat.lib().tps_linear_splits(n, k, B)
+
+    def _linear(self, st, stats, w: torch.Tensor, x: torch.Tensor, B: int) -> list[int]:
+        n, k = w.shape
+        s = self._splits(n, k, B)
+        nat.check(nat.lib().tps_linear(w.data_ptr(), n, k, k, x.data_ptr(), B, x.shape[0],
+                                       x.shape[1], self.ws.data_ptr(), s, st), "tps_linear")
+        stats.add("linear")
+        base = self.ws.data_ptr()
+        return [base + i * B * n * 4 for i in range(s)]
+
+    @staticmethod
+    def _arr(ptrs):
+        # host pointer list, consumed (copied into a by-value kernel parameter) by the call
+        return nat.ptr_array(ptrs)
+
+    # ------------------------------------------------------------ program ---
+    def program(self, B: int, st: int, stats: LaunchStats | None = None):
+        """Issue one decode step for bucket B on stream `st`; yields at peer waits."""
+        stats = stats if stats is not None else LaunchStats()
+        lib = nat.lib()
+        g = self.geom
+        H, D, L = g.hidden, g.head_dim, g.num_layers
+        W = self.w
+        sl = self.slots
+        rs = self.row_slot[B].data_ptr()
+        pos = sl.pos.data_ptr()
+        hist = sl.history.data_ptr()
+        eps = ctypes.c_float(g.rms_eps)
+
+        nat.check(lib.tps_embed(rs, pos, hist, sl.max_len, W.tensor_ptr(-1, "embed"), H, B,
+                                self.resid.data_ptr(), st), "tps_embed")
+        stats.add("embed")
+        nat.check(lib.tps_add_norm(self.resid.data_ptr(), None, 0, None, W.tensor_ptr(0, "ln1"), eps,
+                                   H, B, self.xn.data_ptr(), H, st), "tps_add_norm")
+        stats.add("add_norm")
+        nsplit = lib.tps_attn_splits(B, self.nkv, sl.max_pages)
+        for l in range(L):
+            srcs = self._linear(st, stats, W[(l, "w_qkv")], self.xn, B)
+            kc, vc = self.kv.layer_ptrs(l)
+            bias = W.tensor_ptr(l, "b_qkv") if g.qkv_bias else None
+            nat.check(lib.tps_qkv_rope_append(self._arr(srcs), len(srcs), bias, rs, pos,
+                                              sl.page_table.data_ptr(), sl.max_pages,
+                                              self.cos.data_ptr(), self.sin.data_ptr(), B, self.nq,
+                                              self.nkv, D, PAGE, self.q.data_ptr(), kc, vc, st),
+                      "tps_qkv_rope_append")
+            stats.add("qkv_rope_append")
+            nat.check(lib.tps_paged_attention(self.q.data_ptr(), kc, vc, rs, pos, sl.page_table.data_ptr(),
+                                              sl.max_pages, B, self.nq, self.nkv, D, nsplit,
+                                              self.att_m.data_ptr(), self.att_l.data_ptr(),
+                                              self.att_o.data_ptr(), self.attn.data_ptr(), st),
+                      "tps_paged_attention")
+            stats.add("paged_attention", 2)
+            srcs = self._linear(st, stats, W[(l, "w_o")], self.attn, B)
+            yield from self._allreduce_norm(st, stats, 2 * l, srcs, B, W.tensor_ptr(l, "ln2"))
+            srcs = self._linear(st, stats, W[(l, "w_gu")], self.xn, B)
+            nat.check(lib.tps_silu_mul(self._arr(srcs), len(srcs), B, self.F, self.act.data_ptr(), self.F, st),
+                      "tps_silu_mul")
+            stats.add("silu_mul")
+            srcs = self._linear(st, stats, W[(l, "w_d")], self.act, B)
+            nxt = W.tensor_ptr(l + 1, "ln1") if l + 1 < L else W.tensor_ptr(-1, "ln_f")
+            yield from self._allreduce_norm(st, stats, 2 * l + 1, srcs, B, nxt)
+        srcs = self._linear(st, stats, W[(-1, "lm_head")], self.xn, B)
+        self._last_lm_srcs = (srcs, B)
+        nch = argmax_chunks(B)
+        cm = self.comm
+        if cm is None:
+            nat.check(lib.tps_argmax_stage1(self._arr(srcs), len(srcs), B, self.V, self.shard.vocab[0], nch,
+                                            self.local_cand.data_ptr(), None, 0, None, st), "tps_argmax_stage1")
+            stats.add("argmax_stage1")
+            cands = [self.local_cand.data_ptr()]
+            wait = None
+        else:
+            ph = 2 * L
+            sigs = [p + ph * 8 for p in cm.peer_ctr]
+            nat.check(lib.tps_argmax_stage1(self._arr(srcs), len(srcs), B, self.V, self.shard.vocab[0], nch,
+                                            cm.cand.data_ptr(), self._arr(sigs), len(sigs),
+                                            cm.done.data_ptr() + ph * 4, st), "tps_argmax_stage1")
+            stats.add("argmax_stage1")
+            yield
+            cands = list(cm.peer_cand)
+            wait = nat.wait_spec(cm.ctr.data_ptr() + ph * 8, cm.epoch.data_ptr(), cm.tp, 0)
+        nat.check(lib.tps_argmax_finalize(self._arr(cands), len(cands), nch, wait, B, rs, pos,
+                                          self.prompt_len.data_ptr(), hist, sl.max_len,
+                                          self.out_tok.data_ptr(), st), "tps_argmax_finalize")
+        stats.add("argmax_finalize")
+        if cm is not None:
+            nat.check(lib.tps_epoch_advance(cm.epoch.data_ptr(), st), "tps_epoch_advance")
+            stats.add("epoch_advance")
+
+    def _allreduce_norm(self, st, stats, phase: int, srcs: list[int], B: int, norm_w: int):
+        lib = nat.lib()
+        g = self.geom
+        H = g.hidden
+        eps = ctypes.c_float(g.rms_eps)
+        cm = self.comm
+        if cm is None:
+            nat.check(lib.tps_add_norm(self.resid.data_ptr(), self._arr(srcs), len(srcs), None, norm_w, eps, H,
+                                       B, self.xn.data_ptr(), H, st), "tps_add_norm")
+            stats.add("add_norm")
+            return
+        par = phase % 2
+        dsts = [cm.recv_slot(base, par, self.rank) for base in cm.peer_recv]
+        sigs = [p + phase * 8 for p in cm.peer_ctr]
+        nat.check(lib.tps_reduce_push(self._arr(srcs), len(srcs), self._arr(dsts), len(dsts), B * H,
+                                      self._arr(sigs), len(sigs), cm.done.data_ptr() + phase * 4, st),
+                  "tps_reduce_push")
+        stats.add("reduce_push")
+        yield
+        mine = [cm.recv_slot(cm.recv.data_ptr(), par, r) for r in range(cm.tp)]
+        wait = nat.wait_spec(cm.ctr.data_ptr() + phase * 8, cm.epoch.data_ptr(), cm.tp, 0)
+        nat.check(lib.tps_add_norm(self.resid.data_ptr(), self._arr(mine), len(mine), wait, norm_w, eps, H, B,
+                                   self.xn.data_ptr(), H, st), "tps_add_norm")
+        stats.add("add_norm")
+
+    # ----------------------------------------------------------- batching ---
+    def set_rows(self, B: int, slots: list[int]) -> None:
+        """Bind batch rows of bucket B to sample slots (padding rows -> -1)."""
+        assert len(slots) <= B
+        host = torch.full((B,), -1, dtype=torch.int32)
+        host[:len(slots)] = torch.tensor(slots, dtype=torch.int32)
+        self.row_slot[B].copy_(host.pin_memory() if self.device.type == "cuda" else host,
+                               non_blocking=True)
+
+
+def run_programs(programs) -> None:
+    """Advance per-rank step programs in lock-step (single-GPU virtual group)."""
+    live = list(programs)
+    while live:
+        nxt = []
+        for p in live:
+            try:
+                next(p)
+                nxt.append(p)
+            except StopIteration:
+                pass
+        live = nxt
+
+
+class GroupRunner:
+    """Drives the executors of one DP group (1 rank, or all ranks of a virtual TP group)."""
+
+    def __init__(self, executors: list[InferExecutor], use_graphs: bool = True):
+        self.ex = executors
+        self.use_graphs = use_graphs
+        self.graphs: dict[int, torch.cuda.CUDAGraph] = {}
+        self.stats: dict[int, LaunchStats] = {}
+        self.stream = torch.cuda.current_stream(executors[0].device)
+
+    def set_rows(self, B: int, slots: list[int]) -> None:
+        for e in self.ex:
+            e.set_rows(B, slots)
+
+    def _issue(self, B: int, st: int) -> LaunchStats:
+        stats = LaunchStats()
+        run_programs([e.program(B, st, stats) for e in self.ex])
+        return stats
+
+    def capture(self, B: int) -> None:
+        if B in self.graphs:
+            return
+        g = torch.cuda.CUDAGraph()
+        # state-preserving warm-up is not possible (a step mutates positions), so
+        # capture directly; kernels were already configured by an eager step.
+        with torch.cuda.graph(g):
+            st = torch.cuda.current_stream().cuda_stream
+            self.stats[B] = self._issue(B, st)
+        self.graphs[B] = g
+
+    def step(self, B: int, n: int = 1) -> None:
+        """Run n decode rounds for bucket B (rows bound by set_rows)."""
+        if self.use_graphs and B in self.graphs:
+            g = self.graphs[B]
+            for _ in range(n):
+                g.replay()
+            return
+        st = torch.cuda.current_stream().cuda_stream
+        for _ in range(n):
+            self.stats[B] = self._issue(B, st)
+
+    def kernels_per_step(self, B: int) -> int:
+        return self.stats[B].kernels if B in self.stats else 0

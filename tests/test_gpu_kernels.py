@@ -1,0 +1,158 @@
+"""Kernel-level numerics of libtpshift_b200 on a B200 against plain PyTorch fp32 references.
+
+Tolerances: projections accumulate bf16 x bf16 in fp32 on the tensor cores, so
+they are compared with a torch fp32 matmul of the same bf16 inputs at
+|d| <= 1e-3 * sqrt(K) * max|ref| relative slack; copies are bit-exact.
+"""
+
+import math
+
+import pytest
+import torch
+
+from paper_2605_23945_b200 import _native as nat
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _init():
+    nat.init_device(0)
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+@pytest.mark.parametrize("n,k,b", [
+    (128, 64, 1), (384, 256, 5), (4736, 3584, 16), (1000, 104, 17), (256, 4096, 64),
+    (3584, 18944, 33), (768, 512, 100), (512, 1024, 256), (8192, 256, 2)])
+def test_linear_matches_fp32(n, k, b):
+    torch.manual_seed(n + k + b)
+    w = (torch.randn(n, k, device="cuda") * 0.05).bfloat16()
+    x = torch.randn(b + 3, k, device="cuda").bfloat16()
+    ref = x[:b].float() @ w.float().T
+    lib = nat.lib()
+    for splits in sorted({1, lib.tps_linear_splits(n, k, b), min(3, (k + 63) // 64)}):
+        out = torch.full((splits, b, n), float("nan"), device="cuda")
+        nat.check(lib.tps_linear(w.data_ptr(), n, k, k, x.data_ptr(), b, x.shape[0], k, out.data_ptr(),
+                                 splits, _stream()))
+        got = out.sum(0)
+        torch.cuda.synchronize()
+        tol = 2e-3 * math.sqrt(k) * 0.05 * 4 + 1e-4
+        assert torch.isfinite(got).all()
+        assert (got - ref).abs().max().item() <= tol, (splits, (got - ref).abs().max().item())
+
+
+def test_linear_rejects_bad_args():
+    lib = nat.lib()
+    from paper_2605_23945_b200.errors import ConfigError
+    with pytest.raises(ConfigError):
+        nat.check(lib.tps_linear(0, 128, 64, 64, 0, 1, 1, 64, 0, 1, _stream()))
+    w = torch.zeros(128, 64, device="cuda", dtype=torch.bfloat16)
+    out = torch.zeros(1, 300, 128, device="cuda")
+    with pytest.raises(ConfigError):  # b > 256
+        nat.check(lib.tps_linear(w.data_ptr(), 128, 64, 64, w.data_ptr(), 300, 300, 64, out.data_ptr(), 1,
+                                 _stream()))
+
+
+def _ref_attention(q, kc, vc, page_table, pos, G):
+    """q [B, nq, D]; kc/vc [pages, nkv, 64, D]; returns [B, nq, D] fp32."""
+    B, nq, D = q.shape
+    out = torch.zeros(B, nq, D)
+    for b in range(B):
+        ctx = pos[b] + 1
+        pages = page_table[b][: (ctx + 63) // 64]
+        K = torch.cat([kc[p] for p in pages], dim=1)[:, :ctx].float()  # [nkv, T, D]
+        V = torch.cat([vc[p] for p in pages], dim=1)[:, :ctx].float()
+        for h in range(nq):
+            kvh = h // G
+            s = (K[kvh] @ q[b, h].float()) / math.sqrt(D)
+            p = torch.softmax(s, dim=0)
+            out[b, h] = p @ V[kvh]
+    return out
+
+
+@pytest.mark.parametrize("D,nq,nkv,ctxs", [
+    (128, 7, 1, [1, 64, 65, 300]), (128, 28, 4, [5000, 17]), (64, 4, 2, [130, 1]),
+    (128, 4, 1, [2049]), (128, 16, 1, [100, 1000])])
+def test_paged_attention_matches_fp32(D, nq, nkv, ctxs):
+    torch.manual_seed(D + nq + len(ctxs))
+    B = len(ctxs)
+    max_pages = max((c + 63) // 64 for c in ctxs) + 1
+    num_pages = B * max_pages + 3
+    kc = torch.randn(num_pages, nkv, 64, D, device="cuda").bfloat16()
+    vc = torch.randn(num_pages, nkv, 64, D, device="cuda").bfloat16()
+    perm = torch.randperm(num_pages)[: B * max_pages].view(B, max_pages).int()
+    page_table = perm.cuda()
+    row_slot = torch.arange(B, dtype=torch.int32, device="cuda")
+    pos = torch.tensor([c - 1 for c in ctxs], dtype=torch.int32, device="cuda")
+    q = torch.randn(B, nq, D, device="cuda").bfloat16()
+    lib = nat.lib()
+    for nsplit in (1, lib.tps_attn_splits(B, nkv, max_pages), 7):
+        pm = torch.empty(B * nq * nsplit, device="cuda")
+        pl = torch.empty_like(pm)
+        po = torch.empty(B * nq * nsplit * D, device="cuda")
+        out = torch.empty(B, nq, D, device="cuda", dtype=torch.bfloat16)
+        nat.check(lib.tps_paged_attention(q.data_ptr(), kc.data_ptr(), vc.data_ptr(), row_slot.data_ptr(),
+                                          pos.data_ptr(), page_table.data_ptr(), max_pages, B, nq, nkv, D,
+                                          nsplit, pm.data_ptr(), pl.data_ptr(), po.data_ptr(), out.data_ptr(),
+                                          _stream()))
+        torch.cuda.synchronize()
+        ref = _ref_attention(q.cpu(), kc.cpu(), vc.cpu(), perm.tolist(), [c - 1 for c in ctxs], nq // nkv)
+        err = (out.float().cpu() - ref).abs().max().item()
+        # P is rounded to bf16 before the PV product; outputs are O(1)
+        assert err < 2e-2, (nsplit, err)
+
+
+def test_padding_rows_are_inert():
+    D, nq, nkv = 128, 4, 1
+    kc = torch.randn(4, nkv, 64, D, device="cuda").bfloat16()
+    vc = torch.randn_like(kc)
+    page_table = torch.zeros(1, 2, dtype=torch.int32, device="cuda")
+    row_slot = torch.tensor([-1, 0], dtype=torch.int32, device="cuda")
+    pos = torch.tensor([10], dtype=torch.int32, device="cuda")
+    q = torch.randn(2, nq, D, device="cuda").bfloat16()
+    pm = torch.empty(2 * nq * 3, device="cuda")
+    pl, po = torch.empty_like(pm), torch.empty(2 * nq * 3 * D, device="cuda")
+    out = torch.full((2, nq, D), 7.0, device="cuda", dtype=torch.bfloat16)
+    nat.check(nat.lib().tps_paged_attention(q.data_ptr(), kc.data_ptr(), vc.data_ptr(), row_slot.data_ptr(),
+                                            pos.data_ptr(), page_table.data_ptr(), 2, 2, nq, nkv, D, 3,
+                                            pm.data_ptr(), pl.data_ptr(), po.data_ptr(), out.data_ptr(),
+                                            _stream()))
+    torch.cuda.synchronize()
+    assert (out[0] == 0).all()
+    assert torch.isfinite(out[1].float()).all()
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_copy_items_bit_exact(mode):
+    torch.manual_seed(mode)
+    src = torch.randint(0, 256, (3 << 20,), dtype=torch.uint8, device="cuda")
+    dst = torch.zeros_like(src)
+    # ragged items: 16 B multiples, a large 1 MiB one, and an odd-size tail (LSU only)
+    spec = [(0, 4096, 16384), (1600000, 1 << 20, 65536 - 16), (2 << 20, 1200000, 1 << 20)]
+    if mode == 0:
+        spec.append((12345, 2900000, 77))  # unaligned odd-size item: LSU byte tail
+    items = torch.zeros((len(spec), 4), dtype=torch.int64)
+    for i, (so, do, nb) in enumerate(spec):
+        items[i, 0] = src.data_ptr() + so
+        items[i, 1] = dst.data_ptr() + do
+        items[i, 2] = nb
+    items = items.cuda()
+    nat.check(nat.lib().tps_copy_items(items.data_ptr(), len(spec), mode, 0, _stream()))
+    torch.cuda.synchronize()
+    want = torch.zeros_like(src)
+    for so, do, nb in spec:
+        want[do:do + nb] = src[so:so + nb]
+    assert torch.equal(dst, want)
+
+
+def test_barrier_counters_virtual():
+    ctr = torch.zeros(4, dtype=torch.int64, device="cuda")
+    peers = nat.ptr_array([ctr.data_ptr() + 8 * i for i in range(1, 4)])
+    # this "rank" signals three peers and waits on its own counter, which we pre-arm
+    ctr[0] = 1
+    nat.check(nat.lib().tps_barrier(peers, 3, ctr.data_ptr(), 1, _stream()))
+    torch.cuda.synchronize()
+    assert ctr.tolist() == [1, 1, 1, 1]
