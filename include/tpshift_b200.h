@@ -61,8 +61,11 @@ typedef struct tps_copy_item {
 const char* tps_version(void);
 /* Last error text of the calling thread (valid until the next failing call). */
 const char* tps_last_error(void);
-/* Bind the calling thread to `device`, report its SM count; checks sm_100. */
+/* Bind the calling thread to `device`, report its SM count; checks sm_100 and
+ * configures kernel attributes (call before any stream capture). */
 int tps_init(int device, int* sm_count);
+/* Programmatic dependent launch for decode-step kernels (default on). */
+void tps_set_pdl(int on);
 
 /* ------------------------------------------------ decode step (seam 1) --- */
 /* Split-K count tps_linear will use for an [n x k] weight at batch b. */
@@ -80,23 +83,27 @@ int tps_linear(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, 
 int tps_embed(const int* row_slot, const int* pos_by_slot, const int* history, int hist_ld,
               const void* table, int H, int B, float* resid, void* stream);
 
-/* resid[b] += sum_i srcs[i][b] (list order), then out[b] = bf16(RMSNorm(resid[b]) * w).
- * srcs: host array of nsrc device pointers, each fp32 [B][H]. This is the
- * consumer of the O/down projections and of the TP allreduce receive slots. */
-int tps_add_norm(float* resid, const float* const* srcs, int nsrc, const tps_wait* wait, const void* w,
-                 float eps, int H, int B, void* out, int ldo, void* stream);
+/* Strided source convention (src, nsrc, src_stride): nsrc fp32 buffers at
+ * src + i*src_stride (elements), summed in index order -- the split-K partials
+ * of one projection, or one receive slot per TP rank (rank order). */
+
+/* resid[b] += sum_i src_i[b], then out[b] = bf16(RMSNorm(resid[b]) * w); each
+ * src_i is fp32 [B][H]. Consumer of the O/down projections and of the TP
+ * allreduce receive slots; waits on `wait` first (NULL = no wait). */
+int tps_add_norm(float* resid, const float* src, int nsrc, int64_t src_stride, const tps_wait* wait,
+                 const void* w, float eps, int H, int B, void* out, int ldo, void* stream);
 
 /* One-shot TP allreduce, push half (reference comm term, tpshift/latency.py:125-126):
  * r = sum_i srcs[i] (fp32, n elements), stored to every dsts[d] (this rank's slot
  * in each TP peer's receive area, NVLink P2P stores), then +1 on every sig_ctrs[]
  * (issued once per launch by the last CTA; `done` is that launch site's CTA counter). */
-int tps_reduce_push(const float* const* srcs, int nsrc, float* const* dsts, int ndst, int64_t n,
+int tps_reduce_push(const float* src, int nsrc, int64_t src_stride, float* const* dsts, int ndst, int64_t n,
                     uint64_t* const* sig_ctrs, int nsig, unsigned int* done, void* stream);
 
 /* QKV: sum split partials [s][B][(nq+2nkv)*D] + bias, rotate-half RoPE (fp32
  * cos/sin tables [pos][D/2]), q -> bf16 [B][nq][D], k/v appended at each
  * row's position into the paged cache [page][nkv][64][D]. */
-int tps_qkv_rope_append(const float* const* srcs, int nsrc, const void* bias, const int* row_slot,
+int tps_qkv_rope_append(const float* src, int nsrc, int64_t src_stride, const void* bias, const int* row_slot,
                         const int* pos_by_slot, const int* page_table, int max_pages, const float* cos_t,
                         const float* sin_t, int B, int nq, int nkv, int D, int page_size, void* q_out,
                         void* k_cache, void* v_cache, void* stream);
@@ -104,21 +111,25 @@ int tps_qkv_rope_append(const float* const* srcs, int nsrc, const void* bias, co
 /* Split count for tps_paged_attention. */
 int tps_attn_splits(int B, int nkv, int max_pages);
 
-/* Paged GQA decode attention over ctx = pos+1 tokens per row, split-KV with a
- * log-sum-exp merge; out bf16 [B][nq][D]. part_m/part_l: fp32 [B][nq][nsplit],
- * part_o: fp32 [B][nq][nsplit][D] scratch. KV term of tpshift/latency.py:123. */
+/* Paged GQA decode attention over ctx = pos+1 tokens per row, split-KV; the last
+ * CTA of each (row, kv head) merges the splits (log-sum-exp) and writes out bf16
+ * [B][nq][D]. part_m/part_l: fp32 [B][nq][nsplit], part_o: fp32 [B][nq][nsplit][D]
+ * scratch; merge_ctr: zero-initialised uint32 [B][nkv] (self re-arming). KV term
+ * of tpshift/latency.py:123. */
 int tps_paged_attention(const void* q, const void* k_cache, const void* v_cache, const int* row_slot,
                         const int* pos_by_slot, const int* page_table, int max_pages, int B, int nq,
-                        int nkv, int D, int nsplit, float* part_m, float* part_l, float* part_o, void* out,
-                        void* stream);
+                        int nkv, int D, int nsplit, float* part_m, float* part_l, float* part_o,
+                        unsigned int* merge_ctr, void* out, void* stream);
 
 /* act[b][f] = bf16(silu(g) * u) from split partials [s][B][2F] = [gate | up]. */
-int tps_silu_mul(const float* const* srcs, int nsrc, int B, int F, void* out, int ldo, void* stream);
+int tps_silu_mul(const float* src, int nsrc, int64_t src_stride, int B, int F, void* out, int ldo,
+                 void* stream);
 
 /* Vocab-parallel greedy argmax, stage 1: per-(row, chunk) (max, smallest global
  * index) candidates from LM-head split partials [s][B][V]; signals sig_ctrs. */
-int tps_argmax_stage1(const float* const* srcs, int nsrc, int B, int V, int vocab_offset, int nchunk,
-                      void* cand, uint64_t* const* sig_ctrs, int nsig, unsigned int* done, void* stream);
+int tps_argmax_stage1(const float* src, int nsrc, int64_t src_stride, int B, int V, int vocab_offset,
+                      int nchunk, void* cand, uint64_t* const* sig_ctrs, int nsig, unsigned int* done,
+                      void* stream);
 
 /* Stage 2: reduce candidates of all TP ranks (list = rank order), append the
  * token to history[slot][pos+1] unless pos+1 is still inside the prompt
@@ -130,8 +141,8 @@ int tps_argmax_finalize(const void* const* cands, int ncand, int nchunk, const t
 /* *epoch += 1 (end of a decode step; drives graph-replay-safe counter waits). */
 int tps_epoch_advance(uint64_t* epoch, void* stream);
 
-/* out[i] = sum_s srcs[s][i] for i < n (fp32). */
-int tps_sum_partials(const float* const* srcs, int nsrc, int64_t n, float* out, void* stream);
+/* out[i] = sum_s src_s[i] for i < n (fp32). */
+int tps_sum_partials(const float* src, int nsrc, int64_t src_stride, int64_t n, float* out, void* stream);
 
 /* --------------------------------------------------- switch (seam 2) ----- */
 /* Execute n copy items (device array of tps_copy_item). mode 0 = LSU vector

@@ -20,23 +20,24 @@ int fail(int code, const std::string& msg) {
 }
 
 // launchers (defined in the kernel translation units)
+void set_pdl(bool on);
 int linear_splits(int64_t n, int64_t k, int64_t b);
 int linear(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
            int64_t ldx, float* out, int splits, cudaStream_t stream);
 int embed(const int*, const int*, const int*, int, const void*, int, int, float*, cudaStream_t);
-int add_norm(float*, const SrcList&, const WaitSpec&, const void*, float, int, int, void*, int, cudaStream_t);
-int reduce_push(const SrcList&, const DstList&, int64_t, const SignalSpec&, cudaStream_t);
-int qkv_rope_append(const SrcList&, const void*, const int*, const int*, const int*, int, const float*,
-                    const float*, int, int, int, int, int, void*, void*, void*, cudaStream_t);
-int silu_mul(const SrcList&, int, int, void*, int, cudaStream_t);
-int argmax_stage1(const SrcList&, int, int, int, int, void*, const SignalSpec&, cudaStream_t);
+int add_norm(float*, const Src&, const WaitSpec&, const void*, float, int, int, void*, int, cudaStream_t);
+int reduce_push(const Src&, const DstList&, long long, const SignalSpec&, cudaStream_t);
+int qkv_rope_append(const Src&, const void*, const int*, const int*, const int*, int, const float*, const float*,
+                    int, int, int, int, int, void*, void*, void*, cudaStream_t);
+int silu_mul(const Src&, int, int, void*, int, cudaStream_t);
+int argmax_stage1(const Src&, int, int, int, int, void*, const SignalSpec&, cudaStream_t);
 int argmax_finalize(const CandList&, int, const WaitSpec&, int, const int*, int*, const int*, int*, int, int*,
                     cudaStream_t);
 int epoch_advance(uint64_t*, cudaStream_t);
-int sum_src(const SrcList&, int64_t, float*, cudaStream_t);
+int sum_src(const Src&, long long, float*, cudaStream_t);
 int attn_splits(int B, int nkv, int max_pages);
-int paged_attention(const void*, const void*, const void*, const int*, const int*, const int*, int, int, int,
-                    int, int, int, float*, float*, float*, void*, cudaStream_t);
+int paged_attention(const void*, const void*, const void*, const int*, const int*, const int*, int, int, int, int,
+                    int, int, float*, float*, float*, unsigned int*, void*, cudaStream_t);
 int copy_items(const void*, int, int, int, cudaStream_t);
 int configure_gemm();
 int configure_attention();
@@ -46,14 +47,12 @@ int ipc_get_handle(const void*, void*, int64_t*);
 int ipc_open(const void*, void**);
 int ipc_close(void*);
 
-static int make_src(const float* const* srcs, int nsrc, SrcList* out) {
-  if (nsrc < 0 || nsrc > kMaxSrc) return fail(kInvalid, "source list longer than 64 entries");
-  if (nsrc > 0 && !srcs) return fail(kInvalid, "null source list");
-  out->n = nsrc;
-  for (int i = 0; i < nsrc; ++i) {
-    if (!srcs[i]) return fail(kInvalid, "null source pointer");
-    out->p[i] = srcs[i];
-  }
+static int make_src(const float* base, int n, int64_t stride, Src* out) {
+  if (n < 0 || n > 1024) return fail(kInvalid, "source count must be in [0, 1024]");
+  if (n > 0 && !base) return fail(kInvalid, "null source base");
+  out->base = base;
+  out->n = n;
+  out->stride = stride;
   return kOk;
 }
 
@@ -85,7 +84,7 @@ using namespace tps;
 
 extern "C" {
 
-const char* tps_version(void) { return "tpshift_b200 1.0 (sm_100a; tcgen05 GEMM, paged GQA decode, P2P switch)"; }
+const char* tps_version(void) { return "tpshift_b200 1.1 (sm_100a; tcgen05 GEMM, paged GQA decode, P2P switch, PDL)"; }
 
 const char* tps_last_error(void) { return g_last_error.c_str(); }
 
@@ -104,6 +103,8 @@ int tps_init(int device, int* sm_count) {
   return rc;
 }
 
+void tps_set_pdl(int on) { set_pdl(on != 0); }
+
 int tps_linear_splits(int64_t n, int64_t k, int64_t b) { return linear_splits(n, k, b); }
 
 int tps_linear(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
@@ -117,19 +118,19 @@ int tps_embed(const int* row_slot, const int* pos_by_slot, const int* history, i
   return embed(row_slot, pos_by_slot, history, hist_ld, table, H, B, resid, S(stream));
 }
 
-int tps_add_norm(float* resid, const float* const* srcs, int nsrc, const tps_wait* wait, const void* w,
-                 float eps, int H, int B, void* out, int ldo, void* stream) {
+int tps_add_norm(float* resid, const float* src, int nsrc, int64_t src_stride, const tps_wait* wait,
+                 const void* w, float eps, int H, int B, void* out, int ldo, void* stream) {
   TPS_CHECK_ARG(resid && w && out, "add_norm: null pointer");
-  SrcList sl;
-  int rc = make_src(srcs, nsrc, &sl);
+  Src s;
+  int rc = make_src(src, nsrc, src_stride, &s);
   if (rc) return rc;
-  return add_norm(resid, sl, make_wait(wait), w, eps, H, B, out, ldo, S(stream));
+  return add_norm(resid, s, make_wait(wait), w, eps, H, B, out, ldo, S(stream));
 }
 
-int tps_reduce_push(const float* const* srcs, int nsrc, float* const* dsts, int ndst, int64_t n,
+int tps_reduce_push(const float* src, int nsrc, int64_t src_stride, float* const* dsts, int ndst, int64_t n,
                     uint64_t* const* sig_ctrs, int nsig, unsigned int* done, void* stream) {
-  SrcList sl;
-  int rc = make_src(srcs, nsrc, &sl);
+  Src s;
+  int rc = make_src(src, nsrc, src_stride, &s);
   if (rc) return rc;
   TPS_CHECK_ARG(ndst >= 1 && ndst <= kMaxPeers && dsts, "reduce_push: 1..8 destinations");
   DstList dl;
@@ -138,52 +139,52 @@ int tps_reduce_push(const float* const* srcs, int nsrc, float* const* dsts, int 
   SignalSpec sg;
   rc = make_sig(sig_ctrs, nsig, done, &sg);
   if (rc) return rc;
-  return reduce_push(sl, dl, n, sg, S(stream));
+  return reduce_push(s, dl, n, sg, S(stream));
 }
 
-int tps_qkv_rope_append(const float* const* srcs, int nsrc, const void* bias, const int* row_slot,
+int tps_qkv_rope_append(const float* src, int nsrc, int64_t src_stride, const void* bias, const int* row_slot,
                         const int* pos_by_slot, const int* page_table, int max_pages, const float* cos_t,
                         const float* sin_t, int B, int nq, int nkv, int D, int page_size, void* q_out,
                         void* k_cache, void* v_cache, void* stream) {
   TPS_CHECK_ARG(page_size == 64, "qkv_rope_append: page_size must be 64");
   TPS_CHECK_ARG(row_slot && pos_by_slot && page_table && cos_t && sin_t && q_out && k_cache && v_cache,
                 "qkv_rope_append: null pointer");
-  SrcList sl;
-  int rc = make_src(srcs, nsrc, &sl);
+  Src s;
+  int rc = make_src(src, nsrc, src_stride, &s);
   if (rc) return rc;
-  return qkv_rope_append(sl, bias, row_slot, pos_by_slot, page_table, max_pages, cos_t, sin_t, B, nq, nkv, D,
+  return qkv_rope_append(s, bias, row_slot, pos_by_slot, page_table, max_pages, cos_t, sin_t, B, nq, nkv, D,
                          page_size, q_out, k_cache, v_cache, S(stream));
 }
 
 int tps_attn_splits(int B, int nkv, int max_pages) { return attn_splits(B, nkv, max_pages); }
 
 int tps_paged_attention(const void* q, const void* k_cache, const void* v_cache, const int* row_slot,
-                        const int* pos_by_slot, const int* page_table, int max_pages, int B, int nq, int nkv,
-                        int D, int nsplit, float* part_m, float* part_l, float* part_o, void* out,
-                        void* stream) {
-  TPS_CHECK_ARG(q && k_cache && v_cache && row_slot && pos_by_slot && page_table && part_m && part_l &&
-                    part_o && out,
+                        const int* pos_by_slot, const int* page_table, int max_pages, int B, int nq, int nkv, int D,
+                        int nsplit, float* part_m, float* part_l, float* part_o, unsigned int* merge_ctr,
+                        void* out, void* stream) {
+  TPS_CHECK_ARG(q && k_cache && v_cache && row_slot && pos_by_slot && page_table && part_m && part_l && part_o &&
+                    merge_ctr && out,
                 "paged_attention: null pointer");
-  return paged_attention(q, k_cache, v_cache, row_slot, pos_by_slot, page_table, max_pages, B, nq, nkv, D,
-                         nsplit, part_m, part_l, part_o, out, S(stream));
+  return paged_attention(q, k_cache, v_cache, row_slot, pos_by_slot, page_table, max_pages, B, nq, nkv, D, nsplit,
+                         part_m, part_l, part_o, merge_ctr, out, S(stream));
 }
 
-int tps_silu_mul(const float* const* srcs, int nsrc, int B, int F, void* out, int ldo, void* stream) {
-  SrcList sl;
-  int rc = make_src(srcs, nsrc, &sl);
+int tps_silu_mul(const float* src, int nsrc, int64_t src_stride, int B, int F, void* out, int ldo, void* stream) {
+  Src s;
+  int rc = make_src(src, nsrc, src_stride, &s);
   if (rc) return rc;
-  return silu_mul(sl, B, F, out, ldo, S(stream));
+  return silu_mul(s, B, F, out, ldo, S(stream));
 }
 
-int tps_argmax_stage1(const float* const* srcs, int nsrc, int B, int V, int vocab_offset, int nchunk,
+int tps_argmax_stage1(const float* src, int nsrc, int64_t src_stride, int B, int V, int vocab_offset, int nchunk,
                       void* cand, uint64_t* const* sig_ctrs, int nsig, unsigned int* done, void* stream) {
-  SrcList sl;
-  int rc = make_src(srcs, nsrc, &sl);
+  Src s;
+  int rc = make_src(src, nsrc, src_stride, &s);
   if (rc) return rc;
   SignalSpec sg;
   rc = make_sig(sig_ctrs, nsig, done, &sg);
   if (rc) return rc;
-  return argmax_stage1(sl, B, V, vocab_offset, nchunk, cand, sg, S(stream));
+  return argmax_stage1(s, B, V, vocab_offset, nchunk, cand, sg, S(stream));
 }
 
 int tps_argmax_finalize(const void* const* cands, int ncand, int nchunk, const tps_wait* wait, int B,
@@ -202,11 +203,11 @@ int tps_epoch_advance(uint64_t* epoch, void* stream) {
   return epoch_advance(epoch, S(stream));
 }
 
-int tps_sum_partials(const float* const* srcs, int nsrc, int64_t n, float* out, void* stream) {
-  SrcList sl;
-  int rc = make_src(srcs, nsrc, &sl);
+int tps_sum_partials(const float* src, int nsrc, int64_t src_stride, int64_t n, float* out, void* stream) {
+  Src s;
+  int rc = make_src(src, nsrc, src_stride, &s);
   if (rc) return rc;
-  return sum_src(sl, n, out, S(stream));
+  return sum_src(s, n, out, S(stream));
 }
 
 int tps_copy_items(const tps_copy_item* items, int n, int mode, int grid, void* stream) {

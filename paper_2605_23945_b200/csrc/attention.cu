@@ -1,4 +1,4 @@
-// Paged GQA decode attention (flash-decoding split-KV), sm_100a.
+// Paged GQA decode attention (flash-decoding split-KV with in-kernel merge), sm_100a.
 //
 // The reference prices this work as the KV term of oracle_decode_latency,
 // t * kv_bytes_per_token / (tp * hbm_bw) (tpshift/latency.py:123): one pass over
@@ -7,20 +7,25 @@
 //   * KV layout per layer is [page][kv_head][64 tokens][D] bf16, so one
 //     (page, kv-head) slice is a contiguous 16 KB chunk (D=128). The same chunk
 //     is the unit the Switch Executor migrates.
-//   * grid = (kv_head, row, split): long contexts are split across CTAs so a
-//     tail batch of 1 still spreads over the 148 SMs; splits are merged by
-//     attn_combine_kernel with the usual max-rescaled log-sum-exp.
+//   * grid = (kv_head, row, split): long contexts are split across CTAs (>= 2
+//     pages each) so a tail batch of 1 still spreads over the 148 SMs; the
+//     last CTA of a (row, kv_head) to finish merges the splits' (max, sum, O)
+//     states with the max-rescaled log-sum-exp and writes the bf16 output --
+//     no separate combine launch.
 //   * 3-stage cp.async ring into an XOR-swizzled smem tile (conflict-free
 //     fragment loads); the G query heads sharing a KV head form the 16-row
 //     MMA operand, so QK^T and PV run on the tensor pipe and the CTA only
 //     streams bytes.
 #include "common.cuh"
+#include "decode_ops.cuh"
 
 namespace tps {
 
 constexpr int kPage = 64;
 constexpr int kAttnThreads = 128;
 constexpr int kAttnStages = 3;
+constexpr int kMinPagesPerSplit = 2;
+constexpr int kMaxAttnSplits = 128;
 
 __device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(
@@ -54,26 +59,35 @@ template <int D>
 __global__ void __launch_bounds__(kAttnThreads) paged_attn_kernel(
     const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k_cache,
     const __nv_bfloat16* __restrict__ v_cache, const int* __restrict__ row_slot,
-    const int* __restrict__ pos_by_slot, const int* __restrict__ page_table, int max_pages, int nq,
-    int nkv, int G, int nsplit, float scale_log2, float* __restrict__ part_m, float* __restrict__ part_l,
-    float* __restrict__ part_o) {
-  constexpr int CPR = D / 8;                 // 16-byte chunks per token row
-  constexpr int TILE = kPage * D;            // elements per K (or V) page slice
+    const int* __restrict__ pos_by_slot, const int* __restrict__ page_table, int max_pages, int nq, int nkv,
+    int G, int nsplit, float scale_log2, float* __restrict__ part_m, float* __restrict__ part_l,
+    float* __restrict__ part_o, unsigned int* __restrict__ merge_ctr, __nv_bfloat16* __restrict__ out) {
+  constexpr int CPR = D / 8;       // 16-byte chunks per token row
+  constexpr int TILE = kPage * D;  // elements per K (or V) page slice
   extern __shared__ __align__(128) uint8_t smem_raw[];
   __nv_bfloat16* sk = reinterpret_cast<__nv_bfloat16*>(smem_raw);
   __nv_bfloat16* sv = sk + kAttnStages * TILE;
+  __shared__ int s_last;
 
   const int kvh = blockIdx.x, b = blockIdx.y, split = blockIdx.z;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, c = lane & 3;
 
+  pdl_wait();
+  pdl_launch_dependents();
+
   const int slot = row_slot[b];
   const int ctx = slot >= 0 ? pos_by_slot[slot] + 1 : 0;
   const int npages = (ctx + kPage - 1) / kPage;
-  const int pps = (npages + nsplit - 1) / nsplit;
+  int pps = (npages + nsplit - 1) / nsplit;
+  if (pps < kMinPagesPerSplit) pps = kMinPagesPerSplit;
+  const int active = (npages + pps - 1) / pps;
   const int p0 = split * pps;
   const int p1 = min(npages, p0 + pps);
   const int head0 = kvh * G;
+  float* wm = reinterpret_cast<float*>(smem_raw);
+  float* wl = wm + 4 * 16;
+  float* wo = wl + 4 * 16;  // [warp][16][D]
 
   if (p0 >= p1) {
     for (int h = tid; h < G; h += kAttnThreads) {
@@ -81,256 +95,269 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_kernel(
       part_m[base] = -INFINITY;
       part_l[base] = 0.f;
     }
-    return;
-  }
-
-  const int* pt = page_table + (size_t)slot * max_pages;
-  auto load_page = [&](int p, int st) {
-    const size_t goff = ((size_t)pt[p] * nkv + kvh) * TILE;
-    const __nv_bfloat16* gk = k_cache + goff;
-    const __nv_bfloat16* gv = v_cache + goff;
-    __nv_bfloat16* dk = sk + st * TILE;
-    __nv_bfloat16* dv = sv + st * TILE;
+  } else {
+    const int* pt = page_table + (size_t)slot * max_pages;
+    auto load_page = [&](int p, int st) {
+      const size_t goff = ((size_t)pt[p] * nkv + kvh) * TILE;
+      const __nv_bfloat16* gk = k_cache + goff;
+      const __nv_bfloat16* gv = v_cache + goff;
+      __nv_bfloat16* dk = sk + st * TILE;
+      __nv_bfloat16* dv = sv + st * TILE;
 #pragma unroll
-    for (int i = tid; i < kPage * CPR; i += kAttnThreads) {
-      const int row = i / CPR, cc = i % CPR;
-      const int sw = row * D + ((cc ^ (row & 7)) * 8);
-      cp_async16(dk + sw, gk + row * D + cc * 8);
-      cp_async16(dv + sw, gv + row * D + cc * 8);
-    }
-  };
-
-  // Q fragments for the (up to 16) query heads of this KV group, held for the whole loop.
-  uint32_t qa[D / 16][4];
-  {
-    const __nv_bfloat16* q0 = q + ((size_t)b * nq + head0) * D;
-#pragma unroll
-    for (int ks = 0; ks < D / 16; ++ks) {
-      const int d0 = ks * 16 + 2 * c;
-      qa[ks][0] = (g < G) ? *reinterpret_cast<const uint32_t*>(q0 + g * D + d0) : 0u;
-      qa[ks][1] = (g + 8 < G) ? *reinterpret_cast<const uint32_t*>(q0 + (g + 8) * D + d0) : 0u;
-      qa[ks][2] = (g < G) ? *reinterpret_cast<const uint32_t*>(q0 + g * D + d0 + 8) : 0u;
-      qa[ks][3] = (g + 8 < G) ? *reinterpret_cast<const uint32_t*>(q0 + (g + 8) * D + d0 + 8) : 0u;
-    }
-  }
-
-  float m_r[2] = {-INFINITY, -INFINITY};
-  float l_r[2] = {0.f, 0.f};
-  float o[D / 8][4];
-#pragma unroll
-  for (int i = 0; i < D / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+      for (int i = tid; i < kPage * CPR; i += kAttnThreads) {
+        const int row = i / CPR, cc = i % CPR;
+        const int sw = row * D + ((cc ^ (row & 7)) * 8);
+        cp_async16(dk + sw, gk + row * D + cc * 8);
+        cp_async16(dv + sw, gv + row * D + cc * 8);
+      }
+    };
 
 #pragma unroll
-  for (int i = 0; i < kAttnStages - 1; ++i) {
-    if (p0 + i < p1) load_page(p0 + i, i);
-    cp_async_commit();
-  }
-
-  for (int it = 0; p0 + it < p1; ++it) {
-    cp_async_wait<kAttnStages - 2>();
-    __syncthreads();
-    {
-      const int nxt = it + kAttnStages - 1;
-      if (p0 + nxt < p1) load_page(p0 + nxt, nxt % kAttnStages);
+    for (int i = 0; i < kAttnStages - 1; ++i) {
+      if (p0 + i < p1) load_page(p0 + i, i);
       cp_async_commit();
     }
-    const int st = it % kAttnStages;
-    const __nv_bfloat16* K = sk + st * TILE;
-    const __nv_bfloat16* V = sv + st * TILE;
 
-    // S = Q K^T for this warp's 16 tokens (two 8-token n-tiles)
-    float s[2][4];
-#pragma unroll
-    for (int nt = 0; nt < 2; ++nt) {
-      s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
-      const int t = warp * 16 + nt * 8 + g;
-      const __nv_bfloat16* krow = K + t * D + 2 * c;
+    // Q fragments for the (up to 16) query heads of this KV group, held for the whole loop.
+    uint32_t qa[D / 16][4];
+    {
+      const __nv_bfloat16* q0 = q + ((size_t)b * nq + head0) * D;
 #pragma unroll
       for (int ks = 0; ks < D / 16; ++ks) {
-        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(krow + (((2 * ks) ^ (t & 7)) * 8));
-        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(krow + (((2 * ks + 1) ^ (t & 7)) * 8));
-        mma16816(s[nt], qa[ks], b0, b1);
+        const int d0 = ks * 16 + 2 * c;
+        qa[ks][0] = (g < G) ? *reinterpret_cast<const uint32_t*>(q0 + g * D + d0) : 0u;
+        qa[ks][1] = (g + 8 < G) ? *reinterpret_cast<const uint32_t*>(q0 + (g + 8) * D + d0) : 0u;
+        qa[ks][2] = (g < G) ? *reinterpret_cast<const uint32_t*>(q0 + g * D + d0 + 8) : 0u;
+        qa[ks][3] = (g + 8 < G) ? *reinterpret_cast<const uint32_t*>(q0 + (g + 8) * D + d0 + 8) : 0u;
       }
     }
-    const int tok0 = (p0 + it) * kPage + warp * 16;
+
+    float m_r[2] = {-INFINITY, -INFINITY};
+    float l_r[2] = {0.f, 0.f};
+    float o[D / 8][4];
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt)
+    for (int i = 0; i < D / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+
+    for (int it = 0; p0 + it < p1; ++it) {
+      cp_async_wait<kAttnStages - 2>();
+      __syncthreads();
+      {
+        const int nxt = it + kAttnStages - 1;
+        if (p0 + nxt < p1) load_page(p0 + nxt, nxt % kAttnStages);
+        cp_async_commit();
+      }
+      const int st = it % kAttnStages;
+      const __nv_bfloat16* K = sk + st * TILE;
+      const __nv_bfloat16* V = sv + st * TILE;
+
+      // S = Q K^T for this warp's 16 tokens (two 8-token n-tiles)
+      float s[2][4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int tok = tok0 + nt * 8 + 2 * c + (e & 1);
-        s[nt][e] = (tok < ctx) ? s[nt][e] * scale_log2 : -INFINITY;
+      for (int nt = 0; nt < 2; ++nt) {
+        s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+        const int t = warp * 16 + nt * 8 + g;
+        const __nv_bfloat16* krow = K + t * D + 2 * c;
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+          const uint32_t b0 = *reinterpret_cast<const uint32_t*>(krow + (((2 * ks) ^ (t & 7)) * 8));
+          const uint32_t b1 = *reinterpret_cast<const uint32_t*>(krow + (((2 * ks + 1) ^ (t & 7)) * 8));
+          mma16816(s[nt], qa[ks], b0, b1);
+        }
+      }
+      const int tok0 = (p0 + it) * kPage + warp * 16;
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int tok = tok0 + nt * 8 + 2 * c + (e & 1);
+          s[nt][e] = (tok < ctx) ? s[nt][e] * scale_log2 : -INFINITY;
+        }
+
+      // online softmax (rows g and g+8), per-warp running state
+      float mx[2];
+      mx[0] = fmaxf(fmaxf(s[0][0], s[0][1]), fmaxf(s[1][0], s[1][1]));
+      mx[1] = fmaxf(fmaxf(s[0][2], s[0][3]), fmaxf(s[1][2], s[1][3]));
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
+        mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
+      }
+      float alpha[2], mnew[2];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        mnew[r] = fmaxf(m_r[r], mx[r]);
+        alpha[r] = (mnew[r] == -INFINITY) ? 1.f : exp2f(m_r[r] - mnew[r]);
+        m_r[r] = mnew[r];
+      }
+      float rs[2] = {0.f, 0.f};
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int r = e >> 1;
+          const float p = (mnew[r] == -INFINITY) ? 0.f : exp2f(s[nt][e] - mnew[r]);
+          s[nt][e] = p;
+          rs[r] += p;
+        }
+      l_r[0] = l_r[0] * alpha[0] + rs[0];
+      l_r[1] = l_r[1] * alpha[1] + rs[1];
+#pragma unroll
+      for (int i = 0; i < D / 8; ++i) {
+        o[i][0] *= alpha[0];
+        o[i][1] *= alpha[0];
+        o[i][2] *= alpha[1];
+        o[i][3] *= alpha[1];
       }
 
-    // online softmax (rows g and g+8), per-warp running state
-    float mx[2];
-    mx[0] = fmaxf(fmaxf(s[0][0], s[0][1]), fmaxf(s[1][0], s[1][1]));
-    mx[1] = fmaxf(fmaxf(s[0][2], s[0][3]), fmaxf(s[1][2], s[1][3]));
+      // O += P V
+      uint32_t pa[4];
+      pa[0] = pack_bf16(s[0][0], s[0][1]);
+      pa[1] = pack_bf16(s[0][2], s[0][3]);
+      pa[2] = pack_bf16(s[1][0], s[1][1]);
+      pa[3] = pack_bf16(s[1][2], s[1][3]);
+      const int vrow = warp * 16 + (lane & 15);
+#pragma unroll
+      for (int dn2 = 0; dn2 < D / 16; ++dn2) {
+        const int chunk = 2 * dn2 + (lane >> 4);
+        uint32_t r[4];
+        ldmatrix_x4_trans(r, V + vrow * D + ((chunk ^ (vrow & 7)) * 8));
+        mma16816(o[2 * dn2], pa, r[0], r[1]);
+        mma16816(o[2 * dn2 + 1], pa, r[2], r[3]);
+      }
+    }
+    cp_async_wait<0>();
+
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
-      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
-      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
+      l_r[r] += __shfl_xor_sync(0xffffffffu, l_r[r], 1);
+      l_r[r] += __shfl_xor_sync(0xffffffffu, l_r[r], 2);
     }
-    float alpha[2], mnew[2];
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      mnew[r] = fmaxf(m_r[r], mx[r]);
-      alpha[r] = (mnew[r] == -INFINITY) ? 1.f : exp2f(m_r[r] - mnew[r]);
-      m_r[r] = mnew[r];
+
+    // merge the 4 warps' partial softmax states through shared memory
+    __syncthreads();
+    if (c == 0) {
+      wm[warp * 16 + g] = m_r[0];
+      wm[warp * 16 + g + 8] = m_r[1];
+      wl[warp * 16 + g] = l_r[0];
+      wl[warp * 16 + g + 8] = l_r[1];
     }
-    float rs[2] = {0.f, 0.f};
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt)
+    for (int dn = 0; dn < D / 8; ++dn) {
+      const int d = dn * 8 + 2 * c;
+      wo[(warp * 16 + g) * D + d] = o[dn][0];
+      wo[(warp * 16 + g) * D + d + 1] = o[dn][1];
+      wo[(warp * 16 + g + 8) * D + d] = o[dn][2];
+      wo[(warp * 16 + g + 8) * D + d + 1] = o[dn][3];
+    }
+    __syncthreads();
+    for (int i = tid; i < G * D; i += kAttnThreads) {
+      const int h = i / D, d = i % D;
+      float M = -INFINITY;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int r = e >> 1;
-        const float p = (mnew[r] == -INFINITY) ? 0.f : exp2f(s[nt][e] - mnew[r]);
-        s[nt][e] = p;
-        rs[r] += p;
+      for (int w = 0; w < 4; ++w) M = fmaxf(M, wm[w * 16 + h]);
+      float L = 0.f, acc = 0.f;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const float mw = wm[w * 16 + h];
+        const float f = (mw == -INFINITY) ? 0.f : exp2f(mw - M);
+        L += wl[w * 16 + h] * f;
+        acc += wo[(w * 16 + h) * D + d] * f;
       }
-    l_r[0] = l_r[0] * alpha[0] + rs[0];
-    l_r[1] = l_r[1] * alpha[1] + rs[1];
-#pragma unroll
-    for (int i = 0; i < D / 8; ++i) {
-      o[i][0] *= alpha[0]; o[i][1] *= alpha[0];
-      o[i][2] *= alpha[1]; o[i][3] *= alpha[1];
-    }
-
-    // O += P V
-    uint32_t pa[4];
-    pa[0] = pack_bf16(s[0][0], s[0][1]);
-    pa[1] = pack_bf16(s[0][2], s[0][3]);
-    pa[2] = pack_bf16(s[1][0], s[1][1]);
-    pa[3] = pack_bf16(s[1][2], s[1][3]);
-    const int vrow = warp * 16 + (lane & 15);
-#pragma unroll
-    for (int dn2 = 0; dn2 < D / 16; ++dn2) {
-      const int chunk = 2 * dn2 + (lane >> 4);
-      uint32_t r[4];
-      ldmatrix_x4_trans(r, V + vrow * D + ((chunk ^ (vrow & 7)) * 8));
-      mma16816(o[2 * dn2], pa, r[0], r[1]);
-      mma16816(o[2 * dn2 + 1], pa, r[2], r[3]);
+      const size_t base = ((size_t)b * nq + head0 + h) * nsplit + split;
+      part_o[base * D + d] = acc;
+      if (d == 0) {
+        part_m[base] = M;
+        part_l[base] = L;
+      }
     }
   }
-  cp_async_wait<0>();
 
-#pragma unroll
-  for (int r = 0; r < 2; ++r) {
-    l_r[r] += __shfl_xor_sync(0xffffffffu, l_r[r], 1);
-    l_r[r] += __shfl_xor_sync(0xffffffffu, l_r[r], 2);
-  }
-
-  // merge the 4 warps' partial softmax states through shared memory
+  // ---- split merge by the last CTA of this (row, kv head) ----
+  __threadfence();
   __syncthreads();
-  float* wm = reinterpret_cast<float*>(smem_raw);
-  float* wl = wm + 4 * 16;
-  float* wo = wl + 4 * 16;  // [warp][16][D]
-  if (c == 0) {
-    wm[warp * 16 + g] = m_r[0];
-    wm[warp * 16 + g + 8] = m_r[1];
-    wl[warp * 16 + g] = l_r[0];
-    wl[warp * 16 + g + 8] = l_r[1];
+  if (tid == 0) {
+    const unsigned int prev = atomicAdd(&merge_ctr[b * nkv + kvh], 1u);
+    s_last = (prev == (unsigned int)nsplit - 1u);
   }
-#pragma unroll
-  for (int dn = 0; dn < D / 8; ++dn) {
-    const int d = dn * 8 + 2 * c;
-    wo[(warp * 16 + g) * D + d] = o[dn][0];
-    wo[(warp * 16 + g) * D + d + 1] = o[dn][1];
-    wo[(warp * 16 + g + 8) * D + d] = o[dn][2];
-    wo[(warp * 16 + g + 8) * D + d + 1] = o[dn][3];
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  float* fac = wo + 4 * 16 * D;      // [16][kMaxAttnSplits]
+  float* inv_l = fac + 16 * kMaxAttnSplits;  // [16]
+  for (int h = warp; h < G; h += 4) {
+    const size_t base = ((size_t)b * nq + head0 + h) * nsplit;
+    float M = -INFINITY;
+    for (int s2 = lane; s2 < active; s2 += 32) M = fmaxf(M, __ldcg(part_m + base + s2));
+    M = warp_max(M);
+    float L = 0.f;
+    for (int s2 = lane; s2 < active; s2 += 32) {
+      const float ms = __ldcg(part_m + base + s2);
+      const float f = (ms == -INFINITY || M == -INFINITY) ? 0.f : exp2f(ms - M);
+      fac[h * kMaxAttnSplits + s2] = f;
+      L += __ldcg(part_l + base + s2) * f;
+    }
+    L = warp_sum(L);
+    if (lane == 0) inv_l[h] = L > 0.f ? 1.f / L : 0.f;
   }
   __syncthreads();
   for (int i = tid; i < G * D; i += kAttnThreads) {
     const int h = i / D, d = i % D;
-    float M = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) M = fmaxf(M, wm[w * 16 + h]);
-    float L = 0.f, acc = 0.f;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const float mw = wm[w * 16 + h];
-      const float f = (mw == -INFINITY) ? 0.f : exp2f(mw - M);
-      L += wl[w * 16 + h] * f;
-      acc += wo[(w * 16 + h) * D + d] * f;
+    const size_t base = ((size_t)b * nq + head0 + h) * nsplit;
+    float acc = 0.f;
+    for (int s2 = 0; s2 < active; ++s2) {
+      const float f = fac[h * kMaxAttnSplits + s2];
+      if (f != 0.f) acc += __ldcg(part_o + (base + s2) * D + d) * f;
     }
-    const size_t base = ((size_t)b * nq + head0 + h) * nsplit + split;
-    part_o[base * D + d] = acc;
-    if (d == 0) {
-      part_m[base] = M;
-      part_l[base] = L;
-    }
+    out[((size_t)b * nq + head0 + h) * D + d] = f2bf(acc * inv_l[h]);
   }
+  if (tid == 0) merge_ctr[b * nkv + kvh] = 0u;  // re-arm for the next launch / graph replay
 }
 
 template <int D>
-__global__ void attn_combine_kernel(const float* __restrict__ part_m, const float* __restrict__ part_l,
-                                    const float* __restrict__ part_o, int nq, int nsplit,
-                                    __nv_bfloat16* __restrict__ out) {
-  const int b = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
-  const size_t base = ((size_t)b * nq + h) * nsplit;
-  float M = -INFINITY;
-  for (int s = 0; s < nsplit; ++s) M = fmaxf(M, part_m[base + s]);
-  float L = 0.f, acc = 0.f;
-  if (M != -INFINITY) {
-    for (int s = 0; s < nsplit; ++s) {
-      const float ms = part_m[base + s];
-      if (ms == -INFINITY) continue;
-      const float f = exp2f(ms - M);
-      L += part_l[base + s] * f;
-      acc += part_o[(base + s) * D + d] * f;
-    }
-  }
-  out[((size_t)b * nq + h) * D + d] = f2bf(L > 0.f ? acc / L : 0.f);
+static constexpr int attn_smem() {
+  return 2 * kAttnStages * kPage * D * 2;
 }
 
 int configure_attention() {
   TPS_CUDA_TRY(cudaFuncSetAttribute(paged_attn_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    2 * kAttnStages * kPage * 128 * 2));
+                                    attn_smem<128>()));
   TPS_CUDA_TRY(cudaFuncSetAttribute(paged_attn_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    2 * kAttnStages * kPage * 64 * 2));
+                                    attn_smem<64>()));
   return kOk;
 }
 
 int attn_splits(int B, int nkv, int max_pages) {
   int want = (2 * kNumSMs + B * nkv - 1) / (B * nkv);
+  const int cap = (max_pages + kMinPagesPerSplit - 1) / kMinPagesPerSplit;
+  if (want > cap) want = cap;
+  if (want > kMaxAttnSplits) want = kMaxAttnSplits;
   if (want < 1) want = 1;
-  if (want > max_pages) want = max_pages;
-  if (want > 128) want = 128;
   return want;
 }
 
 int paged_attention(const void* q, const void* k_cache, const void* v_cache, const int* row_slot,
-                    const int* pos_by_slot, const int* page_table, int max_pages, int B, int nq, int nkv,
-                    int D, int nsplit, float* part_m, float* part_l, float* part_o, void* out,
+                    const int* pos_by_slot, const int* page_table, int max_pages, int B, int nq, int nkv, int D,
+                    int nsplit, float* part_m, float* part_l, float* part_o, unsigned int* merge_ctr, void* out,
                     cudaStream_t st) {
   TPS_CHECK_ARG(B > 0 && nkv > 0 && nq % nkv == 0, "paged_attention: nq must be a multiple of nkv");
   const int G = nq / nkv;
   TPS_CHECK_ARG(G <= 16, "paged_attention: at most 16 query heads per KV head");
-  TPS_CHECK_ARG(nsplit >= 1, "paged_attention: nsplit >= 1");
+  TPS_CHECK_ARG(nsplit >= 1 && nsplit <= kMaxAttnSplits, "paged_attention: 1 <= nsplit <= 128");
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)D);
-  dim3 grid(nkv, B, nsplit);
-  if (D == 128) {
-    const int smem = 2 * kAttnStages * kPage * 128 * 2;
-    paged_attn_kernel<128><<<grid, kAttnThreads, smem, st>>>(
-        reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(k_cache),
-        reinterpret_cast<const __nv_bfloat16*>(v_cache), row_slot, pos_by_slot, page_table, max_pages, nq,
-        nkv, G, nsplit, scale_log2, part_m, part_l, part_o);
-    TPS_LAUNCH_CHECK();
-    attn_combine_kernel<128><<<dim3(B, nq), 128, 0, st>>>(part_m, part_l, part_o, nq, nsplit,
-                                                          reinterpret_cast<__nv_bfloat16*>(out));
-  } else if (D == 64) {
-    const int smem = 2 * kAttnStages * kPage * 64 * 2;
-    paged_attn_kernel<64><<<grid, kAttnThreads, smem, st>>>(
-        reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(k_cache),
-        reinterpret_cast<const __nv_bfloat16*>(v_cache), row_slot, pos_by_slot, page_table, max_pages, nq,
-        nkv, G, nsplit, scale_log2, part_m, part_l, part_o);
-    TPS_LAUNCH_CHECK();
-    attn_combine_kernel<64><<<dim3(B, nq), 64, 0, st>>>(part_m, part_l, part_o, nq, nsplit,
-                                                        reinterpret_cast<__nv_bfloat16*>(out));
-  } else {
-    return fail(kInvalid, "paged_attention: head_dim must be 64 or 128");
-  }
-  TPS_LAUNCH_CHECK();
-  return kOk;
+  const dim3 grid(nkv, B, nsplit);
+  const auto* qq = reinterpret_cast<const __nv_bfloat16*>(q);
+  const auto* kk = reinterpret_cast<const __nv_bfloat16*>(k_cache);
+  const auto* vv = reinterpret_cast<const __nv_bfloat16*>(v_cache);
+  auto* oo = reinterpret_cast<__nv_bfloat16*>(out);
+  if (D == 128)
+    return launch_k(paged_attn_kernel<128>, grid, dim3(kAttnThreads), attn_smem<128>(), st, true, qq, kk, vv,
+                    row_slot, pos_by_slot, page_table, max_pages, nq, nkv, G, nsplit, scale_log2, part_m, part_l,
+                    part_o, merge_ctr, oo);
+  if (D == 64)
+    return launch_k(paged_attn_kernel<64>, grid, dim3(kAttnThreads), attn_smem<64>(), st, true, qq, kk, vv,
+                    row_slot, pos_by_slot, page_table, max_pages, nq, nkv, G, nsplit, scale_log2, part_m, part_l,
+                    part_o, merge_ctr, oo);
+  return fail(kInvalid, "paged_attention: head_dim must be 64 or 128");
 }
 
 }  // namespace tps

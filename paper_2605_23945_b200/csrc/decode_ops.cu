@@ -4,6 +4,11 @@
 // vocab-parallel greedy argmax with its cross-rank reduce, and the TP
 // reduce-and-push (one-shot allreduce over NVLink P2P stores).
 //
+// At tail batch sizes these kernels are latency-bound, so they (1) sum split /
+// rank partials from strided sources with all loads issued before the adds,
+// (2) use programmatic dependent launch so their launch and prologue overlap
+// the previous kernel, and (3) keep grids wide enough to spread across SMs.
+//
 // Batch rows are indirected through row_slot[b] -> sample slot; per-slot state
 // (position, page table, token history) stays where it is when the batch is
 // compacted after completions, so a CUDA-graph replay only needs a new
@@ -12,6 +17,10 @@
 #include "decode_ops.cuh"
 
 namespace tps {
+
+static bool g_pdl = true;
+bool pdl_enabled() { return g_pdl; }
+void set_pdl(bool on) { g_pdl = on; }
 
 __device__ __forceinline__ void do_wait(const WaitSpec& w) {
   if (w.ctr == nullptr) return;
@@ -37,6 +46,40 @@ __device__ __forceinline__ void do_signal(const SignalSpec& s) {
   }
 }
 
+// sum_{i<n} base[i*stride + off] in index order, loads batched 8 at a time
+__device__ __forceinline__ float4 src_sum4(const Src& s, long long off4) {
+  const float4* b = reinterpret_cast<const float4*>(s.base) + off4;
+  const long long st4 = s.stride / 4;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int i0 = 0; i0 < s.n; i0 += 8) {
+    float4 v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (i0 + j < s.n) v[j] = b[(long long)(i0 + j) * st4];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (i0 + j < s.n) {
+        acc.x += v[j].x; acc.y += v[j].y; acc.z += v[j].z; acc.w += v[j].w;
+      }
+  }
+  return acc;
+}
+
+__device__ __forceinline__ float src_sum(const Src& s, long long off) {
+  const float* b = s.base + off;
+  float acc = 0.f;
+  for (int i0 = 0; i0 < s.n; i0 += 8) {
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (i0 + j < s.n) v[j] = b[(long long)(i0 + j) * s.stride];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (i0 + j < s.n) acc += v[j];
+  }
+  return acc;
+}
+
 template <int NT>
 __device__ __forceinline__ float block_sum(float v, float* red) {
   v = warp_sum(v);
@@ -56,8 +99,9 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 // resid[b][:] = E[history[slot][pos]][:]  (replicated vocab table, bf16 -> fp32)
 __global__ void embed_kernel(const int* __restrict__ row_slot, const int* __restrict__ pos_by_slot,
                              const int* __restrict__ history, int hist_ld,
-                             const __nv_bfloat16* __restrict__ table, int H,
-                             float* __restrict__ resid) {
+                             const __nv_bfloat16* __restrict__ table, int H, float* __restrict__ resid) {
+  pdl_wait();
+  pdl_launch_dependents();
   const int b = blockIdx.x;
   const int slot = row_slot[b];
   int tok = 0;
@@ -68,37 +112,49 @@ __global__ void embed_kernel(const int* __restrict__ row_slot, const int* __rest
 }
 
 // ------------------------------------------------- residual add + RMSNorm ---
-// resid[b] += sum_i src_i[b] (list order); out[b] = bf16(resid * rstd * w)
-constexpr int kNormThreads = 256;
-__global__ void __launch_bounds__(kNormThreads) add_norm_kernel(
-    float* __restrict__ resid, SrcList src, WaitSpec wait, const __nv_bfloat16* __restrict__ w,
-    float eps, int H, __nv_bfloat16* __restrict__ out, int ldo) {
+// resid[b] += sum_i src_i[b] (index order); out[b] = bf16(resid * rstd * w)
+constexpr int kNormThreads = 512;
+constexpr int kNormVec = 4;  // float4 per thread held in registers (H <= 8192)
+__global__ void __launch_bounds__(kNormThreads) add_norm_kernel(float* __restrict__ resid, Src src,
+                                                                WaitSpec wait,
+                                                                const __nv_bfloat16* __restrict__ w, float eps,
+                                                                int H, __nv_bfloat16* __restrict__ out, int ldo) {
   __shared__ float red[32];
   const int b = blockIdx.x;
+  pdl_wait();
+  pdl_launch_dependents();
   do_wait(wait);
   float4* r4 = reinterpret_cast<float4*>(resid + (size_t)b * H);
   const int H4 = H / 4;
+  float4 v[kNormVec];
   float ss = 0.f;
-  for (int i = threadIdx.x; i < H4; i += kNormThreads) {
-    float4 v = r4[i];
-    for (int s = 0; s < src.n; ++s) {
-      const float4 p = reinterpret_cast<const float4*>(src.p[s] + (size_t)b * H)[i];
-      v.x += p.x; v.y += p.y; v.z += p.z; v.w += p.w;
+#pragma unroll
+  for (int j = 0; j < kNormVec; ++j) {
+    const int i = threadIdx.x + j * kNormThreads;
+    if (i < H4) {
+      float4 x = r4[i];
+      if (src.n > 0) {
+        const float4 p = src_sum4(src, (long long)b * H4 + i);
+        x.x += p.x; x.y += p.y; x.z += p.z; x.w += p.w;
+        r4[i] = x;
+      }
+      v[j] = x;
+      ss += x.x * x.x + x.y * x.y + x.z * x.z + x.w * x.w;
     }
-    r4[i] = v;
-    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
   }
   ss = block_sum<kNormThreads>(ss, red);
   const float rstd = rsqrtf(ss / (float)H + eps);
-  __nv_bfloat16* o = out + (size_t)b * ldo;
-  for (int i = threadIdx.x; i < H4; i += kNormThreads) {
-    const float4 v = r4[i];
-    const __nv_bfloat162* wp = reinterpret_cast<const __nv_bfloat162*>(w) + 2 * i;
-    const float2 w01 = __bfloat1622float2(wp[0]);
-    const float2 w23 = __bfloat1622float2(wp[1]);
-    __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(o) + 2 * i;
-    op[0] = __floats2bfloat162_rn(v.x * rstd * w01.x, v.y * rstd * w01.y);
-    op[1] = __floats2bfloat162_rn(v.z * rstd * w23.x, v.w * rstd * w23.y);
+  __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(out + (size_t)b * ldo);
+  const __nv_bfloat162* wp = reinterpret_cast<const __nv_bfloat162*>(w);
+#pragma unroll
+  for (int j = 0; j < kNormVec; ++j) {
+    const int i = threadIdx.x + j * kNormThreads;
+    if (i < H4) {
+      const float2 w01 = __bfloat1622float2(wp[2 * i]);
+      const float2 w23 = __bfloat1622float2(wp[2 * i + 1]);
+      o[2 * i] = __floats2bfloat162_rn(v[j].x * rstd * w01.x, v[j].y * rstd * w01.y);
+      o[2 * i + 1] = __floats2bfloat162_rn(v[j].z * rstd * w23.x, v[j].w * rstd * w23.y);
+    }
   }
 }
 
@@ -106,15 +162,12 @@ __global__ void __launch_bounds__(kNormThreads) add_norm_kernel(
 // Sum this rank's split-K partials and store the [rows][cols] result into this
 // rank's slot of every TP peer's receive area (NVLink P2P stores), then signal.
 constexpr int kPushBlocks = 64;
-__global__ void __launch_bounds__(256) reduce_push_kernel(SrcList src, DstList dst, int64_t n4,
-                                                          SignalSpec sig) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    float4 v = reinterpret_cast<const float4*>(src.p[0])[i];
-    for (int s = 1; s < src.n; ++s) {
-      const float4 p = reinterpret_cast<const float4*>(src.p[s])[i];
-      v.x += p.x; v.y += p.y; v.z += p.z; v.w += p.w;
-    }
+__global__ void __launch_bounds__(256) reduce_push_kernel(Src src, DstList dst, long long n4, SignalSpec sig) {
+  pdl_wait();
+  pdl_launch_dependents();
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float4 v = src_sum4(src, i);
     for (int d = 0; d < dst.n; ++d) reinterpret_cast<float4*>(dst.p[d])[i] = v;
   }
   do_signal(sig);
@@ -124,67 +177,70 @@ __global__ void __launch_bounds__(256) reduce_push_kernel(SrcList src, DstList d
 // partial layout [split][B][Nqkv] with Nqkv = (nq + 2 nkv) * D, rows ordered
 // [q heads | k heads | v heads] (canonical shard layout). RoPE is the
 // rotate-half form used by Llama/Qwen2 with a host-built fp32 cos/sin table.
-// KV cache per layer: [num_pages][nkv][P][D] bf16.
-__global__ void qkv_rope_append_kernel(SrcList src, const __nv_bfloat16* __restrict__ bias,
-                                       const int* __restrict__ row_slot,
-                                       const int* __restrict__ pos_by_slot,
-                                       const int* __restrict__ page_table, int max_pages,
-                                       const float* __restrict__ cos_t, const float* __restrict__ sin_t,
-                                       int B, int nq, int nkv, int D, int P,
-                                       __nv_bfloat16* __restrict__ q_out,
-                                       __nv_bfloat16* __restrict__ k_cache,
-                                       __nv_bfloat16* __restrict__ v_cache) {
-  const int b = blockIdx.x;
-  const int h = blockIdx.y;
-  const int i = threadIdx.x;  // 0 .. D/2-1
+// KV cache per layer: [num_pages][nkv][P][D] bf16. One warp per (row, head).
+__global__ void __launch_bounds__(128) qkv_rope_append_kernel(
+    Src src, const __nv_bfloat16* __restrict__ bias, const int* __restrict__ row_slot,
+    const int* __restrict__ pos_by_slot, const int* __restrict__ page_table, int max_pages,
+    const float* __restrict__ cos_t, const float* __restrict__ sin_t, int B, int nq, int nkv, int D, int P,
+    __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ k_cache, __nv_bfloat16* __restrict__ v_cache) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const int heads = nq + nkv;
+  const int task = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (task >= B * heads) return;
+  const int b = task / heads, h = task % heads;
+  const int lane = threadIdx.x & 31;
   const int half = D / 2;
   const int slot = row_slot[b];
-  const int N = (nq + 2 * nkv) * D;
+  const long long N = (long long)(nq + 2 * nkv) * D;
   const int pos = slot >= 0 ? pos_by_slot[slot] : 0;
-  auto val = [&](int c) {
-    float v = bias ? bf2f(bias[c]) : 0.f;
-    for (int s = 0; s < src.n; ++s) v += src.p[s][(size_t)b * N + c];
-    return v;
-  };
-  const float cs = cos_t[(size_t)pos * half + i];
-  const float sn = sin_t[(size_t)pos * half + i];
-  if (h < nq) {
-    const int c0 = h * D;
-    const float x1 = val(c0 + i), x2 = val(c0 + i + half);
-    __nv_bfloat16* q = q_out + ((size_t)b * nq + h) * D;
-    q[i] = f2bf(x1 * cs - x2 * sn);
-    q[i + half] = f2bf(x2 * cs + x1 * sn);
-    return;
+  const long long rowoff = (long long)b * N;
+  for (int i = lane; i < half; i += 32) {
+    const float cs = cos_t[(size_t)pos * half + i];
+    const float sn = sin_t[(size_t)pos * half + i];
+    if (h < nq) {
+      const int c0 = h * D;
+      float x1 = src_sum(src, rowoff + c0 + i), x2 = src_sum(src, rowoff + c0 + i + half);
+      if (bias) { x1 += bf2f(bias[c0 + i]); x2 += bf2f(bias[c0 + i + half]); }
+      __nv_bfloat16* q = q_out + ((size_t)b * nq + h) * D;
+      q[i] = f2bf(x1 * cs - x2 * sn);
+      q[i + half] = f2bf(x2 * cs + x1 * sn);
+    } else if (slot >= 0) {
+      const int j = h - nq;
+      const int kc0 = nq * D + j * D;
+      const int vc0 = (nq + nkv) * D + j * D;
+      float k1 = src_sum(src, rowoff + kc0 + i), k2 = src_sum(src, rowoff + kc0 + i + half);
+      float v1 = src_sum(src, rowoff + vc0 + i), v2 = src_sum(src, rowoff + vc0 + i + half);
+      if (bias) {
+        k1 += bf2f(bias[kc0 + i]); k2 += bf2f(bias[kc0 + i + half]);
+        v1 += bf2f(bias[vc0 + i]); v2 += bf2f(bias[vc0 + i + half]);
+      }
+      const int page = page_table[(size_t)slot * max_pages + pos / P];
+      const size_t off = (((size_t)page * nkv + j) * P + (pos % P)) * D;
+      k_cache[off + i] = f2bf(k1 * cs - k2 * sn);
+      k_cache[off + i + half] = f2bf(k2 * cs + k1 * sn);
+      v_cache[off + i] = f2bf(v1);
+      v_cache[off + i + half] = f2bf(v2);
+    }
   }
-  if (slot < 0) return;
-  const int j = h - nq;
-  const int kc0 = nq * D + j * D;
-  const int vc0 = (nq + nkv) * D + j * D;
-  const float k1 = val(kc0 + i), k2 = val(kc0 + i + half);
-  const float v1 = val(vc0 + i), v2 = val(vc0 + i + half);
-  const int page = page_table[(size_t)slot * max_pages + pos / P];
-  const size_t off = (((size_t)page * nkv + j) * P + (pos % P)) * D;
-  k_cache[off + i] = f2bf(k1 * cs - k2 * sn);
-  k_cache[off + i + half] = f2bf(k2 * cs + k1 * sn);
-  v_cache[off + i] = f2bf(v1);
-  v_cache[off + i + half] = f2bf(v2);
 }
 
 // ------------------------------------------------------------- SiLU * up ---
 // partial layout [split][B][2F] = [gate rows | up rows]; out[b][f] = bf16(silu(g) * u)
-__global__ void silu_mul_kernel(SrcList src, int B, int F, __nv_bfloat16* __restrict__ out, int ldo) {
-  const int64_t total = (int64_t)B * F;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int b = (int)(t / F), f = (int)(t % F);
-    float g = 0.f, u = 0.f;
-    for (int s = 0; s < src.n; ++s) {
-      const float* p = src.p[s] + (size_t)b * 2 * F;
-      g += p[f];
-      u += p[F + f];
-    }
-    const float sg = g / (1.f + __expf(-g));
-    out[(size_t)b * ldo + f] = f2bf(sg * u);
+__global__ void silu_mul_kernel(Src src, int B, int F, __nv_bfloat16* __restrict__ out, int ldo) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const int F4 = F / 4;
+  const long long total = (long long)B * F4;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int b = (int)(t / F4), f4 = (int)(t % F4);
+    const long long row4 = (long long)b * 2 * F4;
+    const float4 g = src_sum4(src, row4 + f4);
+    const float4 u = src_sum4(src, row4 + F4 + f4);
+    __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(out + (size_t)b * ldo) + 2 * f4;
+    o[0] = __floats2bfloat162_rn(g.x / (1.f + __expf(-g.x)) * u.x, g.y / (1.f + __expf(-g.y)) * u.y);
+    o[1] = __floats2bfloat162_rn(g.z / (1.f + __expf(-g.z)) * u.z, g.w / (1.f + __expf(-g.w)) * u.w);
   }
 }
 
@@ -192,23 +248,35 @@ __global__ void silu_mul_kernel(SrcList src, int B, int F, __nv_bfloat16* __rest
 // Stage 1: per (row, vocab chunk) max with the smallest index on ties.
 constexpr int kArgmaxThreads = 256;
 __device__ __forceinline__ void cand_merge(float& v, int& i, float v2, int i2) {
-  if (v2 > v || (v2 == v && i2 < i)) { v = v2; i = i2; }
+  if (v2 > v || (v2 == v && i2 < i)) {
+    v = v2;
+    i = i2;
+  }
 }
 
-__global__ void __launch_bounds__(kArgmaxThreads) argmax_stage1_kernel(
-    SrcList src, int B, int V, int vocab_offset, int nchunk, ArgmaxCand* __restrict__ cand,
-    SignalSpec sig) {
+__global__ void __launch_bounds__(kArgmaxThreads) argmax_stage1_kernel(Src src, int B, int V, int vocab_offset,
+                                                                      int nchunk, ArgmaxCand* __restrict__ cand,
+                                                                      SignalSpec sig) {
   __shared__ float sv[kArgmaxThreads / 32];
   __shared__ int si[kArgmaxThreads / 32];
+  pdl_wait();
+  pdl_launch_dependents();
   const int b = blockIdx.x, c = blockIdx.y;
-  const int per = (V + nchunk - 1) / nchunk;
+  const int per = ((V + nchunk - 1) / nchunk + 3) & ~3;
   const int lo = c * per, hi = min(V, lo + per);
   float best = -INFINITY;
   int bidx = 0x7fffffff;
-  for (int j = lo + threadIdx.x; j < hi; j += kArgmaxThreads) {
-    float v = 0.f;
-    for (int s = 0; s < src.n; ++s) v += src.p[s][(size_t)b * V + j];
-    cand_merge(best, bidx, v, j + vocab_offset);
+  if ((V & 3) == 0) {
+    for (int j = lo + 4 * threadIdx.x; j < hi; j += 4 * kArgmaxThreads) {
+      const float4 v = src_sum4(src, ((long long)b * V + j) / 4);
+      cand_merge(best, bidx, v.x, j + vocab_offset);
+      cand_merge(best, bidx, v.y, j + 1 + vocab_offset);
+      cand_merge(best, bidx, v.z, j + 2 + vocab_offset);
+      cand_merge(best, bidx, v.w, j + 3 + vocab_offset);
+    }
+  } else {
+    for (int j = lo + threadIdx.x; j < hi; j += kArgmaxThreads)
+      cand_merge(best, bidx, src_sum(src, (long long)b * V + j), j + vocab_offset);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -217,7 +285,10 @@ __global__ void __launch_bounds__(kArgmaxThreads) argmax_stage1_kernel(
     cand_merge(best, bidx, v2, i2);
   }
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) { sv[w] = best; si[w] = bidx; }
+  if (l == 0) {
+    sv[w] = best;
+    si[w] = bidx;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int k = 1; k < kArgmaxThreads / 32; ++k) cand_merge(best, bidx, sv[k], si[k]);
@@ -228,11 +299,12 @@ __global__ void __launch_bounds__(kArgmaxThreads) argmax_stage1_kernel(
 
 // Stage 2: reduce the candidates of every TP rank (list order = rank order),
 // append the token to the sample's history and advance its position.
-__global__ void argmax_finalize_kernel(CandList cands, int nchunk, WaitSpec wait,
-                                       const int* __restrict__ row_slot, int* __restrict__ pos_by_slot,
-                                       const int* __restrict__ prompt_len, int* __restrict__ history,
-                                       int hist_ld, int* __restrict__ out_tok) {
+__global__ void argmax_finalize_kernel(CandList cands, int nchunk, WaitSpec wait, const int* __restrict__ row_slot,
+                                       int* __restrict__ pos_by_slot, const int* __restrict__ prompt_len,
+                                       int* __restrict__ history, int hist_ld, int* __restrict__ out_tok) {
   const int b = blockIdx.x;
+  pdl_wait();
+  pdl_launch_dependents();
   do_wait(wait);
   float best = -INFINITY;
   int bidx = 0x7fffffff;
@@ -258,101 +330,89 @@ __global__ void argmax_finalize_kernel(CandList cands, int nchunk, WaitSpec wait
   }
 }
 
-__global__ void epoch_advance_kernel(uint64_t* epoch) { *epoch += 1ull; }
+__global__ void epoch_advance_kernel(uint64_t* epoch) {
+  pdl_wait();
+  pdl_launch_dependents();
+  *epoch += 1ull;
+}
 
-// Plain fp32 sum of a SrcList into a dense buffer (tests / logits export).
-__global__ void sum_src_kernel(SrcList src, int64_t n, float* __restrict__ out) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    float v = 0.f;
-    for (int s = 0; s < src.n; ++s) v += src.p[s][i];
-    out[i] = v;
-  }
+// Plain fp32 sum of a Src into a dense buffer (tests / logits export).
+__global__ void sum_src_kernel(Src src, long long n, float* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = src_sum(src, i);
 }
 
 // -------------------------------------------------------------- launchers ---
-int embed(const int* row_slot, const int* pos_by_slot, const int* history, int hist_ld,
-          const void* table, int H, int B, float* resid, cudaStream_t st) {
+static int grid_for(long long work, int per_block, int cap) {
+  long long g = (work + per_block - 1) / per_block;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+int embed(const int* row_slot, const int* pos_by_slot, const int* history, int hist_ld, const void* table,
+          int H, int B, float* resid, cudaStream_t st) {
   TPS_CHECK_ARG(H % 2 == 0 && B > 0, "embed: H must be even, B > 0");
-  embed_kernel<<<B, 256, 0, st>>>(row_slot, pos_by_slot, history, hist_ld,
-                                  reinterpret_cast<const __nv_bfloat16*>(table), H, resid);
-  TPS_LAUNCH_CHECK();
-  return kOk;
+  return launch_k(embed_kernel, dim3(B), dim3(256), 0, st, true, row_slot, pos_by_slot, history, hist_ld,
+                  reinterpret_cast<const __nv_bfloat16*>(table), H, resid);
 }
 
-int add_norm(float* resid, const SrcList& src, const WaitSpec& wait, const void* w, float eps, int H,
-             int B, void* out, int ldo, cudaStream_t st) {
-  TPS_CHECK_ARG(H % 4 == 0 && ldo % 4 == 0 && B > 0, "add_norm: H, ldo must be multiples of 4");
-  TPS_CHECK_ARG(src.n >= 0 && src.n <= kMaxSrc, "add_norm: too many sources");
-  add_norm_kernel<<<B, kNormThreads, 0, st>>>(resid, src, wait, reinterpret_cast<const __nv_bfloat16*>(w),
-                                              eps, H, reinterpret_cast<__nv_bfloat16*>(out), ldo);
-  TPS_LAUNCH_CHECK();
-  return kOk;
+int add_norm(float* resid, const Src& src, const WaitSpec& wait, const void* w, float eps, int H, int B,
+             void* out, int ldo, cudaStream_t st) {
+  TPS_CHECK_ARG(H % 4 == 0 && ldo % 2 == 0 && B > 0, "add_norm: H must be a multiple of 4");
+  TPS_CHECK_ARG(H / 4 <= kNormThreads * kNormVec, "add_norm: H > 8192");
+  TPS_CHECK_ARG(src.n == 0 || src.stride % 4 == 0, "add_norm: source stride must be a multiple of 4");
+  return launch_k(add_norm_kernel, dim3(B), dim3(kNormThreads), 0, st, true, resid, src, wait,
+                  reinterpret_cast<const __nv_bfloat16*>(w), eps, H, reinterpret_cast<__nv_bfloat16*>(out), ldo);
 }
 
-int reduce_push(const SrcList& src, const DstList& dst, int64_t n, const SignalSpec& sig, cudaStream_t st) {
-  TPS_CHECK_ARG(n % 4 == 0 && src.n >= 1 && dst.n >= 1, "reduce_push: n % 4 == 0, >=1 src/dst");
-  reduce_push_kernel<<<kPushBlocks, 256, 0, st>>>(src, dst, n / 4, sig);
-  TPS_LAUNCH_CHECK();
-  return kOk;
+int reduce_push(const Src& src, const DstList& dst, long long n, const SignalSpec& sig, cudaStream_t st) {
+  TPS_CHECK_ARG(n % 4 == 0 && src.n >= 1 && dst.n >= 1 && src.stride % 4 == 0,
+                "reduce_push: n % 4 == 0, >=1 src/dst");
+  return launch_k(reduce_push_kernel, dim3(kPushBlocks), dim3(256), 0, st, true, src, dst, n / 4, sig);
 }
 
-int qkv_rope_append(const SrcList& src, const void* bias, const int* row_slot, const int* pos_by_slot,
-                    const int* page_table, int max_pages, const float* cos_t, const float* sin_t, int B,
-                    int nq, int nkv, int D, int P, void* q_out, void* k_cache, void* v_cache,
-                    cudaStream_t st) {
+int qkv_rope_append(const Src& src, const void* bias, const int* row_slot, const int* pos_by_slot,
+                    const int* page_table, int max_pages, const float* cos_t, const float* sin_t, int B, int nq,
+                    int nkv, int D, int P, void* q_out, void* k_cache, void* v_cache, cudaStream_t st) {
   TPS_CHECK_ARG(D % 2 == 0 && D <= 256 && B > 0 && nq > 0 && nkv > 0, "qkv_rope_append: bad shape");
-  dim3 grid(B, nq + nkv);
-  qkv_rope_append_kernel<<<grid, D / 2, 0, st>>>(
-      src, reinterpret_cast<const __nv_bfloat16*>(bias), row_slot, pos_by_slot, page_table, max_pages,
-      cos_t, sin_t, B, nq, nkv, D, P, reinterpret_cast<__nv_bfloat16*>(q_out),
-      reinterpret_cast<__nv_bfloat16*>(k_cache), reinterpret_cast<__nv_bfloat16*>(v_cache));
-  TPS_LAUNCH_CHECK();
-  return kOk;
+  const int tasks = B * (nq + nkv);
+  return launch_k(qkv_rope_append_kernel, dim3((tasks + 3) / 4), dim3(128), 0, st, true, src,
+                  reinterpret_cast<const __nv_bfloat16*>(bias), row_slot, pos_by_slot, page_table, max_pages,
+                  cos_t, sin_t, B, nq, nkv, D, P, reinterpret_cast<__nv_bfloat16*>(q_out),
+                  reinterpret_cast<__nv_bfloat16*>(k_cache), reinterpret_cast<__nv_bfloat16*>(v_cache));
 }
 
-int silu_mul(const SrcList& src, int B, int F, void* out, int ldo, cudaStream_t st) {
-  TPS_CHECK_ARG(B > 0 && F > 0, "silu_mul: bad shape");
-  const int64_t total = (int64_t)B * F;
-  int blocks = (int)((total + 255) / 256);
-  if (blocks > 4 * kNumSMs) blocks = 4 * kNumSMs;
-  silu_mul_kernel<<<blocks, 256, 0, st>>>(src, B, F, reinterpret_cast<__nv_bfloat16*>(out), ldo);
-  TPS_LAUNCH_CHECK();
-  return kOk;
+int silu_mul(const Src& src, int B, int F, void* out, int ldo, cudaStream_t st) {
+  TPS_CHECK_ARG(B > 0 && F > 0 && F % 4 == 0 && ldo % 4 == 0 && src.stride % 4 == 0,
+                "silu_mul: F, ldo must be multiples of 4");
+  const long long total = (long long)B * (F / 4);
+  return launch_k(silu_mul_kernel, dim3(grid_for(total, 128, 4 * kNumSMs)), dim3(128), 0, st, true, src, B, F,
+                  reinterpret_cast<__nv_bfloat16*>(out), ldo);
 }
 
-int argmax_stage1(const SrcList& src, int B, int V, int vocab_offset, int nchunk, void* cand,
-                  const SignalSpec& sig, cudaStream_t st) {
+int argmax_stage1(const Src& src, int B, int V, int vocab_offset, int nchunk, void* cand, const SignalSpec& sig,
+                  cudaStream_t st) {
   TPS_CHECK_ARG(B > 0 && V > 0 && nchunk > 0, "argmax_stage1: bad shape");
-  dim3 grid(B, nchunk);
-  argmax_stage1_kernel<<<grid, kArgmaxThreads, 0, st>>>(src, B, V, vocab_offset, nchunk,
-                                                        reinterpret_cast<ArgmaxCand*>(cand), sig);
-  TPS_LAUNCH_CHECK();
-  return kOk;
+  return launch_k(argmax_stage1_kernel, dim3(B, nchunk), dim3(kArgmaxThreads), 0, st, true, src, B, V,
+                  vocab_offset, nchunk, reinterpret_cast<ArgmaxCand*>(cand), sig);
 }
 
 int argmax_finalize(const CandList& cands, int nchunk, const WaitSpec& wait, int B, const int* row_slot,
                     int* pos_by_slot, const int* prompt_len, int* history, int hist_ld, int* out_tok,
                     cudaStream_t st) {
   TPS_CHECK_ARG(B > 0 && cands.n >= 1 && cands.n <= kMaxPeers, "argmax_finalize: bad args");
-  argmax_finalize_kernel<<<B, 32, 0, st>>>(cands, nchunk, wait, row_slot, pos_by_slot, prompt_len, history,
-                                           hist_ld, out_tok);
-  TPS_LAUNCH_CHECK();
-  return kOk;
+  return launch_k(argmax_finalize_kernel, dim3(B), dim3(32), 0, st, true, cands, nchunk, wait, row_slot,
+                  pos_by_slot, prompt_len, history, hist_ld, out_tok);
 }
 
 int epoch_advance(uint64_t* epoch, cudaStream_t st) {
-  epoch_advance_kernel<<<1, 1, 0, st>>>(epoch);
-  TPS_LAUNCH_CHECK();
-  return kOk;
+  return launch_k(epoch_advance_kernel, dim3(1), dim3(1), 0, st, true, epoch);
 }
 
-int sum_src(const SrcList& src, int64_t n, float* out, cudaStream_t st) {
-  int blocks = (int)((n + 255) / 256);
-  if (blocks > 4 * kNumSMs) blocks = 4 * kNumSMs;
-  if (blocks < 1) blocks = 1;
-  sum_src_kernel<<<blocks, 256, 0, st>>>(src, n, out);
-  TPS_LAUNCH_CHECK();
-  return kOk;
+int sum_src(const Src& src, long long n, float* out, cudaStream_t st) {
+  return launch_k(sum_src_kernel, dim3(grid_for(n, 256, 4 * kNumSMs)), dim3(256), 0, st, false, src, n, out);
 }
 
 }  // namespace tps

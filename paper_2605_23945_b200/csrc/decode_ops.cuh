@@ -1,18 +1,22 @@
-// Parameter structs shared by the decode kernels and the C-ABI layer.
+// Parameter structs and launch helpers shared by the decode kernels and the C-ABI layer.
 #pragma once
 #include <stdint.h>
 
+#include <utility>
+
+#include "common.cuh"
+
 namespace tps {
 
-constexpr int kMaxSrc = 64;
 constexpr int kMaxPeers = 8;
 
-// An ordered list of fp32 [rows][cols] partial buffers to be summed
-// (split-K partials of one rank, or one slot per TP rank). Summation order
-// is the list order, so every rank of a TP group reduces bitwise-identically.
-struct SrcList {
-  const float* p[kMaxSrc];
+// n fp32 buffers at base + i*stride (elements), summed in index order: the
+// split-K partials of one projection, or one receive slot per TP rank. Fixed
+// order keeps every rank of a TP group bitwise identical.
+struct Src {
+  const float* base;
   int n;
+  long long stride;
 };
 
 // Cross-GPU completion counter wait: spin until *ctr >= (*epoch) * mult + add
@@ -25,8 +29,6 @@ struct WaitSpec {
   uint64_t add;
 };
 
-// After a CTA's stores are globally visible, add 1 to each listed counter
-// (local or NVLink-peer), with release semantics at system scope.
 // The last CTA of the launch (detected with the per-launch-site `done` counter,
 // which it resets) issues the signals, so each rank contributes exactly one
 // arrival per phase regardless of grid size / batch bucket.
@@ -52,5 +54,34 @@ struct CandList {
   const ArgmaxCand* p[kMaxPeers];
   int n;
 };
+
+// ----------------------------------------------- programmatic dependent launch
+// Decode-step kernels are launched with the PDL attribute: each calls
+// pdl_launch_dependents() early (the next kernel may start its prologue) and
+// pdl_wait() before touching data produced or consumed by its predecessors.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+int launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl,
+             Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (pdl && pdl_enabled()) ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+  if (e != cudaSuccess) return fail(kCuda, std::string("launch: ") + cudaGetErrorString(e));
+  return kOk;
+}
 
 }  // namespace tps

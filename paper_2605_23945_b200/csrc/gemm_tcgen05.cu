@@ -24,6 +24,7 @@
 #include <tuple>
 
 #include "common.cuh"
+#include "decode_ops.cuh"
 
 namespace tps {
 
@@ -128,6 +129,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_launch_dependents();
+  if (warp >= 4) pdl_wait();  // epilogue writes the partial buffer the predecessor may still read
 
   if (warp == 0) {
     if (lane == 0) {
@@ -136,11 +139,34 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint64_t pol_x = policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
+      // Weights are never produced by the preceding decode kernels: stream the
+      // first unit's weight tiles into the ring *before* the programmatic
+      // dependency wait, so this kernel's HBM stream starts while its
+      // predecessor is still running; only the activation loads wait.
+      int pre = 0;
+      if ((int)blockIdx.x < units) {
+        const int u = blockIdx.x;
+        const int tile = u / splits, split = u % splits;
+        const int c0 = (int)((long long)split * chunks / splits);
+        const int c1 = (int)((long long)(split + 1) * chunks / splits);
+        pre = min(S, c1 - c0);
+        for (int i = 0; i < pre; ++i) {
+          mbar_arrive_expect_tx(&full[i], Cfg::kStageBytes);
+          tma_load_2d(smem_a + i * Cfg::kABytes, &tmap_w, &full[i], (c0 + i) * kBK, tile * kBM, pol_w);
+        }
+        pdl_wait();
+        for (int i = 0; i < pre; ++i)
+          tma_load_2d(smem_b + i * Cfg::kBBytes, &tmap_x, &full[i], (c0 + i) * kBK, 0, pol_x);
+        stage = pre % S;
+        phase = (pre == S) ? 1u : 0u;
+      } else {
+        pdl_wait();
+      }
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         const int tile = u / splits, split = u % splits;
         const int c0 = (int)((long long)split * chunks / splits);
         const int c1 = (int)((long long)(split + 1) * chunks / splits);
-        for (int c = c0; c < c1; ++c) {
+        for (int c = (u == (int)blockIdx.x ? c0 + pre : c0); c < c1; ++c) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
           tma_load_2d(smem_a + stage * Cfg::kABytes, &tmap_w, &full[stage], c * kBK, tile * kBM, pol_w);
@@ -313,10 +339,8 @@ static int launch_gemm(const CUtensorMap& mw, const CUtensorMap& mx, float* out,
   using Cfg = GemmCfg<BN>;
   const int units = tiles * splits;
   const int grid = units < kNumSMs ? units : kNumSMs;
-  gemm_swapab_kernel<BN><<<grid, kGemmThreads, Cfg::kSmemBytes, stream>>>(mw, mx, out, n, b, tiles, splits,
-                                                                         chunks);
-  TPS_LAUNCH_CHECK();
-  return kOk;
+  return launch_k(gemm_swapab_kernel<BN>, dim3(grid), dim3(kGemmThreads), Cfg::kSmemBytes, stream, true, mw, mx,
+                  out, n, b, tiles, splits, chunks);
 }
 
 template <int BN>

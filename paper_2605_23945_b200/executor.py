@@ -143,12 +143,12 @@ class InferExecutor:
         self.att_m = torch.zeros(max_batch * self.nq * nsplit, dtype=torch.float32, device=dev)
         self.att_l = torch.zeros_like(self.att_m)
         self.att_o = torch.zeros(max_batch * self.nq * nsplit * D, dtype=torch.float32, device=dev)
+        self.att_ctr = torch.zeros(max_batch * self.nkv, dtype=torch.int32, device=dev)
         self.local_cand = torch.zeros((max_batch, 64, 2), dtype=torch.int32, device=dev)
         self.out_tok = torch.zeros(max_batch, dtype=torch.int32, device=dev)
         self.row_slot = {B: torch.full((B,), -1, dtype=torch.int32, device=dev) for B in self.buckets()}
         self.graphs: dict[int, torch.cuda.CUDAGraph] = {}
         self.launch_stats: dict[int, LaunchStats] = {}
-        self._keep = []  # ctypes arrays alive during capture
 
     # ------------------------------------------------------------ shapes ---
     def buckets(self) -> list[int]:
@@ -172,14 +172,14 @@ class InferExecutor:
     def _splits(self, n: int, k: int, B: int) -> int:
         return nat.lib().tps_linear_splits(n, k, B)
 
-    def _linear(self, st, stats, w: torch.Tensor, x: torch.Tensor, B: int) -> list[int]:
+    def _linear(self, st, stats, w: torch.Tensor, x: torch.Tensor, B: int) -> tuple[int, int, int]:
+        """Projection into the split-K workspace; returns the strided source (base, n, stride)."""
         n, k = w.shape
         s = self._splits(n, k, B)
         nat.check(nat.lib().tps_linear(w.data_ptr(), n, k, k, x.data_ptr(), B, x.shape[0],
                                        x.shape[1], self.ws.data_ptr(), s, st), "tps_linear")
         stats.add("linear")
-        base = self.ws.data_ptr()
-        return [base + i * B * n * 4 for i in range(s)]
+        return (self.ws.data_ptr(), s, B * n)
 
     @staticmethod
     def _arr(ptrs):
@@ -203,7 +203,7 @@ class InferExecutor:
         nat.check(lib.tps_embed(rs, pos, hist, sl.max_len, W.tensor_ptr(-1, "embed"), H, B,
                                 self.resid.data_ptr(), st), "tps_embed")
         stats.add("embed")
-        nat.check(lib.tps_add_norm(self.resid.data_ptr(), None, 0, None, W.tensor_ptr(0, "ln1"), eps,
+        nat.check(lib.tps_add_norm(self.resid.data_ptr(), None, 0, 0, None, W.tensor_ptr(0, "ln1"), eps,
                                    H, B, self.xn.data_ptr(), H, st), "tps_add_norm")
         stats.add("add_norm")
         nsplit = lib.tps_attn_splits(B, self.nkv, sl.max_pages)
@@ -211,7 +211,7 @@ class InferExecutor:
             srcs = self._linear(st, stats, W[(l, "w_qkv")], self.xn, B)
             kc, vc = self.kv.layer_ptrs(l)
             bias = W.tensor_ptr(l, "b_qkv") if g.qkv_bias else None
-            nat.check(lib.tps_qkv_rope_append(self._arr(srcs), len(srcs), bias, rs, pos,
+            nat.check(lib.tps_qkv_rope_append(*srcs, bias, rs, pos,
                                               sl.page_table.data_ptr(), sl.max_pages,
                                               self.cos.data_ptr(), self.sin.data_ptr(), B, self.nq,
                                               self.nkv, D, PAGE, self.q.data_ptr(), kc, vc, st),
@@ -220,13 +220,14 @@ class InferExecutor:
             nat.check(lib.tps_paged_attention(self.q.data_ptr(), kc, vc, rs, pos, sl.page_table.data_ptr(),
                                               sl.max_pages, B, self.nq, self.nkv, D, nsplit,
                                               self.att_m.data_ptr(), self.att_l.data_ptr(),
-                                              self.att_o.data_ptr(), self.attn.data_ptr(), st),
+                                              self.att_o.data_ptr(), self.att_ctr.data_ptr(),
+                                              self.attn.data_ptr(), st),
                       "tps_paged_attention")
-            stats.add("paged_attention", 2)
+            stats.add("paged_attention")
             srcs = self._linear(st, stats, W[(l, "w_o")], self.attn, B)
             yield from self._allreduce_norm(st, stats, 2 * l, srcs, B, W.tensor_ptr(l, "ln2"))
             srcs = self._linear(st, stats, W[(l, "w_gu")], self.xn, B)
-            nat.check(lib.tps_silu_mul(self._arr(srcs), len(srcs), B, self.F, self.act.data_ptr(), self.F, st),
+            nat.check(lib.tps_silu_mul(*srcs, B, self.F, self.act.data_ptr(), self.F, st),
                       "tps_silu_mul")
             stats.add("silu_mul")
             srcs = self._linear(st, stats, W[(l, "w_d")], self.act, B)
@@ -237,7 +238,7 @@ class InferExecutor:
         nch = argmax_chunks(B)
         cm = self.comm
         if cm is None:
-            nat.check(lib.tps_argmax_stage1(self._arr(srcs), len(srcs), B, self.V, self.shard.vocab[0], nch,
+            nat.check(lib.tps_argmax_stage1(*srcs, B, self.V, self.shard.vocab[0], nch,
                                             self.local_cand.data_ptr(), None, 0, None, st), "tps_argmax_stage1")
             stats.add("argmax_stage1")
             cands = [self.local_cand.data_ptr()]
@@ -245,7 +246,7 @@ class InferExecutor:
         else:
             ph = 2 * L
             sigs = [p + ph * 8 for p in cm.peer_ctr]
-            nat.check(lib.tps_argmax_stage1(self._arr(srcs), len(srcs), B, self.V, self.shard.vocab[0], nch,
+            nat.check(lib.tps_argmax_stage1(*srcs, B, self.V, self.shard.vocab[0], nch,
                                             cm.cand.data_ptr(), self._arr(sigs), len(sigs),
                                             cm.done.data_ptr() + ph * 4, st), "tps_argmax_stage1")
             stats.add("argmax_stage1")
@@ -260,28 +261,28 @@ class InferExecutor:
             nat.check(lib.tps_epoch_advance(cm.epoch.data_ptr(), st), "tps_epoch_advance")
             stats.add("epoch_advance")
 
-    def _allreduce_norm(self, st, stats, phase: int, srcs: list[int], B: int, norm_w: int):
+    def _allreduce_norm(self, st, stats, phase: int, srcs: tuple[int, int, int], B: int, norm_w: int):
         lib = nat.lib()
         g = self.geom
         H = g.hidden
         eps = ctypes.c_float(g.rms_eps)
         cm = self.comm
         if cm is None:
-            nat.check(lib.tps_add_norm(self.resid.data_ptr(), self._arr(srcs), len(srcs), None, norm_w, eps, H,
+            nat.check(lib.tps_add_norm(self.resid.data_ptr(), *srcs, None, norm_w, eps, H,
                                        B, self.xn.data_ptr(), H, st), "tps_add_norm")
             stats.add("add_norm")
             return
         par = phase % 2
         dsts = [cm.recv_slot(base, par, self.rank) for base in cm.peer_recv]
         sigs = [p + phase * 8 for p in cm.peer_ctr]
-        nat.check(lib.tps_reduce_push(self._arr(srcs), len(srcs), self._arr(dsts), len(dsts), B * H,
+        nat.check(lib.tps_reduce_push(*srcs, self._arr(dsts), len(dsts), B * H,
                                       self._arr(sigs), len(sigs), cm.done.data_ptr() + phase * 4, st),
                   "tps_reduce_push")
         stats.add("reduce_push")
         yield
-        mine = [cm.recv_slot(cm.recv.data_ptr(), par, r) for r in range(cm.tp)]
+        mine = (cm.recv_slot(cm.recv.data_ptr(), par, 0), cm.tp, cm.max_batch * H)
         wait = nat.wait_spec(cm.ctr.data_ptr() + phase * 8, cm.epoch.data_ptr(), cm.tp, 0)
-        nat.check(lib.tps_add_norm(self.resid.data_ptr(), self._arr(mine), len(mine), wait, norm_w, eps, H, B,
+        nat.check(lib.tps_add_norm(self.resid.data_ptr(), *mine, wait, norm_w, eps, H, B,
                                    self.xn.data_ptr(), H, st), "tps_add_norm")
         stats.add("add_norm")
 

@@ -110,7 +110,7 @@ def last_logits(ranks: list[RankState]) -> torch.Tensor:
         ex = r.executor
         srcs, B = ex._last_lm_srcs
         out = torch.empty((B, ex.V), dtype=torch.float32, device=ex.device)
-        nat.check(nat.lib().tps_sum_partials(nat.ptr_array(srcs), len(srcs), B * ex.V, out.data_ptr(),
+        nat.check(nat.lib().tps_sum_partials(*srcs, B * ex.V, out.data_ptr(),
                                              torch.cuda.current_stream().cuda_stream), "tps_sum_partials")
         outs.append(out)
     return torch.cat(outs, dim=1)

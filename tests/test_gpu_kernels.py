@@ -89,6 +89,7 @@ def test_paged_attention_matches_fp32(D, nq, nkv, ctxs):
     pos = torch.tensor([c - 1 for c in ctxs], dtype=torch.int32, device="cuda")
     q = torch.randn(B, nq, D, device="cuda").bfloat16()
     lib = nat.lib()
+    ctr = torch.zeros(B * nkv, dtype=torch.int32, device="cuda")
     for nsplit in (1, lib.tps_attn_splits(B, nkv, max_pages), 7):
         pm = torch.empty(B * nq * nsplit, device="cuda")
         pl = torch.empty_like(pm)
@@ -96,13 +97,14 @@ def test_paged_attention_matches_fp32(D, nq, nkv, ctxs):
         out = torch.empty(B, nq, D, device="cuda", dtype=torch.bfloat16)
         nat.check(lib.tps_paged_attention(q.data_ptr(), kc.data_ptr(), vc.data_ptr(), row_slot.data_ptr(),
                                           pos.data_ptr(), page_table.data_ptr(), max_pages, B, nq, nkv, D,
-                                          nsplit, pm.data_ptr(), pl.data_ptr(), po.data_ptr(), out.data_ptr(),
+                                          nsplit, pm.data_ptr(), pl.data_ptr(), po.data_ptr(), ctr.data_ptr(), out.data_ptr(),
                                           _stream()))
         torch.cuda.synchronize()
         ref = _ref_attention(q.cpu(), kc.cpu(), vc.cpu(), perm.tolist(), [c - 1 for c in ctxs], nq // nkv)
         err = (out.float().cpu() - ref).abs().max().item()
         # P is rounded to bf16 before the PV product; outputs are O(1)
         assert err < 2e-2, (nsplit, err)
+        assert int(ctr.sum()) == 0  # merge counters re-armed by the last CTA
 
 
 def test_padding_rows_are_inert():
@@ -116,9 +118,10 @@ def test_padding_rows_are_inert():
     pm = torch.empty(2 * nq * 3, device="cuda")
     pl, po = torch.empty_like(pm), torch.empty(2 * nq * 3 * D, device="cuda")
     out = torch.full((2, nq, D), 7.0, device="cuda", dtype=torch.bfloat16)
+    ctr = torch.zeros(2 * nkv, dtype=torch.int32, device="cuda")
     nat.check(nat.lib().tps_paged_attention(q.data_ptr(), kc.data_ptr(), vc.data_ptr(), row_slot.data_ptr(),
                                             pos.data_ptr(), page_table.data_ptr(), 2, 2, nq, nkv, D, 3,
-                                            pm.data_ptr(), pl.data_ptr(), po.data_ptr(), out.data_ptr(),
+                                            pm.data_ptr(), pl.data_ptr(), po.data_ptr(), ctr.data_ptr(), out.data_ptr(),
                                             _stream()))
     torch.cuda.synchronize()
     assert (out[0] == 0).all()
