@@ -1,0 +1,72 @@
+"""CPU ORACLE -- test infrastructure only (tests/, smoke(), bench cpu_baseline); never product code.
+
+Restates the Switch Executor's data-movement semantics on the CPU:
+
+* canonical target shards (tpshift/reshard.py:25-43 ShardLayout.rank_slice,
+  applied per tensor family with the GQA head rule of decoder_ref.partition):
+  the bytes every target rank must hold after a weight reshard;
+* merge-first KV migration (tpshift/reshard.py:113-151): after the switch a
+  sample's K/V for kv head h, layer l, token t equals its value before the
+  switch, whichever rank held it;
+* a byte-addressed memory simulator that executes copy items
+  (src_ptr, dst_ptr, bytes) exactly like tps_copy_items, so a plan can be
+  executed on the CPU and its result compared byte-for-byte.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from .decoder_ref import partition
+
+
+def expected_shard(geo: dict, full: dict, tp: int, rank: int, layer: int, family: str) -> torch.Tensor:
+    """The canonical shard of one tensor (bf16) for TP rank `rank` of `tp`."""
+    p = partition(geo, tp, rank)
+    D, nq, nkv, F = geo["head_dim"], geo["n_q"], geo["n_kv"], geo["ffn"]
+    t = full[(layer, family)]
+    q0, q1 = p["q"]
+    k0, k1 = p["kv"]
+    if family in ("w_qkv", "b_qkv"):
+        idx = list(range(q0 * D, q1 * D)) + list(range((nq + k0) * D, (nq + k1) * D)) + \
+            list(range((nq + nkv + k0) * D, (nq + nkv + k1) * D))
+        return t[torch.tensor(idx)]
+    if family == "w_o":
+        return t[:, q0 * D:q1 * D]
+    if family == "w_gu":
+        f0, f1 = p["ffn"]
+        return torch.cat([t[f0:f1], t[F + f0:F + f1]], dim=0)
+    if family == "w_d":
+        f0, f1 = p["ffn"]
+        return t[:, f0:f1]
+    if family == "lm_head":
+        v0, v1 = p["vocab"]
+        return t[v0:v1]
+    return t  # replicated: norms, embedding
+
+
+class ByteMemory:
+    """Sparse byte-addressed memory: named buffers at fake base addresses."""
+
+    def __init__(self):
+        self.bufs: list[tuple[int, np.ndarray]] = []
+        self._next = 1 << 40
+
+    def alloc(self, nbytes: int) -> int:
+        base = self._next
+        self.bufs.append((base, np.zeros(nbytes, dtype=np.uint8)))
+        self._next += ((nbytes + (1 << 20)) >> 20 << 20) + (1 << 30)
+        return base
+
+    def view(self, ptr: int, nbytes: int) -> np.ndarray:
+        for base, arr in self.bufs:
+            if base <= ptr and ptr + nbytes <= base + arr.size:
+                return arr[ptr - base: ptr - base + nbytes]
+        raise IndexError(f"address {ptr:#x}+{nbytes} is outside every buffer")
+
+    def execute(self, items: np.ndarray) -> None:
+        """Apply copy items (read everything first: items of one launch never alias)."""
+        data = [self.view(int(s), int(n)).copy() for s, _, n, _ in items]
+        for (s, d, n, _), blob in zip(items, data):
+            self.view(int(d), int(n))[:] = blob

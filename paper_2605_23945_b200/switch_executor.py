@@ -1,0 +1,273 @@
+"""Switch Executor: reshard a running decode from (tp, dp) to (tp', dp') on B200.
+
+Implements the switch seam (_commit_switch, tpshift/engine.py:206-269) for
+real. The reference prices -- and PAT executes -- a layer-wise All-Gather +
+Slice (tpshift/reshard.py:80-151). Here every *target* rank
+pulls exactly the canonical slices it owns, one-sided, from whichever rank
+holds them: itself when the slice is already resident (no NVLink traffic),
+otherwise a peer over NVLink (CUDA-IPC mapped pointers), with sources spread
+across the old DP replicas. The result is the same canonical layout the
+gather+slice would produce (rank semantics preserved), so the
+transfer is copy-only and bit-exact.
+
+Three pull plans, all pure functions of (geometry, layouts, placements):
+  weights  every tensor family of every layer (QKV rows incl. the uneven
+           query-head split, O columns, gate/up rows, down columns, LM-head
+           vocab rows, replicated norms/embedding);
+  KV       per migrated sample, layer, K|V, valid page and target kv head:
+           one contiguous page_size x head_dim chunk (merge-first: samples
+           land in the groups assign_merged_groups chose);
+  state    token history rows (the sampler state of greedy decoding is the
+           history; positions / prompt lengths are host-known).
+Plans become 32-byte copy items (tps_copy_item) executed by tps_copy_items;
+`verify_cover` checks that the items cover every target byte exactly once.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .errors import PlanVerificationError
+from .kvcache import PAGE, pages_for
+from .models import (GLOBAL_FAMILIES, DecoderGeometry, full_shape, layer_families, rank_shard, shard_ranges)
+from .shards import arena_layout
+
+REPLICATED = ("ln1", "ln2", "ln_f", "embed")
+
+
+@dataclass(frozen=True)
+class Layout:
+    tp: int
+    world: int
+
+    @property
+    def dp(self) -> int:
+        return self.world // self.tp
+
+    def group_of(self, rank: int) -> int:
+        return rank // self.tp
+
+    def tp_rank(self, rank: int) -> int:
+        return rank % self.tp
+
+    def ranks_of_group(self, g: int) -> list[int]:
+        return list(range(g * self.tp, (g + 1) * self.tp))
+
+
+@dataclass
+class Pieces:
+    """Byte-level copy pieces: parallel int64 arrays (src_rank, src_off, dst_off, nbytes)."""
+
+    src_rank: list = field(default_factory=list)
+    src_off: list = field(default_factory=list)
+    dst_off: list = field(default_factory=list)
+    nbytes: list = field(default_factory=list)
+
+    def add(self, src_rank, src_off, dst_off, nbytes):
+        self.src_rank.append(np.asarray(src_rank, dtype=np.int64).ravel())
+        self.src_off.append(np.asarray(src_off, dtype=np.int64).ravel())
+        self.dst_off.append(np.asarray(dst_off, dtype=np.int64).ravel())
+        self.nbytes.append(np.asarray(nbytes, dtype=np.int64).ravel())
+
+    def arrays(self):
+        if not self.src_rank:
+            z = np.zeros(0, dtype=np.int64)
+            return z, z, z, z
+        return (np.concatenate(self.src_rank), np.concatenate(self.src_off), np.concatenate(self.dst_off),
+                np.concatenate(self.nbytes))
+
+
+def _storage_runs(ranges):
+    """[(a, b, storage_offset)] for ranges concatenated in storage order."""
+    out, off = [], 0
+    for a, b in ranges:
+        out.append((a, b, off))
+        off += b - a
+    return out
+
+
+def _pick_source(holders: list[int], dst_rank: int, salt: int) -> int:
+    """Prefer the target rank itself (local copy); otherwise spread over the replicas."""
+    if dst_rank in holders:
+        return dst_rank
+    return holders[(dst_rank + salt) % len(holders)]
+
+
+def plan_weight_pulls(geom: DecoderGeometry, old: Layout, new: Layout, dst_rank: int) -> Pieces:
+    """Pieces that fill `dst_rank`'s new arena from the old arenas (offsets are arena bytes)."""
+    new_sh = rank_shard(geom, new.tp, new.tp_rank(dst_rank))
+    new_arena = arena_layout(geom, new_sh)
+    old_sh = [rank_shard(geom, old.tp, r) for r in range(old.tp)]
+    old_arena = [arena_layout(geom, s) for s in old_sh]
+    pieces = Pieces()
+    salt = 0
+    for (layer, fam), (dst_base, dst_shape) in new_arena.entries.items():
+        full = full_shape(geom, fam)
+        if fam in REPLICATED:
+            holders = list(range(old.world))
+            src = _pick_source(holders, dst_rank, salt)
+            sbase = old_arena[old.tp_rank(src)].entries[(layer, fam)][0]
+            pieces.add(src, sbase, dst_base, 2 * int(np.prod(dst_shape)))
+            salt += 1
+            continue
+        axis, dst_ranges = shard_ranges(geom, fam, new_sh)
+        row_elems = full[1] if len(full) == 2 else 1
+        for a, b, doff in _storage_runs(dst_ranges):
+            # candidate sources: every old tp-rank run intersecting [a, b); replicated
+            # KV heads appear on several tp-ranks, so sweep and take each byte once,
+            # preferring a run that is resident on the target rank itself
+            cands = []
+            for otr in range(old.tp):
+                _, src_ranges = shard_ranges(geom, fam, old_sh[otr])
+                for c, d, soff in _storage_runs(src_ranges):
+                    x, y = max(a, c), min(b, d)
+                    if x < y:
+                        local = any(g * old.tp + otr == dst_rank for g in range(old.dp))
+                        cands.append((x, 0 if local else 1, y, otr, c, soff))
+            cands.sort()
+            pos = a
+            for x, _, y, otr, c, soff in cands:
+                x = max(x, pos)
+                if x >= y:
+                    continue
+                pos = y
+                if True:
+                    holders = [g * old.tp + otr for g in range(old.dp)]
+                    src = _pick_source(holders, dst_rank, salt)
+                    salt += 1
+                    sbase = old_arena[otr].entries[(layer, fam)][0]
+                    s_lo, d_lo, w = soff + (x - c), doff + (x - a), y - x
+                    if axis == 0 or len(full) == 1:
+                        pieces.add(src, sbase + 2 * s_lo * row_elems, dst_base + 2 * d_lo * row_elems,
+                                   2 * w * row_elems)
+                    else:  # column slice of a row-major [rows][cols] tensor: one piece per row
+                        rows = full[0]
+                        src_ld = old_arena[otr].entries[(layer, fam)][1][1]
+                        dst_ld = dst_shape[1]
+                        r = np.arange(rows, dtype=np.int64)
+                        pieces.add(np.full(rows, src), sbase + 2 * (r * src_ld + s_lo),
+                                   dst_base + 2 * (r * dst_ld + d_lo), np.full(rows, 2 * w))
+    return pieces
+
+
+@dataclass(frozen=True)
+class KVSource:
+    """Where a migrating sample lives before the switch (on every rank of its old group)."""
+
+    old_group: int
+    slot: int
+    pages: tuple[int, ...]
+
+
+@dataclass(frozen=True)
+class KVTarget:
+    slot: int
+    pages: tuple[int, ...]
+
+
+def kv_chunk_offset(geom: DecoderGeometry, n_kv_local: int, num_pages: int, layer: int, kv: int, page: int,
+                    head: int) -> int:
+    """Byte offset of a (layer, k|v, page, head) chunk in a pool [L][2][pages][nkv][64][D]."""
+    chunk = PAGE * geom.head_dim * 2
+    return ((((layer * 2 + kv) * num_pages + page) * n_kv_local + head) * chunk)
+
+
+def plan_kv_pulls(geom: DecoderGeometry, old: Layout, new: Layout, dst_rank: int, sources: list[KVSource],
+                  targets: list[KVTarget], ctx_lens: list[int], old_num_pages: int, new_num_pages: int) -> Pieces:
+    """KV chunk pieces for the samples placed on dst_rank's new group (offsets are pool bytes).
+
+    Each sample's valid pages (ceil(ctx/64)) of every layer, K and V, and every
+    kv head the target rank owns are pulled from a rank of the sample's old
+    group that holds that head (itself if possible).
+    """
+    new_sh = rank_shard(geom, new.tp, new.tp_rank(dst_rank))
+    old_shards = [rank_shard(geom, old.tp, r) for r in range(old.tp)]
+    L = geom.num_layers
+    pieces = Pieces()
+    chunk = PAGE * geom.head_dim * 2
+    for src, tgt, ctx in zip(sources, targets, ctx_lens):
+        npg = pages_for(ctx)
+        if npg == 0:
+            continue
+        for h in range(*new_sh.kv_heads):
+            holders = [src.old_group * old.tp + r for r in range(old.tp)
+                       if old_shards[r].kv_heads[0] <= h < old_shards[r].kv_heads[1]]
+            src_rank = _pick_source(holders, dst_rank, h)
+            osh = old_shards[old.tp_rank(src_rank)]
+            sh_ = h - osh.kv_heads[0]
+            dh_ = h - new_sh.kv_heads[0]
+            l = np.arange(L, dtype=np.int64)[:, None, None]
+            kv = np.arange(2, dtype=np.int64)[None, :, None]
+            sp = np.asarray(src.pages[:npg], dtype=np.int64)[None, None, :]
+            dp = np.asarray(tgt.pages[:npg], dtype=np.int64)[None, None, :]
+            soff = ((((l * 2 + kv) * old_num_pages + sp) * osh.n_kv + sh_) * chunk)
+            doff = ((((l * 2 + kv) * new_num_pages + dp) * new_sh.n_kv + dh_) * chunk)
+            n = soff.size
+            pieces.add(np.full(n, src_rank), soff, doff, np.full(n, chunk))
+    return pieces
+
+
+def plan_history_pulls(old: Layout, dst_rank: int, sources: list[KVSource], targets: list[KVTarget],
+                       lens: list[int], old_hist_ld: int, new_hist_ld: int) -> Pieces:
+    """Token-history rows (prompt + generated so far) of the migrating samples."""
+    pieces = Pieces()
+    for src, tgt, n in zip(sources, targets, lens):
+        holders = old.ranks_of_group(src.old_group)
+        s = _pick_source(holders, dst_rank, 0)
+        pieces.add(s, 4 * src.slot * old_hist_ld, 4 * tgt.slot * new_hist_ld, 4 * n)
+    return pieces
+
+
+def to_items(pieces: Pieces, src_base: dict[int, int], dst_base: int, max_chunk: int = 1 << 16) -> np.ndarray:
+    """Copy items [n, 4] int64 (src_ptr, dst_ptr, bytes, 0), large pieces split to <= max_chunk."""
+    sr, so, do, nb = pieces.arrays()
+    if sr.size == 0:
+        return np.zeros((0, 4), dtype=np.int64)
+    bases = np.array([src_base[int(r)] for r in sr], dtype=np.int64) if sr.size < 4096 else \
+        np.vectorize(lambda r: src_base[int(r)], otypes=[np.int64])(sr)
+    nsplit = (nb + max_chunk - 1) // max_chunk
+    idx = np.repeat(np.arange(sr.size), nsplit)
+    first = np.repeat(np.cumsum(nsplit) - nsplit, nsplit)
+    k = np.arange(idx.size) - first
+    off = k * max_chunk
+    items = np.zeros((idx.size, 4), dtype=np.int64)
+    items[:, 0] = bases[idx] + so[idx] + off
+    items[:, 1] = dst_base + do[idx] + off
+    items[:, 2] = np.minimum(max_chunk, nb[idx] - off)
+    return items
+
+
+def verify_cover(pieces: Pieces, total_bytes: int, allow_gaps: bool = False) -> list[str]:
+    """Every destination byte in [0, total_bytes) written at most once (exactly once unless allow_gaps)."""
+    _, _, do, nb = pieces.arrays()
+    issues = []
+    if do.size == 0:
+        return [] if (allow_gaps or total_bytes == 0) else ["empty plan"]
+    order = np.argsort(do, kind="stable")
+    d, n = do[order], nb[order]
+    if np.any(n <= 0):
+        issues.append("non-positive piece size")
+    ends = d + n
+    if np.any(d[1:] < ends[:-1]):
+        issues.append("overlapping destination pieces")
+    if np.any(ends > total_bytes) or np.any(d < 0):
+        issues.append("piece outside the destination buffer")
+    if not allow_gaps:
+        covered = int(n.sum())
+        if covered != total_bytes:
+            issues.append(f"covers {covered} of {total_bytes} bytes")
+    return issues
+
+
+def nvlink_bytes(pieces: Pieces, dst_rank: int) -> tuple[int, int]:
+    """(bytes pulled from peers, bytes copied locally)."""
+    sr, _, _, nb = pieces.arrays()
+    remote = int(nb[sr != dst_rank].sum())
+    return remote, int(nb.sum()) - remote
+
+
+def check(issues: list[str], what: str) -> None:
+    if issues:
+        raise PlanVerificationError(f"{what}: " + "; ".join(issues))

@@ -1,0 +1,165 @@
+"""CPU parity of the Switch Executor's pull plans against the oracle restatement.
+
+Every (tp -> tp') transition over a simulated 8-GPU node: old arenas are filled
+with the canonical shards of seeded full weights, the target rank's copy items
+are executed on a byte-addressed CPU memory, and the result must equal the
+oracle's canonical target shards byte for byte (bit-exact reshard). KV pages
+and token histories are checked the same way after a merge-and-redistribute.
+"""
+
+import itertools
+
+import numpy as np
+import pytest
+import torch
+
+from oracle.decoder_ref import numpy_weights
+from oracle.reshard_ref import ByteMemory, expected_shard
+from paper_2605_23945_b200.models import geometry, rank_shard
+from paper_2605_23945_b200.shards import arena_layout
+from paper_2605_23945_b200.switch_executor import (KVSource, KVTarget, Layout, kv_chunk_offset, nvlink_bytes,
+                                                   plan_history_pulls, plan_kv_pulls, plan_weight_pulls,
+                                                   to_items, verify_cover)
+
+GEOS = {name: geometry(name) for name in ("tiny", "mini-qwen")}
+
+
+def geo_dict(g):
+    return dict(num_layers=g.num_layers, hidden=g.hidden, n_q=g.n_q, n_kv=g.n_kv, head_dim=g.head_dim,
+                ffn=g.ffn, vocab=g.vocab, qkv_bias=g.qkv_bias, rope_theta=g.rope_theta, rms_eps=g.rms_eps)
+
+
+def _bytes(t: torch.Tensor) -> np.ndarray:
+    return t.contiguous().view(torch.int16).numpy().view(np.uint8).ravel()
+
+
+def fill_arena(mem, base, geom, geo, full, tp, rank):
+    lay = arena_layout(geom, rank_shard(geom, tp, rank))
+    for (layer, fam), (off, shape) in lay.entries.items():
+        blob = _bytes(expected_shard(geo, full, tp, rank, layer, fam).to(torch.bfloat16))
+        mem.view(base + off, blob.size)[:] = blob
+
+
+def valid_tps(geom):
+    out = []
+    for tp in (1, 2, 4, 8):
+        try:
+            geom.check_tp(tp)
+            out.append(tp)
+        except Exception:
+            pass
+    return out
+
+
+@pytest.mark.parametrize("name", sorted(GEOS))
+def test_weight_reshard_bit_exact_all_transitions(name):
+    geom = GEOS[name]
+    geo = geo_dict(geom)
+    full = {k: v.to(torch.bfloat16) for k, v in numpy_weights(geo, 5).items()}
+    world = 8
+    tps = valid_tps(geom)
+    assert len(tps) >= 3
+    for t_old, t_new in itertools.product(tps, tps):
+        if t_old == t_new:
+            continue
+        old, new = Layout(t_old, world), Layout(t_new, world)
+        mem = ByteMemory()
+        old_base = {}
+        for r in range(world):
+            lay = arena_layout(geom, rank_shard(geom, t_old, r % t_old))
+            old_base[r] = mem.alloc(lay.total_bytes)
+            fill_arena(mem, old_base[r], geom, geo, full, t_old, r % t_old)
+        remote_total = 0
+        for dst in range(world):
+            lay = arena_layout(geom, rank_shard(geom, t_new, dst % t_new))
+            pieces = plan_weight_pulls(geom, old, new, dst)
+            payload = sum(2 * int(np.prod(s)) for _, s in lay.entries.values())
+            assert verify_cover(pieces, lay.total_bytes, allow_gaps=True) == []
+            assert int(pieces.arrays()[3].sum()) == payload
+            base = mem.alloc(lay.total_bytes)
+            mem.execute(to_items(pieces, old_base, base, max_chunk=4096))
+            for (layer, fam), (off, shape) in lay.entries.items():
+                want = _bytes(expected_shard(geo, full, t_new, dst % t_new, layer, fam).to(torch.bfloat16))
+                got = mem.view(base + off, want.size)
+                assert np.array_equal(got, want), (t_old, t_new, dst, layer, fam)
+            remote, local = nvlink_bytes(pieces, dst)
+            remote_total += remote
+            if t_old == 1:  # every target slice is already resident: zero NVLink bytes
+                assert remote == 0
+        if t_old < t_new and t_new % t_old == 0 and t_old > 1:
+            assert remote_total > 0
+
+
+def test_kv_and_history_migration_bit_exact():
+    geom = GEOS["mini-qwen"]
+    world, L, D = 8, geom.num_layers, geom.head_dim
+    rng = np.random.default_rng(0)
+    for t_old, t_new in [(1, 2), (1, 8), (2, 8), (4, 2), (2, 4), (8, 1)]:
+        old, new = Layout(t_old, world), Layout(t_new, world)
+        n_samples = 5
+        ctx = [int(x) for x in rng.integers(1, 300, n_samples)]
+        old_group = [int(x) for x in rng.integers(0, old.dp, n_samples)]
+        num_pages_old, num_pages_new, max_pages = 64, 64, 8
+        hist_ld = 512
+        # logical truth: kv[(sample, layer, kvsel, head)] -> [ctx, D] bf16 bytes ; history[sample] -> ints
+        truth = {}
+        mem = ByteMemory()
+        pool_base, hist_base, src_desc = {}, {}, []
+        old_pages = {}
+        for r in range(world):
+            sh = rank_shard(geom, t_old, r % t_old)
+            pool_base[r] = mem.alloc(L * 2 * num_pages_old * sh.n_kv * 64 * D * 2)
+            hist_base[r] = mem.alloc(16 * hist_ld * 4)
+        perm = rng.permutation(num_pages_old)  # disjoint page sets per sample
+        for i in range(n_samples):
+            pages = tuple(int(p) for p in perm[i * max_pages:(i + 1) * max_pages])
+            old_pages[i] = pages
+            slot = 3 + i
+            src_desc.append(KVSource(old_group=old_group[i], slot=slot, pages=pages))
+            hist = rng.integers(0, 1 << 20, ctx[i]).astype(np.int32)
+            truth[("h", i)] = hist
+            for h in range(geom.n_kv):
+                for l in range(L):
+                    for kv in range(2):
+                        truth[(i, l, kv, h)] = rng.integers(0, 256, (ctx[i], D * 2)).astype(np.uint8)
+            for r in old.ranks_of_group(old_group[i]):
+                sh = rank_shard(geom, t_old, r % t_old)
+                mem.view(hist_base[r] + 4 * slot * hist_ld, 4 * ctx[i])[:] = hist.view(np.uint8)
+                for h in range(*sh.kv_heads):
+                    for l in range(L):
+                        for kv in range(2):
+                            tok = truth[(i, l, kv, h)]
+                            for p in range((ctx[i] + 63) // 64):
+                                off = kv_chunk_offset(geom, sh.n_kv, num_pages_old, l, kv, pages[p],
+                                                      h - sh.kv_heads[0])
+                                rows = tok[p * 64:(p + 1) * 64]
+                                mem.view(pool_base[r] + off, rows.size)[:] = rows.ravel()
+        # merge: samples spread over the new groups round-robin
+        placement = {g: [i for i in range(n_samples) if i % new.dp == g] for g in range(new.dp)}
+        for dst in range(world):
+            g = new.group_of(dst)
+            mine = placement[g]
+            sh = rank_shard(geom, t_new, dst % t_new)
+            tgts = [KVTarget(slot=j, pages=tuple(range(j * max_pages, (j + 1) * max_pages))) for j in range(len(mine))]
+            srcs = [src_desc[i] for i in mine]
+            kp = plan_kv_pulls(geom, old, new, dst, srcs, tgts, [ctx[i] for i in mine], num_pages_old, num_pages_new)
+            hp = plan_history_pulls(old, dst, srcs, tgts, [ctx[i] for i in mine], hist_ld, hist_ld)
+            pool_sz = L * 2 * num_pages_new * sh.n_kv * 64 * D * 2
+            assert verify_cover(kp, pool_sz, allow_gaps=True) == []
+            nb = mem.alloc(pool_sz)
+            hb = mem.alloc(16 * hist_ld * 4)
+            mem.execute(to_items(kp, pool_base, nb))
+            mem.execute(to_items(hp, hist_base, hb))
+            for j, i in enumerate(mine):
+                got_hist = mem.view(hb + 4 * j * hist_ld, 4 * ctx[i]).view(np.int32)
+                assert np.array_equal(got_hist, truth[("h", i)])
+                for h in range(*sh.kv_heads):
+                    for l in range(L):
+                        for kv in range(2):
+                            tok = truth[(i, l, kv, h)]
+                            for p in range((ctx[i] + 63) // 64):
+                                off = kv_chunk_offset(geom, sh.n_kv, num_pages_new, l, kv, tgts[j].pages[p],
+                                                      h - sh.kv_heads[0])
+                                n = min(64, ctx[i] - p * 64)
+                                got = mem.view(nb + off, n * D * 2).reshape(n, D * 2)
+                                assert np.array_equal(got, tok[p * 64:p * 64 + n]), (t_old, t_new, i, l, kv, h, p)
