@@ -330,14 +330,25 @@ class GroupRunner:
         return stats
 
     def capture(self, B: int) -> None:
+        """Capture bucket B's step program into a CUDA graph.
+
+        Captured on a private side stream without a device synchronize, so a
+        coordinator running ahead of the GPU can capture while earlier rounds
+        are still queued. No warm-up run is needed (a step mutates positions):
+        kernel attributes are configured once by tps_init.
+        """
         if B in self.graphs:
             return
         g = torch.cuda.CUDAGraph()
-        # state-preserving warm-up is not possible (a step mutates positions), so
-        # capture directly; kernels were already configured by an eager step.
-        with torch.cuda.graph(g):
-            st = torch.cuda.current_stream().cuda_stream
-            self.stats[B] = self._issue(B, st)
+        if not hasattr(self, "_cap_stream"):
+            self._cap_stream = torch.cuda.Stream(self.ex[0].device)
+        s = self._cap_stream
+        with torch.cuda.stream(s):
+            g.capture_begin()
+            try:
+                self.stats[B] = self._issue(B, s.cuda_stream)
+            finally:
+                g.capture_end()
         self.graphs[B] = g
 
     def step(self, B: int, n: int = 1) -> None:

@@ -80,6 +80,8 @@ def admit(ranks: list[RankState], sample_id: int, prompt: list[int], max_ctx: in
     """
     n_pages = pages_for(max_ctx)
     got = None
+    if not isinstance(prompt, torch.Tensor):
+        prompt = torch.tensor(prompt, dtype=torch.int32)
     for r in ranks:
         s = r.slots.alloc(sample_id) if slot is None else slot
         if got is not None and s != got:
@@ -89,12 +91,19 @@ def admit(ranks: list[RankState], sample_id: int, prompt: list[int], max_ctx: in
             raise ValueError("max_ctx exceeds the slot table's max_len")
         pages = r.kv.alloc(n_pages)
         r.slots.pages[s] = pages
-        dev = r.slots.device
-        r.slots.page_table[s, :n_pages] = torch.tensor(pages, dtype=torch.int32, device=dev)
-        r.slots.history[s, :len(prompt)] = torch.tensor(prompt, dtype=torch.int32, device=dev)
+        h2d(r.slots.page_table[s, :n_pages], pages)
+        r.slots.history[s, :prompt.numel()].copy_(prompt, non_blocking=True)
         r.slots.pos[s] = 0
-        r.executor.prompt_len[s] = len(prompt)
+        r.executor.prompt_len[s] = prompt.numel()
     return got
+
+
+def h2d(dst: torch.Tensor, values) -> None:
+    """Asynchronous small host->device write through pinned memory (never syncs the stream)."""
+    host = torch.as_tensor(values, dtype=dst.dtype)
+    if dst.device.type == "cuda":
+        host = host.pin_memory()
+    dst.copy_(host, non_blocking=True)
 
 
 def retire(ranks: list[RankState], slot: int) -> None:
