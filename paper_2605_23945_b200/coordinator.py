@@ -92,7 +92,8 @@ class B200Backend:
         # device-timed runs start with the prompts already resident in HBM
         self.prompts_dev = None if host_io else self.prompts_host.to(dev0)
         self.out_host = torch.zeros((spec.global_batch, spec.l_max), dtype=torch.int32).pin_memory()
-        self.cache = CacheManager(world, self.max_batch, geom.hidden, n_phases(geom))
+        # receive slots must hold any group's batch after merges: size them for the whole node
+        self.cache = CacheManager(world, per_node, geom.hidden, n_phases(geom))
         self.epoch = 0
         self.ranks: dict[int, RankState] = {}
         self.runners: dict[int, GroupRunner] = {}
@@ -137,7 +138,7 @@ class B200Backend:
             w.fill_random(weights_seed)
         kv = KVPool(self.geom.num_layers, sh.n_kv, self.geom.head_dim, slots * pages_for(self.max_len), dev)
         st = SlotTable(slots, self.max_len, dev)
-        ex = InferExecutor(self.geom, sh, w, kv, st, max(1, min(self.max_batch, slots)), dev, comm=comm)
+        ex = InferExecutor(self.geom, sh, w, kv, st, slots, dev, comm=comm)
         return RankState(w, kv, st, ex, comm)
 
     def capture_all(self) -> float:
