@@ -89,8 +89,9 @@ class B200Backend:
         host = torch.from_numpy(np.ascontiguousarray(prompts, dtype=np.int32))
         dev0 = world.devices[world.local_ranks[0]]
         self.prompts_host = host.pin_memory()
-        # device-timed runs start with the prompts already resident in HBM
-        self.prompts_dev = None if host_io else self.prompts_host.to(dev0)
+        # device-timed runs start with the prompts already resident in HBM; host_io
+        # runs (the e2e measurement) copy each prompt from pinned host memory
+        self.prompts_dev = self.prompts_host.to(dev0)
         self.out_host = torch.zeros((spec.global_batch, spec.l_max), dtype=torch.int32).pin_memory()
         # receive slots must hold any group's batch after merges: size them for the whole node
         self.cache = CacheManager(world, per_node, geom.hidden, n_phases(geom))
@@ -141,6 +142,22 @@ class B200Backend:
         ex = InferExecutor(self.geom, sh, w, kv, st, slots, dev, comm=comm)
         return RankState(w, kv, st, ex, comm)
 
+    def reset(self, seed: int) -> None:
+        """Return to the initial layout with no samples (between repeated stages)."""
+        init = Layout(self.spec.initial_tp, self.world.gpus)
+        if self.epoch or self.layout != init:
+            self.layout = init
+            self._build_layout(init, weights_seed=seed)
+            self.capture_all()
+        self.epoch = 0
+        self.timeline = {}
+        self.switches = []
+        self.slot_of = {}
+        self.kernels_launched = 0
+        self.h2d_bytes = self.d2h_bytes = 0
+        self.start = {}
+        self._keep.clear()
+
     def capture_all(self) -> float:
         """Capture the decode graph of every bucket of every local group (host seconds)."""
         t0 = time.perf_counter()
@@ -171,7 +188,7 @@ class B200Backend:
         grp = self.group_ranks(g)
         slots = []
         for s in members:
-            if self.prompts_dev is not None:
+            if not self.host_io:
                 prompt = self.prompts_dev[s.id]
             else:
                 prompt = self.prompts_host[s.id].to(grp[0].slots.device, non_blocking=True)
@@ -460,15 +477,24 @@ class GlobalCoordinator:
         self.geom = geom
         self.world = world or World.virtual(spec.cluster.gpus_per_node)
         self.table = table
+        self.seed = seed
         self.backend = B200Backend(spec, geom, self.world, seed=seed, use_graphs=use_graphs,
                                    copy_mode=copy_mode, host_io=host_io)
         self.setup_capture_s = self.backend.capture_all()
+        self.runs = 0
+        self.last_wall_s = 0.0
 
     def run(self) -> tuple[SimReport, dict]:
+        """One generation stage: real execution, then the measured-clock report."""
         be = self.backend
+        if self.runs:
+            be.reset(self.seed)
+        self.runs += 1
         be.begin()
+        t0 = time.perf_counter()
         run(self.spec, self.table, backend=be)
-        meas = be.measurements()
+        meas = be.measurements()  # synchronises: includes the final device->host token copies
+        self.last_wall_s = time.perf_counter() - t0
         report = run(self.spec, self.table, backend=RecordedBackend(self.world.allgather(meas)))
         return report, meas
 
