@@ -302,11 +302,17 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_kernel(
   __syncthreads();
   for (int i = tid; i < G * D; i += kAttnThreads) {
     const int h = i / D, d = i % D;
-    const size_t base = ((size_t)b * nq + head0 + h) * nsplit;
+    const float* po = part_o + ((size_t)b * nq + head0 + h) * nsplit * D + d;
+    const float* fh = fac + h * kMaxAttnSplits;
     float acc = 0.f;
-    for (int s2 = 0; s2 < active; ++s2) {
-      const float f = fac[h * kMaxAttnSplits + s2];
-      if (f != 0.f) acc += __ldcg(part_o + (base + s2) * D + d) * f;
+    // independent loads in batches of 8: the merge is latency-, not bandwidth-bound
+    for (int s0 = 0; s0 < active; s0 += 8) {
+      float v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = (s0 + j < active) ? __ldcg(po + (size_t)(s0 + j) * D) : 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (s0 + j < active) acc += v[j] * fh[s0 + j];
     }
     out[((size_t)b * nq + head0 + h) * D + d] = f2bf(acc * inv_l[h]);
   }
@@ -330,7 +336,7 @@ int attn_splits(int B, int nkv, int max_pages) {
   int want = (2 * kNumSMs + B * nkv - 1) / (B * nkv);
   const int cap = (max_pages + kMinPagesPerSplit - 1) / kMinPagesPerSplit;
   if (want > cap) want = cap;
-  if (want > kMaxAttnSplits) want = kMaxAttnSplits;
+  if (want > 32) want = 32;  // the last-CTA merge reads active x G x D partials: keep it short
   if (want < 1) want = 1;
   return want;
 }
