@@ -79,9 +79,14 @@ int tps_linear_splits(int64_t n, int64_t k, int64_t b);
 int tps_linear(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,
                int64_t x_rows, int64_t ldx, float* out, int splits, void* stream);
 
-/* resid[b] = E[history[slot][pos_by_slot[slot]]] (slot = row_slot[b]). */
-int tps_embed(const int* row_slot, const int* pos_by_slot, const int* history, int hist_ld,
-              const void* table, int H, int B, float* resid, void* stream);
+/* Row indirection used by every decode kernel: row b processes sample slot
+ * row_slot[b] (< 0: padding row) at position row_pos[b], or at pos_by_slot[slot]
+ * when row_pos is NULL (decode); row_pos lets one launch process several prompt
+ * positions of a sample (chunked prefill through the decode kernels). */
+
+/* resid[b] = E[history[slot][pos]] (replicated vocab table). */
+int tps_embed(const int* row_slot, const int* pos_by_slot, const int* row_pos, const int* history,
+              int hist_ld, const void* table, int H, int B, float* resid, void* stream);
 
 /* Strided source convention (src, nsrc, src_stride): nsrc fp32 buffers at
  * src + i*src_stride (elements), summed in index order -- the split-K partials
@@ -104,7 +109,8 @@ int tps_reduce_push(const float* src, int nsrc, int64_t src_stride, float* const
  * cos/sin tables [pos][D/2]), q -> bf16 [B][nq][D], k/v appended at each
  * row's position into the paged cache [page][nkv][64][D]. */
 int tps_qkv_rope_append(const float* src, int nsrc, int64_t src_stride, const void* bias, const int* row_slot,
-                        const int* pos_by_slot, const int* page_table, int max_pages, const float* cos_t,
+                        const int* pos_by_slot, const int* row_pos, const int* page_table, int max_pages,
+                        const float* cos_t,
                         const float* sin_t, int B, int nq, int nkv, int D, int page_size, void* q_out,
                         void* k_cache, void* v_cache, void* stream);
 
@@ -117,7 +123,8 @@ int tps_attn_splits(int B, int nkv, int max_pages);
  * scratch; merge_ctr: zero-initialised uint32 [B][nkv] (self re-arming). KV term
  * of tpshift/latency.py:123. */
 int tps_paged_attention(const void* q, const void* k_cache, const void* v_cache, const int* row_slot,
-                        const int* pos_by_slot, const int* page_table, int max_pages, int B, int nq,
+                        const int* pos_by_slot, const int* row_pos, const int* page_table, int max_pages, int B,
+                        int nq,
                         int nkv, int D, int nsplit, float* part_m, float* part_l, float* part_o,
                         unsigned int* merge_ctr, void* out, void* stream);
 

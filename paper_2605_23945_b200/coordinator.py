@@ -43,6 +43,9 @@ from .switch_executor import (KVSource, KVTarget, Layout, Pieces, check, nvlink_
 from .switchcost import RECOMPUTE, SwitchCostBreakdown
 
 
+PREFILL_ROWS = 512  # (sample, prompt position) rows per chunked-prefill step
+
+
 def _event(stream) -> torch.cuda.Event:
     e = torch.cuda.Event(enable_timing=True)
     e.record(stream)
@@ -93,8 +96,10 @@ class B200Backend:
         # runs (the e2e measurement) copy each prompt from pinned host memory
         self.prompts_dev = self.prompts_host.to(dev0)
         self.out_host = torch.zeros((spec.global_batch, spec.l_max), dtype=torch.int32).pin_memory()
-        # receive slots must hold any group's batch after merges: size them for the whole node
-        self.cache = CacheManager(world, per_node, geom.hidden, n_phases(geom))
+        # receive slots must hold any group's batch after merges (size them for the whole
+        # node) and a chunked-prefill step's rows
+        self.cache = CacheManager(world, max(per_node, PREFILL_ROWS + self.max_batch), geom.hidden,
+                                  n_phases(geom))
         self.epoch = 0
         self.ranks: dict[int, RankState] = {}
         self.runners: dict[int, GroupRunner] = {}
@@ -139,17 +144,19 @@ class B200Backend:
             w.fill_random(weights_seed)
         kv = KVPool(self.geom.num_layers, sh.n_kv, self.geom.head_dim, slots * pages_for(self.max_len), dev)
         st = SlotTable(slots, self.max_len, dev)
-        ex = InferExecutor(self.geom, sh, w, kv, st, slots, dev, comm=comm)
+        pf = slots * max(1, PREFILL_ROWS // slots) if self.epoch == 0 else 0
+        ex = InferExecutor(self.geom, sh, w, kv, st, slots, dev, comm=comm, prefill_rows=pf)
         return RankState(w, kv, st, ex, comm)
 
     def reset(self, seed: int) -> None:
         """Return to the initial layout with no samples (between repeated stages)."""
         init = Layout(self.spec.initial_tp, self.world.gpus)
-        if self.epoch or self.layout != init:
+        rebuild = bool(self.epoch) or self.layout != init
+        self.epoch = 0
+        if rebuild:
             self.layout = init
             self._build_layout(init, weights_seed=seed)
             self.capture_all()
-        self.epoch = 0
         self.timeline = {}
         self.switches = []
         self.slot_of = {}
@@ -165,6 +172,9 @@ class B200Backend:
             for runner in self.runners.values():
                 for b in runner.ex[0].buckets():
                     runner.capture(b)
+                R = runner.ex[0].prefill_rows
+                if R and ("prefill", R) not in runner.graphs:
+                    runner._capture_key(("prefill", R), lambda st, rr=runner, n=R: rr._issue_prefill(n, st))
         return time.perf_counter() - t0
 
     def group_ranks(self, g: int) -> list[RankState]:
@@ -196,14 +206,11 @@ class B200Backend:
             slots.append(admit(grp, s.id, prompt, max_ctx=self.max_len))
             self.slot_of[s.id] = slots[-1]
         runner = self.runners[g]
-        B = runner.ex[0].bucket(len(slots))
-        runner.set_rows(B, slots)
         r = self.first_local(g)
         tl = self.timeline.setdefault((self.epoch, g), GroupTimeline(rank=r))
-        steps = self.spec.prompt_len - 1  # prompt processed through the decode path
-        if steps > 0:
-            runner.step(B, steps)
-            self.kernels_launched += steps * runner.kernels_per_step(B)
+        # chunked prefill through the decode kernels: prompt positions 0..L-2 of every
+        # sample, several positions per launch; position L-1 is decode round 1
+        self.kernels_launched += runner.prefill(slots, self.spec.prompt_len)
         tl.prefill_end = _event(self.stream(r))
         return 0.0
 

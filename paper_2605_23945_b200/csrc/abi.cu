@@ -24,11 +24,11 @@ void set_pdl(bool on);
 int linear_splits(int64_t n, int64_t k, int64_t b);
 int linear(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
            int64_t ldx, float* out, int splits, cudaStream_t stream);
-int embed(const int*, const int*, const int*, int, const void*, int, int, float*, cudaStream_t);
+int embed(const int*, const int*, const int*, const int*, int, const void*, int, int, float*, cudaStream_t);
 int add_norm(float*, const Src&, const WaitSpec&, const void*, float, int, int, void*, int, cudaStream_t);
 int reduce_push(const Src&, const DstList&, long long, const SignalSpec&, cudaStream_t);
-int qkv_rope_append(const Src&, const void*, const int*, const int*, const int*, int, const float*, const float*,
-                    int, int, int, int, int, void*, void*, void*, cudaStream_t);
+int qkv_rope_append(const Src&, const void*, const int*, const int*, const int*, const int*, int, const float*,
+                    const float*, int, int, int, int, int, void*, void*, void*, cudaStream_t);
 int silu_mul(const Src&, int, int, void*, int, cudaStream_t);
 int argmax_stage1(const Src&, int, int, int, int, void*, const SignalSpec&, cudaStream_t);
 int argmax_finalize(const CandList&, int, const WaitSpec&, int, const int*, int*, const int*, int*, int, int*,
@@ -36,8 +36,8 @@ int argmax_finalize(const CandList&, int, const WaitSpec&, int, const int*, int*
 int epoch_advance(uint64_t*, cudaStream_t);
 int sum_src(const Src&, long long, float*, cudaStream_t);
 int attn_splits(int B, int nkv, int max_pages);
-int paged_attention(const void*, const void*, const void*, const int*, const int*, const int*, int, int, int, int,
-                    int, int, float*, float*, float*, unsigned int*, void*, cudaStream_t);
+int paged_attention(const void*, const void*, const void*, const int*, const int*, const int*, const int*, int, int,
+                    int, int, int, int, float*, float*, float*, unsigned int*, void*, cudaStream_t);
 int copy_items(const void*, int, int, int, cudaStream_t);
 int configure_gemm();
 int configure_attention();
@@ -112,10 +112,10 @@ int tps_linear(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, 
   return linear(w, n, k, ldw, x, b, x_rows, ldx, out, splits, S(stream));
 }
 
-int tps_embed(const int* row_slot, const int* pos_by_slot, const int* history, int hist_ld, const void* table,
-              int H, int B, float* resid, void* stream) {
+int tps_embed(const int* row_slot, const int* pos_by_slot, const int* row_pos, const int* history, int hist_ld,
+              const void* table, int H, int B, float* resid, void* stream) {
   TPS_CHECK_ARG(row_slot && pos_by_slot && history && table && resid, "embed: null pointer");
-  return embed(row_slot, pos_by_slot, history, hist_ld, table, H, B, resid, S(stream));
+  return embed(row_slot, pos_by_slot, row_pos, history, hist_ld, table, H, B, resid, S(stream));
 }
 
 int tps_add_norm(float* resid, const float* src, int nsrc, int64_t src_stride, const tps_wait* wait,
@@ -143,7 +143,8 @@ int tps_reduce_push(const float* src, int nsrc, int64_t src_stride, float* const
 }
 
 int tps_qkv_rope_append(const float* src, int nsrc, int64_t src_stride, const void* bias, const int* row_slot,
-                        const int* pos_by_slot, const int* page_table, int max_pages, const float* cos_t,
+                        const int* pos_by_slot, const int* row_pos, const int* page_table, int max_pages,
+                        const float* cos_t,
                         const float* sin_t, int B, int nq, int nkv, int D, int page_size, void* q_out,
                         void* k_cache, void* v_cache, void* stream) {
   TPS_CHECK_ARG(page_size == 64, "qkv_rope_append: page_size must be 64");
@@ -152,20 +153,23 @@ int tps_qkv_rope_append(const float* src, int nsrc, int64_t src_stride, const vo
   Src s;
   int rc = make_src(src, nsrc, src_stride, &s);
   if (rc) return rc;
-  return qkv_rope_append(s, bias, row_slot, pos_by_slot, page_table, max_pages, cos_t, sin_t, B, nq, nkv, D,
+  return qkv_rope_append(s, bias, row_slot, pos_by_slot, row_pos, page_table, max_pages, cos_t, sin_t, B, nq, nkv,
+                         D,
                          page_size, q_out, k_cache, v_cache, S(stream));
 }
 
 int tps_attn_splits(int B, int nkv, int max_pages) { return attn_splits(B, nkv, max_pages); }
 
 int tps_paged_attention(const void* q, const void* k_cache, const void* v_cache, const int* row_slot,
-                        const int* pos_by_slot, const int* page_table, int max_pages, int B, int nq, int nkv, int D,
+                        const int* pos_by_slot, const int* row_pos, const int* page_table, int max_pages, int B,
+                        int nq, int nkv, int D,
                         int nsplit, float* part_m, float* part_l, float* part_o, unsigned int* merge_ctr,
                         void* out, void* stream) {
   TPS_CHECK_ARG(q && k_cache && v_cache && row_slot && pos_by_slot && page_table && part_m && part_l && part_o &&
                     merge_ctr && out,
                 "paged_attention: null pointer");
-  return paged_attention(q, k_cache, v_cache, row_slot, pos_by_slot, page_table, max_pages, B, nq, nkv, D, nsplit,
+  return paged_attention(q, k_cache, v_cache, row_slot, pos_by_slot, row_pos, page_table, max_pages, B, nq, nkv, D,
+                         nsplit,
                          part_m, part_l, part_o, merge_ctr, out, S(stream));
 }
 

@@ -59,7 +59,8 @@ template <int D>
 __global__ void __launch_bounds__(kAttnThreads) paged_attn_kernel(
     const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k_cache,
     const __nv_bfloat16* __restrict__ v_cache, const int* __restrict__ row_slot,
-    const int* __restrict__ pos_by_slot, const int* __restrict__ page_table, int max_pages, int nq, int nkv,
+    const int* __restrict__ pos_by_slot, const int* __restrict__ row_pos, const int* __restrict__ page_table,
+    int max_pages, int nq, int nkv,
     int G, int nsplit, float scale_log2, float* __restrict__ part_m, float* __restrict__ part_l,
     float* __restrict__ part_o, unsigned int* __restrict__ merge_ctr, __nv_bfloat16* __restrict__ out) {
   constexpr int CPR = D / 8;       // 16-byte chunks per token row
@@ -77,7 +78,7 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_kernel(
   pdl_launch_dependents();
 
   const int slot = row_slot[b];
-  const int ctx = slot >= 0 ? pos_by_slot[slot] + 1 : 0;
+  const int ctx = slot >= 0 ? (row_pos ? row_pos[b] : pos_by_slot[slot]) + 1 : 0;
   const int npages = (ctx + kPage - 1) / kPage;
   int pps = (npages + nsplit - 1) / nsplit;
   if (pps < kMinPagesPerSplit) pps = kMinPagesPerSplit;
@@ -342,7 +343,8 @@ int attn_splits(int B, int nkv, int max_pages) {
 }
 
 int paged_attention(const void* q, const void* k_cache, const void* v_cache, const int* row_slot,
-                    const int* pos_by_slot, const int* page_table, int max_pages, int B, int nq, int nkv, int D,
+                    const int* pos_by_slot, const int* row_pos, const int* page_table, int max_pages, int B, int nq,
+                    int nkv, int D,
                     int nsplit, float* part_m, float* part_l, float* part_o, unsigned int* merge_ctr, void* out,
                     cudaStream_t st) {
   TPS_CHECK_ARG(B > 0 && nkv > 0 && nq % nkv == 0, "paged_attention: nq must be a multiple of nkv");
@@ -357,11 +359,11 @@ int paged_attention(const void* q, const void* k_cache, const void* v_cache, con
   auto* oo = reinterpret_cast<__nv_bfloat16*>(out);
   if (D == 128)
     return launch_k(paged_attn_kernel<128>, grid, dim3(kAttnThreads), attn_smem<128>(), st, true, qq, kk, vv,
-                    row_slot, pos_by_slot, page_table, max_pages, nq, nkv, G, nsplit, scale_log2, part_m, part_l,
+                    row_slot, pos_by_slot, row_pos, page_table, max_pages, nq, nkv, G, nsplit, scale_log2, part_m, part_l,
                     part_o, merge_ctr, oo);
   if (D == 64)
     return launch_k(paged_attn_kernel<64>, grid, dim3(kAttnThreads), attn_smem<64>(), st, true, qq, kk, vv,
-                    row_slot, pos_by_slot, page_table, max_pages, nq, nkv, G, nsplit, scale_log2, part_m, part_l,
+                    row_slot, pos_by_slot, row_pos, page_table, max_pages, nq, nkv, G, nsplit, scale_log2, part_m, part_l,
                     part_o, merge_ctr, oo);
   return fail(kInvalid, "paged_attention: head_dim must be 64 or 128");
 }

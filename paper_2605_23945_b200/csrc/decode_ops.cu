@@ -98,14 +98,14 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 // ------------------------------------------------------------ embedding ---
 // resid[b][:] = E[history[slot][pos]][:]  (replicated vocab table, bf16 -> fp32)
 __global__ void embed_kernel(const int* __restrict__ row_slot, const int* __restrict__ pos_by_slot,
-                             const int* __restrict__ history, int hist_ld,
+                             const int* __restrict__ row_pos, const int* __restrict__ history, int hist_ld,
                              const __nv_bfloat16* __restrict__ table, int H, float* __restrict__ resid) {
   pdl_wait();
   pdl_launch_dependents();
   const int b = blockIdx.x;
   const int slot = row_slot[b];
   int tok = 0;
-  if (slot >= 0) tok = history[(size_t)slot * hist_ld + pos_by_slot[slot]];
+  if (slot >= 0) tok = history[(size_t)slot * hist_ld + (row_pos ? row_pos[b] : pos_by_slot[slot])];
   const __nv_bfloat162* src = reinterpret_cast<const __nv_bfloat162*>(table + (size_t)tok * H);
   float2* dst = reinterpret_cast<float2*>(resid + (size_t)b * H);
   for (int i = threadIdx.x; i < H / 2; i += blockDim.x) dst[i] = __bfloat1622float2(src[i]);
@@ -180,7 +180,8 @@ __global__ void __launch_bounds__(256) reduce_push_kernel(Src src, DstList dst, 
 // KV cache per layer: [num_pages][nkv][P][D] bf16. One warp per (row, head).
 __global__ void __launch_bounds__(128) qkv_rope_append_kernel(
     Src src, const __nv_bfloat16* __restrict__ bias, const int* __restrict__ row_slot,
-    const int* __restrict__ pos_by_slot, const int* __restrict__ page_table, int max_pages,
+    const int* __restrict__ pos_by_slot, const int* __restrict__ row_pos, const int* __restrict__ page_table,
+    int max_pages,
     const float* __restrict__ cos_t, const float* __restrict__ sin_t, int B, int nq, int nkv, int D, int P,
     __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ k_cache, __nv_bfloat16* __restrict__ v_cache) {
   pdl_wait();
@@ -193,7 +194,7 @@ __global__ void __launch_bounds__(128) qkv_rope_append_kernel(
   const int half = D / 2;
   const int slot = row_slot[b];
   const long long N = (long long)(nq + 2 * nkv) * D;
-  const int pos = slot >= 0 ? pos_by_slot[slot] : 0;
+  const int pos = slot >= 0 ? (row_pos ? row_pos[b] : pos_by_slot[slot]) : 0;
   const long long rowoff = (long long)b * N;
   for (int i = lane; i < half; i += 32) {
     const float cs = cos_t[(size_t)pos * half + i];
@@ -351,10 +352,10 @@ static int grid_for(long long work, int per_block, int cap) {
   return (int)g;
 }
 
-int embed(const int* row_slot, const int* pos_by_slot, const int* history, int hist_ld, const void* table,
-          int H, int B, float* resid, cudaStream_t st) {
+int embed(const int* row_slot, const int* pos_by_slot, const int* row_pos, const int* history, int hist_ld,
+          const void* table, int H, int B, float* resid, cudaStream_t st) {
   TPS_CHECK_ARG(H % 2 == 0 && B > 0, "embed: H must be even, B > 0");
-  return launch_k(embed_kernel, dim3(B), dim3(256), 0, st, true, row_slot, pos_by_slot, history, hist_ld,
+  return launch_k(embed_kernel, dim3(B), dim3(256), 0, st, true, row_slot, pos_by_slot, row_pos, history, hist_ld,
                   reinterpret_cast<const __nv_bfloat16*>(table), H, resid);
 }
 
@@ -374,12 +375,14 @@ int reduce_push(const Src& src, const DstList& dst, long long n, const SignalSpe
 }
 
 int qkv_rope_append(const Src& src, const void* bias, const int* row_slot, const int* pos_by_slot,
-                    const int* page_table, int max_pages, const float* cos_t, const float* sin_t, int B, int nq,
+                    const int* row_pos, const int* page_table, int max_pages, const float* cos_t,
+                    const float* sin_t, int B, int nq,
                     int nkv, int D, int P, void* q_out, void* k_cache, void* v_cache, cudaStream_t st) {
   TPS_CHECK_ARG(D % 2 == 0 && D <= 256 && B > 0 && nq > 0 && nkv > 0, "qkv_rope_append: bad shape");
   const int tasks = B * (nq + nkv);
   return launch_k(qkv_rope_append_kernel, dim3((tasks + 3) / 4), dim3(128), 0, st, true, src,
-                  reinterpret_cast<const __nv_bfloat16*>(bias), row_slot, pos_by_slot, page_table, max_pages,
+                  reinterpret_cast<const __nv_bfloat16*>(bias), row_slot, pos_by_slot, row_pos, page_table,
+                  max_pages,
                   cos_t, sin_t, B, nq, nkv, D, P, reinterpret_cast<__nv_bfloat16*>(q_out),
                   reinterpret_cast<__nv_bfloat16*>(k_cache), reinterpret_cast<__nv_bfloat16*>(v_cache));
 }

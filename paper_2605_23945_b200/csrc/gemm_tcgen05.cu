@@ -86,7 +86,7 @@ template <int BN>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_swapab_kernel(const __grid_constant__ CUtensorMap tmap_w,
                        const __grid_constant__ CUtensorMap tmap_x, float* __restrict__ out, int N,
-                       int B, int num_tiles, int splits, int chunks) {
+                       int B, int num_tiles, int splits, int chunks, int acts) {
   using Cfg = GemmCfg<BN>;
   constexpr int S = Cfg::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -102,7 +102,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int units = num_tiles * splits;
+  // unit u = ((tile * splits + split) * acts + act): the activation tiles of one weight
+  // chunk range run on neighbouring CTAs at the same time, so L2 dedups the weight stream
+  const int units = num_tiles * splits * acts;
+  auto unit_of = [&](int u, int& tile, int& act, int& c0, int& c1) {
+    act = u % acts;
+    const int ts = u / acts;
+    tile = ts / splits;
+    const int split = ts % splits;
+    c0 = (int)((long long)split * chunks / splits);
+    c1 = (int)((long long)(split + 1) * chunks / splits);
+    return split;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -145,10 +156,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // predecessor is still running; only the activation loads wait.
       int pre = 0;
       if ((int)blockIdx.x < units) {
-        const int u = blockIdx.x;
-        const int tile = u / splits, split = u % splits;
-        const int c0 = (int)((long long)split * chunks / splits);
-        const int c1 = (int)((long long)(split + 1) * chunks / splits);
+        int tile, act, c0, c1;
+        unit_of(blockIdx.x, tile, act, c0, c1);
         pre = min(S, c1 - c0);
         for (int i = 0; i < pre; ++i) {
           mbar_arrive_expect_tx(&full[i], Cfg::kStageBytes);
@@ -156,21 +165,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
         pdl_wait();
         for (int i = 0; i < pre; ++i)
-          tma_load_2d(smem_b + i * Cfg::kBBytes, &tmap_x, &full[i], (c0 + i) * kBK, 0, pol_x);
+          tma_load_2d(smem_b + i * Cfg::kBBytes, &tmap_x, &full[i], (c0 + i) * kBK, act * BN, pol_x);
         stage = pre % S;
         phase = (pre == S) ? 1u : 0u;
       } else {
         pdl_wait();
       }
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const int tile = u / splits, split = u % splits;
-        const int c0 = (int)((long long)split * chunks / splits);
-        const int c1 = (int)((long long)(split + 1) * chunks / splits);
+        int tile, act, c0, c1;
+        unit_of(u, tile, act, c0, c1);
         for (int c = (u == (int)blockIdx.x ? c0 + pre : c0); c < c1; ++c) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
           tma_load_2d(smem_a + stage * Cfg::kABytes, &tmap_w, &full[stage], c * kBK, tile * kBM, pol_w);
-          tma_load_2d(smem_b + stage * Cfg::kBBytes, &tmap_x, &full[stage], c * kBK, 0, pol_x);
+          tma_load_2d(smem_b + stage * Cfg::kBBytes, &tmap_x, &full[stage], c * kBK, act * BN, pol_x);
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
@@ -188,9 +196,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const int split = u % splits;
-        const int c0 = (int)((long long)split * chunks / splits);
-        const int c1 = (int)((long long)(split + 1) * chunks / splits);
+        int tile, act, c0, c1;
+        unit_of(u, tile, act, c0, c1);
         mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
@@ -222,18 +229,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const int tile = u / splits, split = u % splits;
+      int tile, act, c0, c1;
+      const int split = unit_of(u, tile, act, c0, c1);
       mbar_wait(&tmem_full[acc], acc_phase);
       tc_fence_after();
       const int n = tile * kBM + q * 32 + lane;
-      float* dst = out + (size_t)split * (size_t)B * (size_t)N + (size_t)n;
-      for (int j0 = 0; j0 < BN && j0 < B; j0 += 16) {
+      const int b0 = act * BN;
+      const int rows = min(BN, B - b0);
+      float* dst = out + ((size_t)split * (size_t)B + (size_t)b0) * (size_t)N + (size_t)n;
+      for (int j0 = 0; j0 < rows; j0 += 16) {
         uint32_t r[16];
         tmem_ld16(tmem_base + (uint32_t)(acc * BN + j0) + ((uint32_t)(q * 32) << 16), r);
         if (n < N) {
 #pragma unroll
           for (int j = 0; j < 16; ++j)
-            if (j0 + j < B) dst[(size_t)(j0 + j) * N] = __uint_as_float(r[j]);
+            if (j0 + j < rows) dst[(size_t)(j0 + j) * N] = __uint_as_float(r[j]);
         }
       }
       tc_fence_before();
@@ -313,7 +323,8 @@ static int pick_bn(int64_t b) {
 // Split-K choice: minimise (waves x chunks-per-unit) for a 148-SM persistent grid,
 // plus a small charge for the fp32 partial traffic the consumer has to reduce.
 int linear_splits(int64_t n, int64_t k, int64_t b) {
-  const int64_t tiles = (n + kBM - 1) / kBM;
+  const int bn = pick_bn(b);
+  const int64_t tiles = ((n + kBM - 1) / kBM) * ((b + bn - 1) / bn);
   const int64_t chunks = (k + kBK - 1) / kBK;
   int best = 1;
   double best_cost = 1e30;
@@ -337,10 +348,11 @@ template <int BN>
 static int launch_gemm(const CUtensorMap& mw, const CUtensorMap& mx, float* out, int n, int b,
                        int tiles, int splits, int chunks, cudaStream_t stream) {
   using Cfg = GemmCfg<BN>;
-  const int units = tiles * splits;
+  const int acts = (b + BN - 1) / BN;
+  const int units = tiles * splits * acts;
   const int grid = units < kNumSMs ? units : kNumSMs;
   return launch_k(gemm_swapab_kernel<BN>, dim3(grid), dim3(kGemmThreads), Cfg::kSmemBytes, stream, true, mw, mx,
-                  out, n, b, tiles, splits, chunks);
+                  out, n, b, tiles, splits, chunks, acts);
 }
 
 template <int BN>
@@ -363,7 +375,7 @@ int configure_gemm() {
 int linear(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,
            int64_t x_rows, int64_t ldx, float* out, int splits, cudaStream_t stream) {
   TPS_CHECK_ARG(w && x && out, "linear: null pointer");
-  TPS_CHECK_ARG(n > 0 && k > 0 && b > 0 && b <= 256, "linear: need n,k > 0 and 1 <= b <= 256");
+  TPS_CHECK_ARG(n > 0 && k > 0 && b > 0 && b <= (1 << 20), "linear: need n,k > 0 and 1 <= b <= 2^20");
   TPS_CHECK_ARG(x_rows >= b && ldw >= k && ldx >= k, "linear: bad leading dimensions");
   const int64_t chunks = (k + kBK - 1) / kBK;
   TPS_CHECK_ARG(splits >= 1 && splits <= chunks, "linear: splits must be in [1, ceil(k/64)]");

@@ -105,13 +105,17 @@ class InferExecutor:
 
     def __init__(self, geom: DecoderGeometry, shard: RankShard, weights: RankWeights, kv: KVPool,
                  slots: SlotTable, max_batch: int, device: torch.device | str,
-                 comm: GroupComm | None = None, stream: torch.cuda.Stream | None = None):
+                 comm: GroupComm | None = None, stream: torch.cuda.Stream | None = None,
+                 prefill_rows: int = 0):
         self.geom = geom
         self.shard = shard
         self.w = weights
         self.kv = kv
         self.slots = slots
         self.max_batch = max_batch
+        # chunked prefill runs `prefill_rows` (sample, prompt position) rows per step
+        self.prefill_rows = prefill_rows
+        rows = max(max_batch, prefill_rows)
         self.device = torch.device(device)
         self.comm = comm
         self.tp = shard.tp
@@ -127,26 +131,29 @@ class InferExecutor:
         cos, sin = rope_tables(geom, slots.max_len + 1)
         self.cos = torch.from_numpy(cos).to(dev)
         self.sin = torch.from_numpy(sin).to(dev)
-        self.resid = torch.zeros((max_batch, H), dtype=torch.float32, device=dev)
-        self.xn = torch.zeros((max_batch, H), dtype=torch.bfloat16, device=dev)
-        self.q = torch.zeros((max_batch, self.nq, D), dtype=torch.bfloat16, device=dev)
-        self.attn = torch.zeros((max_batch, self.nq * D), dtype=torch.bfloat16, device=dev)
-        self.act = torch.zeros((max_batch, self.F), dtype=torch.bfloat16, device=dev)
+        self.resid = torch.zeros((rows, H), dtype=torch.float32, device=dev)
+        self.xn = torch.zeros((rows, H), dtype=torch.bfloat16, device=dev)
+        self.q = torch.zeros((rows, self.nq, D), dtype=torch.bfloat16, device=dev)
+        self.attn = torch.zeros((rows, self.nq * D), dtype=torch.bfloat16, device=dev)
+        self.act = torch.zeros((rows, self.F), dtype=torch.bfloat16, device=dev)
         self.prompt_len = torch.zeros(slots.num_slots, dtype=torch.int32, device=dev)
-        # split-K workspace sized for the worst projection over all buckets
+        sizes = self.buckets() + ([prefill_rows] if prefill_rows else [])
+        # split-K workspace sized for the worst projection over all row counts
         ws = 0
-        for B in self.buckets():
+        for B in sizes:
             for n, k in self._proj_shapes():
                 ws = max(ws, nat.lib().tps_linear_splits(n, k, B) * B * n)
         self.ws = torch.zeros(ws, dtype=torch.float32, device=dev)
-        nsplit = max(nat.lib().tps_attn_splits(B, self.nkv, slots.max_pages) for B in self.buckets())
-        self.att_m = torch.zeros(max_batch * self.nq * nsplit, dtype=torch.float32, device=dev)
+        att = max(nat.lib().tps_attn_splits(B, self.nkv, slots.max_pages) * B for B in sizes)
+        self.att_m = torch.zeros(att * self.nq, dtype=torch.float32, device=dev)
         self.att_l = torch.zeros_like(self.att_m)
-        self.att_o = torch.zeros(max_batch * self.nq * nsplit * D, dtype=torch.float32, device=dev)
-        self.att_ctr = torch.zeros(max_batch * self.nkv, dtype=torch.int32, device=dev)
+        self.att_o = torch.zeros(att * self.nq * D, dtype=torch.float32, device=dev)
+        self.att_ctr = torch.zeros(rows * self.nkv, dtype=torch.int32, device=dev)
         self.local_cand = torch.zeros((max_batch, 64, 2), dtype=torch.int32, device=dev)
         self.out_tok = torch.zeros(max_batch, dtype=torch.int32, device=dev)
-        self.row_slot = {B: torch.full((B,), -1, dtype=torch.int32, device=dev) for B in self.buckets()}
+        self.row_slot = {B: torch.full((B,), -1, dtype=torch.int32, device=dev) for B in sizes}
+        self.row_pos = {prefill_rows: torch.zeros(prefill_rows, dtype=torch.int32, device=dev)} \
+            if prefill_rows else {}
         self.graphs: dict[int, torch.cuda.CUDAGraph] = {}
         self.launch_stats: dict[int, LaunchStats] = {}
 
@@ -187,8 +194,14 @@ class InferExecutor:
         return nat.ptr_array(ptrs)
 
     # ------------------------------------------------------------ program ---
-    def program(self, B: int, st: int, stats: LaunchStats | None = None):
-        """Issue one decode step for bucket B on stream `st`; yields at peer waits."""
+    def program(self, B: int, st: int, stats: LaunchStats | None = None, prefill: bool = False):
+        """Issue one decode step for bucket B on stream `st`; yields at peer waits.
+
+        prefill=True: B = prefill_rows (sample, prompt position) rows bound by
+        set_prefill_rows; the layers run exactly as in decode (K/V of every row
+        appended before attention, each row attending causally to positions <=
+        its own), and the LM head / argmax are skipped.
+        """
         stats = stats if stats is not None else LaunchStats()
         lib = nat.lib()
         g = self.geom
@@ -196,11 +209,12 @@ class InferExecutor:
         W = self.w
         sl = self.slots
         rs = self.row_slot[B].data_ptr()
+        rp = self.row_pos[B].data_ptr() if prefill else None
         pos = sl.pos.data_ptr()
         hist = sl.history.data_ptr()
         eps = ctypes.c_float(g.rms_eps)
 
-        nat.check(lib.tps_embed(rs, pos, hist, sl.max_len, W.tensor_ptr(-1, "embed"), H, B,
+        nat.check(lib.tps_embed(rs, pos, rp, hist, sl.max_len, W.tensor_ptr(-1, "embed"), H, B,
                                 self.resid.data_ptr(), st), "tps_embed")
         stats.add("embed")
         nat.check(lib.tps_add_norm(self.resid.data_ptr(), None, 0, 0, None, W.tensor_ptr(0, "ln1"), eps,
@@ -211,13 +225,13 @@ class InferExecutor:
             srcs = self._linear(st, stats, W[(l, "w_qkv")], self.xn, B)
             kc, vc = self.kv.layer_ptrs(l)
             bias = W.tensor_ptr(l, "b_qkv") if g.qkv_bias else None
-            nat.check(lib.tps_qkv_rope_append(*srcs, bias, rs, pos,
+            nat.check(lib.tps_qkv_rope_append(*srcs, bias, rs, pos, rp,
                                               sl.page_table.data_ptr(), sl.max_pages,
                                               self.cos.data_ptr(), self.sin.data_ptr(), B, self.nq,
                                               self.nkv, D, PAGE, self.q.data_ptr(), kc, vc, st),
                       "tps_qkv_rope_append")
             stats.add("qkv_rope_append")
-            nat.check(lib.tps_paged_attention(self.q.data_ptr(), kc, vc, rs, pos, sl.page_table.data_ptr(),
+            nat.check(lib.tps_paged_attention(self.q.data_ptr(), kc, vc, rs, pos, rp, sl.page_table.data_ptr(),
                                               sl.max_pages, B, self.nq, self.nkv, D, nsplit,
                                               self.att_m.data_ptr(), self.att_l.data_ptr(),
                                               self.att_o.data_ptr(), self.att_ctr.data_ptr(),
@@ -233,10 +247,23 @@ class InferExecutor:
             srcs = self._linear(st, stats, W[(l, "w_d")], self.act, B)
             nxt = W.tensor_ptr(l + 1, "ln1") if l + 1 < L else W.tensor_ptr(-1, "ln_f")
             yield from self._allreduce_norm(st, stats, 2 * l + 1, srcs, B, nxt)
+        cm = self.comm
+        if prefill:
+            if cm is not None:
+                # keep every phase counter in step with the epoch: an empty push that
+                # only signals the argmax phase, then advance the epoch
+                ph = 2 * L
+                sigs = [p + ph * 8 for p in cm.peer_ctr]
+                nat.check(lib.tps_reduce_push(self.ws.data_ptr(), 1, 0, self._arr([self.ws.data_ptr()]), 1, 0,
+                                              self._arr(sigs), len(sigs), cm.done.data_ptr() + ph * 4, st),
+                          "tps_reduce_push")
+                nat.check(lib.tps_epoch_advance(cm.epoch.data_ptr(), st), "tps_epoch_advance")
+                stats.add("reduce_push")
+                stats.add("epoch_advance")
+            return
         srcs = self._linear(st, stats, W[(-1, "lm_head")], self.xn, B)
         self._last_lm_srcs = (srcs, B)
         nch = argmax_chunks(B)
-        cm = self.comm
         if cm is None:
             nat.check(lib.tps_argmax_stage1(*srcs, B, self.V, self.shard.vocab[0], nch,
                                             self.local_cand.data_ptr(), None, 0, None, st), "tps_argmax_stage1")
@@ -362,5 +389,62 @@ class GroupRunner:
         for _ in range(n):
             self.stats[B] = self._issue(B, st)
 
-    def kernels_per_step(self, B: int) -> int:
+    def kernels_per_step(self, B) -> int:
         return self.stats[B].kernels if B in self.stats else 0
+
+    # ------------------------------------------------------ chunked prefill ---
+    def prefill(self, slots: list[int], prompt_len: int) -> int:
+        """Process prompt positions 0 .. prompt_len-2 of `slots` through the decode kernels,
+        `prefill_rows // len(slots)` positions per step (each step's K/V appended before its
+        attention, so rows attend causally). Position prompt_len-1 is left for decode
+        round 1, matching the reference's round accounting. Returns kernels launched."""
+        R = self.ex[0].prefill_rows
+        todo = prompt_len - 1
+        if todo <= 0 or not slots:
+            return 0
+        if R < len(slots):
+            raise ValueError(f"prefill_rows={R} < {len(slots)} samples")
+        chunk = R // len(slots)
+        key = ("prefill", R)
+        kernels = 0
+        sl = torch.tensor(slots, dtype=torch.int32)
+        for p0 in range(0, todo, chunk):
+            n = min(chunk, todo - p0)
+            rs = torch.full((R,), -1, dtype=torch.int32)
+            rp = torch.zeros(R, dtype=torch.int32)
+            k = n * len(slots)          # position-major rows: (p0 + j, slot)
+            rs[:k] = sl.repeat(n)
+            rp[:k] = torch.arange(p0, p0 + n, dtype=torch.int32).repeat_interleave(len(slots))
+            for e in self.ex:
+                e.row_slot[R].copy_(rs.pin_memory(), non_blocking=True)
+                e.row_pos[R].copy_(rp.pin_memory(), non_blocking=True)
+            if self.use_graphs:
+                if key not in self.graphs:
+                    self._capture_key(key, lambda st: self._issue_prefill(R, st))
+                self.graphs[key].replay()
+            else:
+                self.stats[key] = self._issue_prefill(R, torch.cuda.current_stream().cuda_stream)
+            kernels += self.kernels_per_step(key)
+        idx = sl.long().pin_memory()
+        val = torch.full((len(slots),), prompt_len - 1, dtype=torch.int32).pin_memory()
+        for e in self.ex:  # decode round 1 processes the last prompt token
+            e.slots.pos.index_copy_(0, idx.to(e.device, non_blocking=True), val.to(e.device, non_blocking=True))
+        return kernels
+
+    def _issue_prefill(self, R: int, st: int) -> LaunchStats:
+        stats = LaunchStats()
+        run_programs([e.program(R, st, stats, prefill=True) for e in self.ex])
+        return stats
+
+    def _capture_key(self, key, issue) -> None:
+        g = torch.cuda.CUDAGraph()
+        if not hasattr(self, "_cap_stream"):
+            self._cap_stream = torch.cuda.Stream(self.ex[0].device)
+        s = self._cap_stream
+        with torch.cuda.stream(s):
+            g.capture_begin()
+            try:
+                self.stats[key] = issue(s.cuda_stream)
+            finally:
+                g.capture_end()
+        self.graphs[key] = g

@@ -26,11 +26,12 @@ def _stream():
 
 @pytest.mark.parametrize("n,k,b", [
     (128, 64, 1), (384, 256, 5), (4736, 3584, 16), (1000, 104, 17), (256, 4096, 64),
-    (3584, 18944, 33), (768, 512, 100), (512, 1024, 256), (8192, 256, 2)])
+    (3584, 18944, 33), (768, 512, 100), (512, 1024, 256), (8192, 256, 2),
+    (3584, 512, 300), (640, 1024, 1000), (4736, 3584, 512)])  # > 256 rows: activation tiles
 def test_linear_matches_fp32(n, k, b):
     torch.manual_seed(n + k + b)
     w = (torch.randn(n, k, device="cuda") * 0.05).bfloat16()
-    x = torch.randn(b + 3, k, device="cuda").bfloat16()
+    x = torch.randn(b + 3, k, device="cuda").bfloat16()  # extra rows are never read
     ref = x[:b].float() @ w.float().T
     lib = nat.lib()
     for splits in sorted({1, lib.tps_linear_splits(n, k, b), min(3, (k + 63) // 64)}):
@@ -51,8 +52,11 @@ def test_linear_rejects_bad_args():
         nat.check(lib.tps_linear(0, 128, 64, 64, 0, 1, 1, 64, 0, 1, _stream()))
     w = torch.zeros(128, 64, device="cuda", dtype=torch.bfloat16)
     out = torch.zeros(1, 300, 128, device="cuda")
-    with pytest.raises(ConfigError):  # b > 256
-        nat.check(lib.tps_linear(w.data_ptr(), 128, 64, 64, w.data_ptr(), 300, 300, 64, out.data_ptr(), 1,
+    with pytest.raises(ConfigError):  # fewer activation rows than the batch
+        nat.check(lib.tps_linear(w.data_ptr(), 128, 64, 64, w.data_ptr(), 300, 200, 64, out.data_ptr(), 1,
+                                 _stream()))
+    with pytest.raises(ConfigError):  # more splits than 64-wide K chunks
+        nat.check(lib.tps_linear(w.data_ptr(), 128, 64, 64, w.data_ptr(), 1, 1, 64, out.data_ptr(), 2,
                                  _stream()))
 
 
@@ -96,7 +100,7 @@ def test_paged_attention_matches_fp32(D, nq, nkv, ctxs):
         po = torch.empty(B * nq * nsplit * D, device="cuda")
         out = torch.empty(B, nq, D, device="cuda", dtype=torch.bfloat16)
         nat.check(lib.tps_paged_attention(q.data_ptr(), kc.data_ptr(), vc.data_ptr(), row_slot.data_ptr(),
-                                          pos.data_ptr(), page_table.data_ptr(), max_pages, B, nq, nkv, D,
+                                          pos.data_ptr(), None, page_table.data_ptr(), max_pages, B, nq, nkv, D,
                                           nsplit, pm.data_ptr(), pl.data_ptr(), po.data_ptr(), ctr.data_ptr(), out.data_ptr(),
                                           _stream()))
         torch.cuda.synchronize()
@@ -120,7 +124,7 @@ def test_padding_rows_are_inert():
     out = torch.full((2, nq, D), 7.0, device="cuda", dtype=torch.bfloat16)
     ctr = torch.zeros(2 * nkv, dtype=torch.int32, device="cuda")
     nat.check(nat.lib().tps_paged_attention(q.data_ptr(), kc.data_ptr(), vc.data_ptr(), row_slot.data_ptr(),
-                                            pos.data_ptr(), page_table.data_ptr(), 2, 2, nq, nkv, D, 3,
+                                            pos.data_ptr(), None, page_table.data_ptr(), 2, 2, nq, nkv, D, 3,
                                             pm.data_ptr(), pl.data_ptr(), po.data_ptr(), ctr.data_ptr(), out.data_ptr(),
                                             _stream()))
     torch.cuda.synchronize()
