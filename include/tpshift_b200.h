@@ -79,6 +79,12 @@ int tps_linear_splits(int64_t n, int64_t k, int64_t b);
 int tps_linear(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,
                int64_t x_rows, int64_t ldx, float* out, int splits, void* stream);
 
+/* Gate/up projection with the SwiGLU fused into the epilogue (no split-K):
+ * W rows are 64-row blocks [gate c | up c] (n = 2F, F % 64 == 0);
+ * act[i][f] = bf16(silu(gate_f . x_i) * (up_f . x_i)), act: bf16 [b][ld_act]. */
+int tps_linear_silu(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,
+                    int64_t x_rows, int64_t ldx, void* act, int64_t ld_act, void* stream);
+
 /* Row indirection used by every decode kernel: row b processes sample slot
  * row_slot[b] (< 0: padding row) at position row_pos[b], or at pos_by_slot[slot]
  * when row_pos is NULL (decode); row_pos lets one launch process several prompt

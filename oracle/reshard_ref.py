@@ -35,8 +35,13 @@ def expected_shard(geo: dict, full: dict, tp: int, rank: int, layer: int, family
     if family == "w_o":
         return t[:, q0 * D:q1 * D]
     if family == "w_gu":
+        # storage order of the engine: 64-row blocks [gate c | up c] (fused SwiGLU epilogue)
         f0, f1 = p["ffn"]
-        return torch.cat([t[f0:f1], t[F + f0:F + f1]], dim=0)
+        blocks = []
+        for a in range(f0, f1, 64):
+            b = min(a + 64, f1)
+            blocks += [t[a:b], t[F + a:F + b]]
+        return torch.cat(blocks, dim=0)
     if family == "w_d":
         f0, f1 = p["ffn"]
         return t[:, f0:f1]

@@ -22,6 +22,8 @@ int fail(int code, const std::string& msg) {
 // launchers (defined in the kernel translation units)
 void set_pdl(bool on);
 int linear_splits(int64_t n, int64_t k, int64_t b);
+int linear_silu(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
+                int64_t ldx, void* act, int64_t ld_act, cudaStream_t stream);
 int linear(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
            int64_t ldx, float* out, int splits, cudaStream_t stream);
 int embed(const int*, const int*, const int*, const int*, int, const void*, int, int, float*, cudaStream_t);
@@ -110,6 +112,11 @@ int tps_linear_splits(int64_t n, int64_t k, int64_t b) { return linear_splits(n,
 int tps_linear(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
                int64_t ldx, float* out, int splits, void* stream) {
   return linear(w, n, k, ldw, x, b, x_rows, ldx, out, splits, S(stream));
+}
+
+int tps_linear_silu(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
+                    int64_t ldx, void* act, int64_t ld_act, void* stream) {
+  return linear_silu(w, n, k, ldw, x, b, x_rows, ldx, act, ld_act, S(stream));
 }
 
 int tps_embed(const int* row_slot, const int* pos_by_slot, const int* row_pos, const int* history, int hist_ld,

@@ -237,8 +237,10 @@ __global__ void silu_mul_kernel(Src src, int B, int F, __nv_bfloat16* __restrict
        t += (long long)gridDim.x * blockDim.x) {
     const int b = (int)(t / F4), f4 = (int)(t % F4);
     const long long row4 = (long long)b * 2 * F4;
-    const float4 g = src_sum4(src, row4 + f4);
-    const float4 u = src_sum4(src, row4 + F4 + f4);
+    // interleaved 64-row blocks [gate c | up c]: 16 float4 per half-block
+    const long long g4 = (f4 / 16) * 32 + (f4 % 16);
+    const float4 g = src_sum4(src, row4 + g4);
+    const float4 u = src_sum4(src, row4 + g4 + 16);
     __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(out + (size_t)b * ldo) + 2 * f4;
     o[0] = __floats2bfloat162_rn(g.x / (1.f + __expf(-g.x)) * u.x, g.y / (1.f + __expf(-g.y)) * u.y);
     o[1] = __floats2bfloat162_rn(g.z / (1.f + __expf(-g.z)) * u.z, g.w / (1.f + __expf(-g.w)) * u.w);

@@ -41,7 +41,8 @@ struct GemmCfg {
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
   static constexpr int kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
   static constexpr int kBarBytes = 256;
-  static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kBarBytes;
+  static constexpr int kEpiBytes = 64 * 17 * 4;  // SwiGLU epilogue exchange buffer
+  static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kBarBytes + kEpiBytes;
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128 must be 16..256, %16");
   static_assert(kStages >= 3, "need at least 3 stages");
 };
@@ -82,17 +83,25 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-template <int BN>
+// Epilogue modes: kEpiPartial writes fp32 split-K partials [split][B][N]; kEpiSiluMul
+// (splits == 1, gate/up weights stored as interleaved 64-row blocks [gate c | up c])
+// writes act[b][f] = bf16(silu(gate) * up) directly -- the SwiGLU never round-trips HBM.
+constexpr int kEpiPartial = 0;
+constexpr int kEpiSiluMul = 1;
+
+template <int BN, int EPI>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_swapab_kernel(const __grid_constant__ CUtensorMap tmap_w,
                        const __grid_constant__ CUtensorMap tmap_x, float* __restrict__ out, int N,
-                       int B, int num_tiles, int splits, int chunks, int acts) {
+                       int B, int num_tiles, int splits, int chunks, int acts,
+                       __nv_bfloat16* __restrict__ act_out, int ld_act) {
   using Cfg = GemmCfg<BN>;
   constexpr int S = Cfg::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + S * Cfg::kABytes;
+  float* up_buf = reinterpret_cast<float*>(smem + S * Cfg::kStageBytes + Cfg::kBarBytes);  // [64][17]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + S;
@@ -236,14 +245,41 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int n = tile * kBM + q * 32 + lane;
       const int b0 = act * BN;
       const int rows = min(BN, B - b0);
-      float* dst = out + ((size_t)split * (size_t)B + (size_t)b0) * (size_t)N + (size_t)n;
-      for (int j0 = 0; j0 < rows; j0 += 16) {
-        uint32_t r[16];
-        tmem_ld16(tmem_base + (uint32_t)(acc * BN + j0) + ((uint32_t)(q * 32) << 16), r);
-        if (n < N) {
+      if constexpr (EPI == kEpiPartial) {
+        float* dst = out + ((size_t)split * (size_t)B + (size_t)b0) * (size_t)N + (size_t)n;
+        for (int j0 = 0; j0 < rows; j0 += 16) {
+          uint32_t r[16];
+          tmem_ld16(tmem_base + (uint32_t)(acc * BN + j0) + ((uint32_t)(q * 32) << 16), r);
+          if (n < N) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (j0 + j < rows) dst[(size_t)(j0 + j) * N] = __uint_as_float(r[j]);
+            for (int j = 0; j < 16; ++j)
+              if (j0 + j < rows) dst[(size_t)(j0 + j) * N] = __uint_as_float(r[j]);
+          }
+        }
+      } else {
+        // rows 0..63 of the tile are gate(f), rows 64..127 up(f), f = tile*64 + row
+        const int m = (q & 1) * 32 + lane;
+        const int f = tile * 64 + m;
+        const int F = N / 2;
+        for (int j0 = 0; j0 < rows; j0 += 16) {
+          uint32_t r[16];
+          tmem_ld16(tmem_base + (uint32_t)(acc * BN + j0) + ((uint32_t)(q * 32) << 16), r);
+          if (q >= 2) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) up_buf[m * 17 + j] = __uint_as_float(r[j]);
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (q < 2 && f < F) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              if (j0 + j < rows) {
+                const float g = __uint_as_float(r[j]);
+                const float u = up_buf[m * 17 + j];
+                act_out[(size_t)(b0 + j0 + j) * ld_act + f] = f2bf(g / (1.f + __expf(-g)) * u);
+              }
+            }
+          }
+          asm volatile("bar.sync 2, 128;" ::: "memory");
         }
       }
       tc_fence_before();
@@ -344,20 +380,22 @@ int linear_splits(int64_t n, int64_t k, int64_t b) {
   return best;
 }
 
-template <int BN>
-static int launch_gemm(const CUtensorMap& mw, const CUtensorMap& mx, float* out, int n, int b,
-                       int tiles, int splits, int chunks, cudaStream_t stream) {
+template <int BN, int EPI>
+static int launch_gemm(const CUtensorMap& mw, const CUtensorMap& mx, float* out, int n, int b, int tiles,
+                       int splits, int chunks, __nv_bfloat16* act_out, int ld_act, cudaStream_t stream) {
   using Cfg = GemmCfg<BN>;
   const int acts = (b + BN - 1) / BN;
   const int units = tiles * splits * acts;
   const int grid = units < kNumSMs ? units : kNumSMs;
-  return launch_k(gemm_swapab_kernel<BN>, dim3(grid), dim3(kGemmThreads), Cfg::kSmemBytes, stream, true, mw, mx,
-                  out, n, b, tiles, splits, chunks, acts);
+  return launch_k(gemm_swapab_kernel<BN, EPI>, dim3(grid), dim3(kGemmThreads), Cfg::kSmemBytes, stream, true, mw,
+                  mx, out, n, b, tiles, splits, chunks, acts, act_out, ld_act);
 }
 
 template <int BN>
 static int configure_one() {
-  TPS_CUDA_TRY(cudaFuncSetAttribute(gemm_swapab_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  TPS_CUDA_TRY(cudaFuncSetAttribute(gemm_swapab_kernel<BN, kEpiPartial>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    GemmCfg<BN>::kSmemBytes));
+  TPS_CUDA_TRY(cudaFuncSetAttribute(gemm_swapab_kernel<BN, kEpiSiluMul>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     GemmCfg<BN>::kSmemBytes));
   return kOk;
 }
@@ -372,27 +410,53 @@ int configure_gemm() {
   return rc;
 }
 
-int linear(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,
-           int64_t x_rows, int64_t ldx, float* out, int splits, cudaStream_t stream) {
-  TPS_CHECK_ARG(w && x && out, "linear: null pointer");
+template <int EPI>
+static int dispatch(int bn, const CUtensorMap& mw, const CUtensorMap& mx, float* out, int n, int b, int tiles,
+                    int splits, int chunks, __nv_bfloat16* act_out, int ld_act, cudaStream_t st) {
+  switch (bn) {
+    case 16: return launch_gemm<16, EPI>(mw, mx, out, n, b, tiles, splits, chunks, act_out, ld_act, st);
+    case 32: return launch_gemm<32, EPI>(mw, mx, out, n, b, tiles, splits, chunks, act_out, ld_act, st);
+    case 64: return launch_gemm<64, EPI>(mw, mx, out, n, b, tiles, splits, chunks, act_out, ld_act, st);
+    case 128: return launch_gemm<128, EPI>(mw, mx, out, n, b, tiles, splits, chunks, act_out, ld_act, st);
+    default: return launch_gemm<256, EPI>(mw, mx, out, n, b, tiles, splits, chunks, act_out, ld_act, st);
+  }
+}
+
+static int prepare(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
+                   int64_t ldx, CUtensorMap* mw, CUtensorMap* mx, int* bn) {
+  TPS_CHECK_ARG(w && x, "linear: null pointer");
   TPS_CHECK_ARG(n > 0 && k > 0 && b > 0 && b <= (1 << 20), "linear: need n,k > 0 and 1 <= b <= 2^20");
   TPS_CHECK_ARG(x_rows >= b && ldw >= k && ldx >= k, "linear: bad leading dimensions");
+  *bn = pick_bn(b);
+  int rc = make_tmap_bf16(mw, w, n, k, ldw, kBM);
+  if (rc) return rc;
+  return make_tmap_bf16(mx, x, x_rows, k, ldx, *bn);
+}
+
+int linear(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,
+           int64_t x_rows, int64_t ldx, float* out, int splits, cudaStream_t stream) {
+  TPS_CHECK_ARG(out, "linear: null output");
   const int64_t chunks = (k + kBK - 1) / kBK;
   TPS_CHECK_ARG(splits >= 1 && splits <= chunks, "linear: splits must be in [1, ceil(k/64)]");
-  const int bn = pick_bn(b);
   CUtensorMap mw, mx;
-  int rc = make_tmap_bf16(&mw, w, n, k, ldw, kBM);
+  int bn;
+  int rc = prepare(w, n, k, ldw, x, b, x_rows, ldx, &mw, &mx, &bn);
   if (rc) return rc;
-  rc = make_tmap_bf16(&mx, x, x_rows, k, ldx, bn);
+  return dispatch<kEpiPartial>(bn, mw, mx, out, (int)n, (int)b, (int)((n + kBM - 1) / kBM), splits, (int)chunks,
+                               nullptr, 0, stream);
+}
+
+int linear_silu(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
+                int64_t ldx, void* act, int64_t ld_act, cudaStream_t stream) {
+  TPS_CHECK_ARG(act && n % kBM == 0, "linear_silu: N = 2F must be a multiple of 128 (64-row gate/up blocks)");
+  TPS_CHECK_ARG(ld_act >= n / 2, "linear_silu: ld_act must be >= F");
+  const int64_t chunks = (k + kBK - 1) / kBK;
+  CUtensorMap mw, mx;
+  int bn;
+  int rc = prepare(w, n, k, ldw, x, b, x_rows, ldx, &mw, &mx, &bn);
   if (rc) return rc;
-  const int tiles = (int)((n + kBM - 1) / kBM);
-  switch (bn) {
-    case 16: return launch_gemm<16>(mw, mx, out, (int)n, (int)b, tiles, splits, (int)chunks, stream);
-    case 32: return launch_gemm<32>(mw, mx, out, (int)n, (int)b, tiles, splits, (int)chunks, stream);
-    case 64: return launch_gemm<64>(mw, mx, out, (int)n, (int)b, tiles, splits, (int)chunks, stream);
-    case 128: return launch_gemm<128>(mw, mx, out, (int)n, (int)b, tiles, splits, (int)chunks, stream);
-    default: return launch_gemm<256>(mw, mx, out, (int)n, (int)b, tiles, splits, (int)chunks, stream);
-  }
+  return dispatch<kEpiSiluMul>(bn, mw, mx, nullptr, (int)n, (int)b, (int)(n / kBM), 1, (int)chunks,
+                               reinterpret_cast<__nv_bfloat16*>(act), (int)ld_act, stream);
 }
 
 }  // namespace tps

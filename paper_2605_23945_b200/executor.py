@@ -179,6 +179,13 @@ class InferExecutor:
     def _splits(self, n: int, k: int, B: int) -> int:
         return nat.lib().tps_linear_splits(n, k, B)
 
+    def _fuse_silu(self, B: int) -> bool:
+        """SwiGLU in the gate/up epilogue needs split-K = 1: worth it when the 128-row
+        tiles (x activation tiles) alone fill most of the 148 SMs."""
+        bn = 16 if B <= 16 else 32 if B <= 32 else 64 if B <= 64 else 128 if B <= 128 else 256
+        units = (2 * self.F // 128) * (-(-B // bn))
+        return units >= 120
+
     def _linear(self, st, stats, w: torch.Tensor, x: torch.Tensor, B: int) -> tuple[int, int, int]:
         """Projection into the split-K workspace; returns the strided source (base, n, stride)."""
         n, k = w.shape
@@ -240,10 +247,17 @@ class InferExecutor:
             stats.add("paged_attention")
             srcs = self._linear(st, stats, W[(l, "w_o")], self.attn, B)
             yield from self._allreduce_norm(st, stats, 2 * l, srcs, B, W.tensor_ptr(l, "ln2"))
-            srcs = self._linear(st, stats, W[(l, "w_gu")], self.xn, B)
-            nat.check(lib.tps_silu_mul(*srcs, B, self.F, self.act.data_ptr(), self.F, st),
-                      "tps_silu_mul")
-            stats.add("silu_mul")
+            w_gu = W[(l, "w_gu")]
+            if self._fuse_silu(B):
+                nat.check(lib.tps_linear_silu(w_gu.data_ptr(), 2 * self.F, H, H, self.xn.data_ptr(), B,
+                                              self.xn.shape[0], H, self.act.data_ptr(), self.F, st),
+                          "tps_linear_silu")
+                stats.add("linear")
+            else:
+                srcs = self._linear(st, stats, w_gu, self.xn, B)
+                nat.check(lib.tps_silu_mul(*srcs, B, self.F, self.act.data_ptr(), self.F, st),
+                          "tps_silu_mul")
+                stats.add("silu_mul")
             srcs = self._linear(st, stats, W[(l, "w_d")], self.act, B)
             nxt = W.tensor_ptr(l + 1, "ln1") if l + 1 < L else W.tensor_ptr(-1, "ln_f")
             yield from self._allreduce_norm(st, stats, 2 * l + 1, srcs, B, nxt)

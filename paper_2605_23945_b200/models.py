@@ -89,6 +89,8 @@ class DecoderGeometry:
             raise ConfigError(f"{self.name}: too few query heads per KV head for tp={tp}")
         if self.ffn % tp or self.vocab % tp:
             raise ConfigError(f"{self.name}: ffn and vocab must be divisible by tp={tp}")
+        if (self.ffn // tp) % 64:
+            raise ConfigError(f"{self.name}: ffn/tp must be a multiple of 64 (gate/up blocks)")
 
 
 PRESETS: dict[str, DecoderGeometry] = {
@@ -171,6 +173,9 @@ def rank_shard(geom: DecoderGeometry, tp: int, rank: int) -> RankShard:
                      ffn=(rank * fw, (rank + 1) * fw), vocab=(rank * vw, (rank + 1) * vw))
 
 
+GU_BLOCK = 64  # gate/up interleave block (rows)
+
+
 # Sharded tensor families: (axis, full-coordinate ranges in shard storage order).
 # axis 0 = rows of a row-major [rows][cols] tensor, axis 1 = columns.
 def shard_ranges(geom: DecoderGeometry, family: str, sh: RankShard) -> tuple[int, list[tuple[int, int]]]:
@@ -184,8 +189,14 @@ def shard_ranges(geom: DecoderGeometry, family: str, sh: RankShard) -> tuple[int
     if family == "w_o":
         return 1, [(q0 * D, q1 * D)]
     if family == "w_gu":
+        # interleaved 64-row blocks [gate c | up c]: one 128-row GEMM tile holds the gate
+        # and up rows of the same 64 features, so SiLU(gate)*up fuses into its epilogue
         f0, f1 = sh.ffn
-        return 0, [(f0, f1), (geom.ffn + f0, geom.ffn + f1)]
+        out = []
+        for a in range(f0, f1, GU_BLOCK):
+            b = min(a + GU_BLOCK, f1)
+            out += [(a, b), (geom.ffn + a, geom.ffn + b)]
+        return 0, out
     if family == "w_d":
         return 1, [sh.ffn]
     if family == "lm_head":

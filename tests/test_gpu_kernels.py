@@ -163,3 +163,21 @@ def test_barrier_counters_virtual():
     nat.check(nat.lib().tps_barrier(peers, 3, ctr.data_ptr(), 1, _stream()))
     torch.cuda.synchronize()
     assert ctr.tolist() == [1, 1, 1, 1]
+
+
+@pytest.mark.parametrize("F,k,b", [(1024, 256, 1), (2368, 3584, 16), (18944, 3584, 64), (512, 512, 300)])
+def test_linear_silu_fused_epilogue(F, k, b):
+    """Gate/up GEMM with SwiGLU in the epilogue vs torch fp32 on the interleaved weight layout."""
+    torch.manual_seed(F + b)
+    w = (torch.randn(2 * F, k, device="cuda") * 0.05).bfloat16()   # rows: 64-blocks [gate c | up c]
+    x = torch.randn(b, k, device="cuda").bfloat16()
+    act = torch.zeros(b, F, device="cuda", dtype=torch.bfloat16)
+    nat.check(nat.lib().tps_linear_silu(w.data_ptr(), 2 * F, k, k, x.data_ptr(), b, b, k, act.data_ptr(), F,
+                                        _stream()))
+    torch.cuda.synchronize()
+    y = x.float() @ w.float().T                                       # [b, 2F]
+    blk = y.view(b, F // 64, 2, 64)
+    g, u = blk[:, :, 0, :].reshape(b, F), blk[:, :, 1, :].reshape(b, F)
+    ref = torch.nn.functional.silu(g) * u
+    err = (act.float() - ref).abs() / (ref.abs() + 1.0)
+    assert err.max().item() < 2e-2
