@@ -132,7 +132,12 @@ int tps_paged_attention(const void* q, const void* k_cache, const void* v_cache,
                         const int* pos_by_slot, const int* row_pos, const int* page_table, int max_pages, int B,
                         int nq,
                         int nkv, int D, int nsplit, float* part_m, float* part_l, float* part_o,
-                        unsigned int* merge_ctr, void* out, void* stream);
+                        unsigned int* merge_ctr, void* out, const float* qkv, int nqkv, int64_t qkv_stride,
+                        const void* qkv_bias, const float* cos_t, const float* sin_t, void* stream);
+/* Fused decode form (qkv != NULL, row_pos == NULL): q is not read; each CTA finishes its
+ * KV group's queries from the QKV split partials (sum + bias + RoPE), and the CTA owning
+ * the current token's page also appends that token's k/v to the cache -- the separate
+ * tps_qkv_rope_append launch is not needed. */
 
 /* act[b][f] = bf16(silu(g) * u) from split partials [s][B][2F] = [gate | up]. */
 int tps_silu_mul(const float* src, int nsrc, int64_t src_stride, int B, int F, void* out, int ldo,

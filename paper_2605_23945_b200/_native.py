@@ -43,7 +43,7 @@ SIGNATURES = {
                                    _i32, _i32, _vp, _vp, _vp, _vp]),
     "tps_attn_splits": (_i32, [_i32, _i32, _i32]),
     "tps_paged_attention": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32,
-                                   _vp, _vp, _vp, _vp, _vp, _vp]),
+                                   _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp, _vp]),
     "tps_silu_mul": (_i32, [_vp, _i32, _i64, _i32, _i32, _vp, _i32, _vp]),
     "tps_argmax_stage1": (_i32, [_vp, _i32, _i64, _i32, _i32, _i32, _i32, _vp, _pp, _i32, _vp, _vp]),
     "tps_argmax_finalize": (_i32, [_pp, _i32, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _i32, _vp, _vp]),

@@ -39,7 +39,8 @@ int epoch_advance(uint64_t*, cudaStream_t);
 int sum_src(const Src&, long long, float*, cudaStream_t);
 int attn_splits(int B, int nkv, int max_pages);
 int paged_attention(const void*, const void*, const void*, const int*, const int*, const int*, const int*, int, int,
-                    int, int, int, int, float*, float*, float*, unsigned int*, void*, cudaStream_t);
+                    int, int, int, int, float*, float*, float*, unsigned int*, void*, const Src&, const void*,
+                    const float*, const float*, cudaStream_t);
 int copy_items(const void*, int, int, int, cudaStream_t);
 int configure_gemm();
 int configure_attention();
@@ -171,13 +172,16 @@ int tps_paged_attention(const void* q, const void* k_cache, const void* v_cache,
                         const int* pos_by_slot, const int* row_pos, const int* page_table, int max_pages, int B,
                         int nq, int nkv, int D,
                         int nsplit, float* part_m, float* part_l, float* part_o, unsigned int* merge_ctr,
-                        void* out, void* stream) {
-  TPS_CHECK_ARG(q && k_cache && v_cache && row_slot && pos_by_slot && page_table && part_m && part_l && part_o &&
-                    merge_ctr && out,
+                        void* out, const float* qkv, int nqkv, int64_t qkv_stride, const void* qkv_bias,
+                        const float* cos_t, const float* sin_t, void* stream) {
+  TPS_CHECK_ARG(k_cache && v_cache && row_slot && pos_by_slot && page_table && part_m && part_l && part_o &&
+                    merge_ctr && out && (q || qkv),
                 "paged_attention: null pointer");
+  Src s;
+  int rc = make_src(qkv, qkv ? nqkv : 0, qkv_stride, &s);
+  if (rc) return rc;
   return paged_attention(q, k_cache, v_cache, row_slot, pos_by_slot, row_pos, page_table, max_pages, B, nq, nkv, D,
-                         nsplit,
-                         part_m, part_l, part_o, merge_ctr, out, S(stream));
+                         nsplit, part_m, part_l, part_o, merge_ctr, out, s, qkv_bias, cos_t, sin_t, S(stream));
 }
 
 int tps_silu_mul(const float* src, int nsrc, int64_t src_stride, int B, int F, void* out, int ldo, void* stream) {

@@ -62,13 +62,21 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_kernel(
     const int* __restrict__ pos_by_slot, const int* __restrict__ row_pos, const int* __restrict__ page_table,
     int max_pages, int nq, int nkv,
     int G, int nsplit, float scale_log2, float* __restrict__ part_m, float* __restrict__ part_l,
-    float* __restrict__ part_o, unsigned int* __restrict__ merge_ctr, __nv_bfloat16* __restrict__ out) {
+    float* __restrict__ part_o, unsigned int* __restrict__ merge_ctr, __nv_bfloat16* __restrict__ out,
+    Src qkv, const __nv_bfloat16* __restrict__ qkv_bias, const float* __restrict__ cos_t,
+    const float* __restrict__ sin_t) {
   constexpr int CPR = D / 8;       // 16-byte chunks per token row
   constexpr int TILE = kPage * D;  // elements per K (or V) page slice
+  constexpr int HALF = D / 2;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   __nv_bfloat16* sk = reinterpret_cast<__nv_bfloat16*>(smem_raw);
   __nv_bfloat16* sv = sk + kAttnStages * TILE;
   __shared__ int s_last;
+  // fused decode path: q (rotated) of this KV group and the current token's k/v,
+  // finished here from the QKV projection's split partials (no separate rope kernel)
+  __shared__ __align__(16) __nv_bfloat16 sq[16 * D];
+  __shared__ __align__(16) __nv_bfloat16 skv[2 * D];
+  const bool fused = qkv.n > 0;
 
   const int kvh = blockIdx.x, b = blockIdx.y, split = blockIdx.z;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -119,9 +127,67 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_kernel(
       cp_async_commit();
     }
 
+    const bool owner = fused && (p1 == npages);  // this split holds the current token's page
+    if (fused) {
+      // sum split partials + bias, rotate-half RoPE at pos = ctx-1, round to bf16
+      const int pos = ctx - 1;
+      const long long N = (long long)(nq + 2 * nkv) * D;
+      const long long row = (long long)b * N;
+      auto val = [&](int col) {
+        float v = qkv_bias ? bf2f(qkv_bias[col]) : 0.f;
+        const float* p = qkv.base + row + col;
+        for (int s = 0; s < qkv.n; ++s) v += p[(long long)s * qkv.stride];
+        return v;
+      };
+      for (int i = tid; i < 16 * HALF; i += kAttnThreads) {
+        const int h = i / HALF, d = i % HALF;
+        float y1 = 0.f, y2 = 0.f;
+        if (h < G) {
+          const float cs = cos_t[(size_t)pos * HALF + d], sn = sin_t[(size_t)pos * HALF + d];
+          const int c0 = (head0 + h) * D;
+          const float x1 = val(c0 + d), x2 = val(c0 + d + HALF);
+          y1 = x1 * cs - x2 * sn;
+          y2 = x2 * cs + x1 * sn;
+        }
+        sq[h * D + d] = f2bf(y1);
+        sq[h * D + d + HALF] = f2bf(y2);
+      }
+      if (owner) {
+        const int page = pt[pos / kPage];
+        const size_t off = (((size_t)page * nkv + kvh) * kPage + (pos % kPage)) * D;
+        for (int i = tid; i < 2 * HALF; i += kAttnThreads) {
+          const bool is_v = i >= HALF;
+          const int d = i % HALF;
+          const int c0 = (is_v ? (nq + nkv + kvh) : (nq + kvh)) * D;
+          const float x1 = val(c0 + d), x2 = val(c0 + d + HALF);
+          float y1 = x1, y2 = x2;
+          if (!is_v) {
+            const float cs = cos_t[(size_t)pos * HALF + d], sn = sin_t[(size_t)pos * HALF + d];
+            y1 = x1 * cs - x2 * sn;
+            y2 = x2 * cs + x1 * sn;
+          }
+          __nv_bfloat16* cache = const_cast<__nv_bfloat16*>(is_v ? v_cache : k_cache) + off;
+          cache[d] = f2bf(y1);
+          cache[d + HALF] = f2bf(y2);
+          skv[(is_v ? D : 0) + d] = f2bf(y1);
+          skv[(is_v ? D : 0) + d + HALF] = f2bf(y2);
+        }
+      }
+      __syncthreads();
+    }
+
     // Q fragments for the (up to 16) query heads of this KV group, held for the whole loop.
     uint32_t qa[D / 16][4];
-    {
+    if (fused) {
+#pragma unroll
+      for (int ks = 0; ks < D / 16; ++ks) {
+        const int d0 = ks * 16 + 2 * c;
+        qa[ks][0] = *reinterpret_cast<const uint32_t*>(sq + g * D + d0);
+        qa[ks][1] = *reinterpret_cast<const uint32_t*>(sq + (g + 8) * D + d0);
+        qa[ks][2] = *reinterpret_cast<const uint32_t*>(sq + g * D + d0 + 8);
+        qa[ks][3] = *reinterpret_cast<const uint32_t*>(sq + (g + 8) * D + d0 + 8);
+      }
+    } else {
       const __nv_bfloat16* q0 = q + ((size_t)b * nq + head0) * D;
 #pragma unroll
       for (int ks = 0; ks < D / 16; ++ks) {
@@ -148,6 +214,17 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_kernel(
         cp_async_commit();
       }
       const int st = it % kAttnStages;
+      if (owner && p0 + it == npages - 1) {
+        // the current token's k/v were computed in-kernel: patch them into the landed tile
+        const int r = (ctx - 1) % kPage;
+        for (int i = tid; i < 2 * CPR; i += kAttnThreads) {
+          const bool is_v = i >= CPR;
+          const int cc = i % CPR;
+          __nv_bfloat16* dst = (is_v ? sv : sk) + st * TILE + r * D + ((cc ^ (r & 7)) * 8);
+          *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(skv + (is_v ? D : 0) + cc * 8);
+        }
+        __syncthreads();
+      }
       const __nv_bfloat16* K = sk + st * TILE;
       const __nv_bfloat16* V = sv + st * TILE;
 
@@ -202,12 +279,16 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_kernel(
         }
       l_r[0] = l_r[0] * alpha[0] + rs[0];
       l_r[1] = l_r[1] * alpha[1] + rs[1];
+      // once the running max has settled (the common case after the first pages)
+      // the rescale is the identity: skip its D/2 multiplies per thread
+      if (!__all_sync(0xffffffffu, alpha[0] == 1.f && alpha[1] == 1.f)) {
 #pragma unroll
-      for (int i = 0; i < D / 8; ++i) {
-        o[i][0] *= alpha[0];
-        o[i][1] *= alpha[0];
-        o[i][2] *= alpha[1];
-        o[i][3] *= alpha[1];
+        for (int i = 0; i < D / 8; ++i) {
+          o[i][0] *= alpha[0];
+          o[i][1] *= alpha[0];
+          o[i][2] *= alpha[1];
+          o[i][3] *= alpha[1];
+        }
       }
 
       // O += P V
@@ -274,6 +355,8 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_kernel(
   }
 
   // ---- split merge by the last CTA of this (row, kv head) ----
+  // (with many splits the merge is done by attn_combine_kernel instead: merge_ctr == null)
+  if (merge_ctr == nullptr) return;
   __threadfence();
   __syncthreads();
   if (tid == 0) {
@@ -320,6 +403,59 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_kernel(
   if (tid == 0) merge_ctr[b * nkv + kvh] = 0u;  // re-arm for the next launch / graph replay
 }
 
+// Many-split merge (long contexts at small batch): one CTA per (row, query head), one
+// thread per head dim; the split maxima are reduced across lanes and every thread's
+// partial-O loads are issued in batches of 16, so the merge costs ~one L2 round trip.
+template <int D>
+__global__ void __launch_bounds__(D) attn_combine_kernel(const int* __restrict__ row_slot,
+                                                         const int* __restrict__ pos_by_slot,
+                                                         const int* __restrict__ row_pos, int nq, int nsplit,
+                                                         const float* __restrict__ part_m,
+                                                         const float* __restrict__ part_l,
+                                                         const float* __restrict__ part_o,
+                                                         __nv_bfloat16* __restrict__ out) {
+  __shared__ float fac[kMaxAttnSplits];
+  __shared__ float s_inv;
+  pdl_wait();
+  pdl_launch_dependents();
+  const int b = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
+  const int slot = row_slot[b];
+  const int ctx = slot >= 0 ? (row_pos ? row_pos[b] : pos_by_slot[slot]) + 1 : 0;
+  const int npages = (ctx + kPage - 1) / kPage;
+  int pps = (npages + nsplit - 1) / nsplit;
+  if (pps < kMinPagesPerSplit) pps = kMinPagesPerSplit;
+  const int active = (npages + pps - 1) / pps;
+  const size_t base = ((size_t)b * nq + h) * nsplit;
+  if (d < 32) {
+    float M = -INFINITY;
+    for (int s = d; s < active; s += 32) M = fmaxf(M, part_m[base + s]);
+    M = warp_max(M);
+    float L = 0.f;
+    for (int s = d; s < active; s += 32) {
+      const float ms = part_m[base + s];
+      const float f = (ms == -INFINITY || M == -INFINITY) ? 0.f : exp2f(ms - M);
+      fac[s] = f;
+      L += part_l[base + s] * f;
+    }
+    L = warp_sum(L);
+    if (d == 0) s_inv = L > 0.f ? 1.f / L : 0.f;
+  }
+  __syncthreads();
+  const float* po = part_o + base * D + d;
+  float acc = 0.f;
+  for (int s0 = 0; s0 < active; s0 += 16) {
+    float v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = (s0 + j < active) ? po[(size_t)(s0 + j) * D] : 0.f;
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (s0 + j < active) acc += v[j] * fac[s0 + j];
+  }
+  out[((size_t)b * nq + h) * D + d] = f2bf(acc * s_inv);
+}
+
+constexpr int kInKernelMergeMaxSplits = 4;
+
 template <int D>
 static constexpr int attn_smem() {
   return 2 * kAttnStages * kPage * D * 2;
@@ -346,8 +482,12 @@ int paged_attention(const void* q, const void* k_cache, const void* v_cache, con
                     const int* pos_by_slot, const int* row_pos, const int* page_table, int max_pages, int B, int nq,
                     int nkv, int D,
                     int nsplit, float* part_m, float* part_l, float* part_o, unsigned int* merge_ctr, void* out,
+                    const Src& qkv, const void* qkv_bias, const float* cos_t, const float* sin_t,
                     cudaStream_t st) {
   TPS_CHECK_ARG(B > 0 && nkv > 0 && nq % nkv == 0, "paged_attention: nq must be a multiple of nkv");
+  TPS_CHECK_ARG(qkv.n == 0 || (cos_t && sin_t && !row_pos),
+                "paged_attention: fused QKV finishing needs rope tables and is decode-only (row_pos == NULL)");
+  const auto* bias = reinterpret_cast<const __nv_bfloat16*>(qkv_bias);
   const int G = nq / nkv;
   TPS_CHECK_ARG(G <= 16, "paged_attention: at most 16 query heads per KV head");
   TPS_CHECK_ARG(nsplit >= 1 && nsplit <= kMaxAttnSplits, "paged_attention: 1 <= nsplit <= 128");
@@ -357,15 +497,25 @@ int paged_attention(const void* q, const void* k_cache, const void* v_cache, con
   const auto* kk = reinterpret_cast<const __nv_bfloat16*>(k_cache);
   const auto* vv = reinterpret_cast<const __nv_bfloat16*>(v_cache);
   auto* oo = reinterpret_cast<__nv_bfloat16*>(out);
+  const bool in_kernel = nsplit <= kInKernelMergeMaxSplits;
+  unsigned int* mc = in_kernel ? merge_ctr : nullptr;
+  int rc;
   if (D == 128)
-    return launch_k(paged_attn_kernel<128>, grid, dim3(kAttnThreads), attn_smem<128>(), st, true, qq, kk, vv,
-                    row_slot, pos_by_slot, row_pos, page_table, max_pages, nq, nkv, G, nsplit, scale_log2, part_m, part_l,
-                    part_o, merge_ctr, oo);
-  if (D == 64)
-    return launch_k(paged_attn_kernel<64>, grid, dim3(kAttnThreads), attn_smem<64>(), st, true, qq, kk, vv,
-                    row_slot, pos_by_slot, row_pos, page_table, max_pages, nq, nkv, G, nsplit, scale_log2, part_m, part_l,
-                    part_o, merge_ctr, oo);
-  return fail(kInvalid, "paged_attention: head_dim must be 64 or 128");
+    rc = launch_k(paged_attn_kernel<128>, grid, dim3(kAttnThreads), attn_smem<128>(), st, true, qq, kk, vv,
+                  row_slot, pos_by_slot, row_pos, page_table, max_pages, nq, nkv, G, nsplit, scale_log2, part_m,
+                  part_l, part_o, mc, oo, qkv, bias, cos_t, sin_t);
+  else if (D == 64)
+    rc = launch_k(paged_attn_kernel<64>, grid, dim3(kAttnThreads), attn_smem<64>(), st, true, qq, kk, vv,
+                  row_slot, pos_by_slot, row_pos, page_table, max_pages, nq, nkv, G, nsplit, scale_log2, part_m,
+                  part_l, part_o, mc, oo, qkv, bias, cos_t, sin_t);
+  else
+    return fail(kInvalid, "paged_attention: head_dim must be 64 or 128");
+  if (rc || in_kernel) return rc;
+  if (D == 128)
+    return launch_k(attn_combine_kernel<128>, dim3(B, nq), dim3(128), 0, st, true, row_slot, pos_by_slot, row_pos,
+                    nq, nsplit, (const float*)part_m, (const float*)part_l, (const float*)part_o, oo);
+  return launch_k(attn_combine_kernel<64>, dim3(B, nq), dim3(64), 0, st, true, row_slot, pos_by_slot, row_pos, nq,
+                  nsplit, (const float*)part_m, (const float*)part_l, (const float*)part_o, oo);
 }
 
 }  // namespace tps

@@ -116,6 +116,9 @@ class InferExecutor:
         # chunked prefill runs `prefill_rows` (sample, prompt position) rows per step
         self.prefill_rows = prefill_rows
         rows = max(max_batch, prefill_rows)
+        # finishing q/k/v inside the attention kernel saves a launch but every split CTA
+        # recomputes its group's queries; measured slower at B >= 1 on B200 (off by default)
+        self.fuse_rope = False
         self.device = torch.device(device)
         self.comm = comm
         self.tp = shard.tp
@@ -232,19 +235,26 @@ class InferExecutor:
             srcs = self._linear(st, stats, W[(l, "w_qkv")], self.xn, B)
             kc, vc = self.kv.layer_ptrs(l)
             bias = W.tensor_ptr(l, "b_qkv") if g.qkv_bias else None
-            nat.check(lib.tps_qkv_rope_append(*srcs, bias, rs, pos, rp,
-                                              sl.page_table.data_ptr(), sl.max_pages,
-                                              self.cos.data_ptr(), self.sin.data_ptr(), B, self.nq,
-                                              self.nkv, D, PAGE, self.q.data_ptr(), kc, vc, st),
-                      "tps_qkv_rope_append")
-            stats.add("qkv_rope_append")
+            if prefill or not self.fuse_rope:
+                # separate bias+RoPE+append launch (always for prefill: many rows of one
+                # sample per launch need every row's K/V appended before attention)
+                nat.check(lib.tps_qkv_rope_append(*srcs, bias, rs, pos, rp,
+                                                  sl.page_table.data_ptr(), sl.max_pages,
+                                                  self.cos.data_ptr(), self.sin.data_ptr(), B, self.nq,
+                                                  self.nkv, D, PAGE, self.q.data_ptr(), kc, vc, st),
+                          "tps_qkv_rope_append")
+                stats.add("qkv_rope_append")
+                fused = (None, 0, 0, None, None, None)
+            else:
+                # decode: bias + RoPE + KV append are finished inside the attention kernel
+                fused = (*srcs, bias, self.cos.data_ptr(), self.sin.data_ptr())
             nat.check(lib.tps_paged_attention(self.q.data_ptr(), kc, vc, rs, pos, rp, sl.page_table.data_ptr(),
                                               sl.max_pages, B, self.nq, self.nkv, D, nsplit,
                                               self.att_m.data_ptr(), self.att_l.data_ptr(),
                                               self.att_o.data_ptr(), self.att_ctr.data_ptr(),
-                                              self.attn.data_ptr(), st),
+                                              self.attn.data_ptr(), *fused, st),
                       "tps_paged_attention")
-            stats.add("paged_attention")
+            stats.add("paged_attention", 1 if nsplit <= 4 else 2)  # + split-merge kernel
             srcs = self._linear(st, stats, W[(l, "w_o")], self.attn, B)
             yield from self._allreduce_norm(st, stats, 2 * l, srcs, B, W.tensor_ptr(l, "ln2"))
             w_gu = W[(l, "w_gu")]

@@ -101,7 +101,7 @@ def test_paged_attention_matches_fp32(D, nq, nkv, ctxs):
         out = torch.empty(B, nq, D, device="cuda", dtype=torch.bfloat16)
         nat.check(lib.tps_paged_attention(q.data_ptr(), kc.data_ptr(), vc.data_ptr(), row_slot.data_ptr(),
                                           pos.data_ptr(), None, page_table.data_ptr(), max_pages, B, nq, nkv, D,
-                                          nsplit, pm.data_ptr(), pl.data_ptr(), po.data_ptr(), ctr.data_ptr(), out.data_ptr(),
+                                          nsplit, pm.data_ptr(), pl.data_ptr(), po.data_ptr(), ctr.data_ptr(), out.data_ptr(), None, 0, 0, None, None, None,
                                           _stream()))
         torch.cuda.synchronize()
         ref = _ref_attention(q.cpu(), kc.cpu(), vc.cpu(), perm.tolist(), [c - 1 for c in ctxs], nq // nkv)
@@ -125,7 +125,7 @@ def test_padding_rows_are_inert():
     ctr = torch.zeros(2 * nkv, dtype=torch.int32, device="cuda")
     nat.check(nat.lib().tps_paged_attention(q.data_ptr(), kc.data_ptr(), vc.data_ptr(), row_slot.data_ptr(),
                                             pos.data_ptr(), None, page_table.data_ptr(), 2, 2, nq, nkv, D, 3,
-                                            pm.data_ptr(), pl.data_ptr(), po.data_ptr(), ctr.data_ptr(), out.data_ptr(),
+                                            pm.data_ptr(), pl.data_ptr(), po.data_ptr(), ctr.data_ptr(), out.data_ptr(), None, 0, 0, None, None, None,
                                             _stream()))
     torch.cuda.synchronize()
     assert (out[0] == 0).all()
