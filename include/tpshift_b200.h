@@ -120,21 +120,28 @@ int tps_qkv_rope_append(const float* src, int nsrc, int64_t src_stride, const vo
                         const float* sin_t, int B, int nq, int nkv, int D, int page_size, void* q_out,
                         void* k_cache, void* v_cache, void* stream);
 
-/* Split count for tps_paged_attention. */
+/* Split policy for tps_paged_attention: 0 = page-balanced schedule (B x nkv >= 64,
+ * B <= 512), else the fixed split count for this shape. */
 int tps_attn_splits(int B, int nkv, int max_pages);
+/* fp32 elements of part_o a tps_paged_attention call needs (part_m / part_l: that / D);
+ * nsplit = 0 selects the page-balanced schedule. */
+int64_t tps_attn_workspace(int B, int nq, int D, int nsplit);
 
-/* Paged GQA decode attention over ctx = pos+1 tokens per row, split-KV; the last
- * CTA of each (row, kv head) merges the splits (log-sum-exp) and writes out bf16
- * [B][nq][D]. part_m/part_l: fp32 [B][nq][nsplit], part_o: fp32 [B][nq][nsplit][D]
- * scratch; merge_ctr: zero-initialised uint32 [B][nkv] (self re-arming). KV term
- * of tpshift/latency.py:123. */
+/* Paged GQA decode attention over ctx = pos+1 tokens per row, out bf16 [B][nq][D].
+ * nsplit = 0 (default): page-balanced schedule -- the (row, kv head, page) units of
+ * the launch are divided evenly over a persistent grid of resident CTAs, whatever the
+ * context lengths; a (row, kv head) cut between CTAs is merged (log-sum-exp) by its
+ * last piece. nsplit > 0: fixed split-KV per (row, kv head), merged by the last CTA.
+ * part_m/part_l/part_o: fp32 scratch of tps_attn_workspace elements (part_o; the
+ * others / D); merge_ctr: zero-initialised uint32 [B][nkv] (self re-arming). B <= 512
+ * for the balanced form. KV term of tpshift/latency.py:123. */
 int tps_paged_attention(const void* q, const void* k_cache, const void* v_cache, const int* row_slot,
-                        const int* pos_by_slot, const int* row_pos, const int* page_table, int max_pages, int B,
-                        int nq,
+                        const int* pos_by_slot, const int* row_pos, const int* page_table, int max_pages,
+                        int B, int nq,
                         int nkv, int D, int nsplit, float* part_m, float* part_l, float* part_o,
                         unsigned int* merge_ctr, void* out, const float* qkv, int nqkv, int64_t qkv_stride,
                         const void* qkv_bias, const float* cos_t, const float* sin_t, void* stream);
-/* Fused decode form (qkv != NULL, row_pos == NULL): q is not read; each CTA finishes its
+/* Fused decode form (qkv != NULL, row_pos == NULL, nsplit > 0): q is not read; each CTA finishes its
  * KV group's queries from the QKV split partials (sum + bias + RoPE), and the CTA owning
  * the current token's page also appends that token's k/v to the cache -- the separate
  * tps_qkv_rope_append launch is not needed. */

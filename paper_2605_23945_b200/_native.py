@@ -42,6 +42,7 @@ SIGNATURES = {
     "tps_qkv_rope_append": (_i32, [_vp, _i32, _i64, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _i32, _i32, _i32,
                                    _i32, _i32, _vp, _vp, _vp, _vp]),
     "tps_attn_splits": (_i32, [_i32, _i32, _i32]),
+    "tps_attn_workspace": (_i64, [_i32, _i32, _i32, _i32]),
     "tps_paged_attention": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32,
                                    _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp, _vp]),
     "tps_silu_mul": (_i32, [_vp, _i32, _i64, _i32, _i32, _vp, _i32, _vp]),

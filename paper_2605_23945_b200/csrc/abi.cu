@@ -38,8 +38,9 @@ int argmax_finalize(const CandList&, int, const WaitSpec&, int, const int*, int*
 int epoch_advance(uint64_t*, cudaStream_t);
 int sum_src(const Src&, long long, float*, cudaStream_t);
 int attn_splits(int B, int nkv, int max_pages);
-int paged_attention(const void*, const void*, const void*, const int*, const int*, const int*, const int*, int, int,
-                    int, int, int, int, float*, float*, float*, unsigned int*, void*, const Src&, const void*,
+int attn_balanced_grid(int D);
+int paged_attention(const void*, const void*, const void*, const int*, const int*, const int*, const int*, int,
+                    int, int, int, int, int, float*, float*, float*, unsigned int*, void*, const Src&, const void*,
                     const float*, const float*, cudaStream_t);
 int copy_items(const void*, int, int, int, cudaStream_t);
 int configure_gemm();
@@ -168,9 +169,14 @@ int tps_qkv_rope_append(const float* src, int nsrc, int64_t src_stride, const vo
 
 int tps_attn_splits(int B, int nkv, int max_pages) { return attn_splits(B, nkv, max_pages); }
 
+int64_t tps_attn_workspace(int B, int nq, int D, int nsplit) {
+  if (nsplit > 0) return (int64_t)B * nq * nsplit * D;
+  return (int64_t)attn_balanced_grid(D) * 2 * 16 * D;
+}
+
 int tps_paged_attention(const void* q, const void* k_cache, const void* v_cache, const int* row_slot,
-                        const int* pos_by_slot, const int* row_pos, const int* page_table, int max_pages, int B,
-                        int nq, int nkv, int D,
+                        const int* pos_by_slot, const int* row_pos, const int* page_table, int max_pages,
+                        int B, int nq, int nkv, int D,
                         int nsplit, float* part_m, float* part_l, float* part_o, unsigned int* merge_ctr,
                         void* out, const float* qkv, int nqkv, int64_t qkv_stride, const void* qkv_bias,
                         const float* cos_t, const float* sin_t, void* stream) {
@@ -180,7 +186,8 @@ int tps_paged_attention(const void* q, const void* k_cache, const void* v_cache,
   Src s;
   int rc = make_src(qkv, qkv ? nqkv : 0, qkv_stride, &s);
   if (rc) return rc;
-  return paged_attention(q, k_cache, v_cache, row_slot, pos_by_slot, row_pos, page_table, max_pages, B, nq, nkv, D,
+  return paged_attention(q, k_cache, v_cache, row_slot, pos_by_slot, row_pos, page_table, max_pages, B, nq,
+                         nkv, D,
                          nsplit, part_m, part_l, part_o, merge_ctr, out, s, qkv_bias, cos_t, sin_t, S(stream));
 }
 

@@ -16,44 +16,13 @@
 //     fragment loads); the G query heads sharing a KV head form the 16-row
 //     MMA operand, so QK^T and PV run on the tensor pipe and the CTA only
 //     streams bytes.
-#include "common.cuh"
-#include "decode_ops.cuh"
+#include "attention_common.cuh"
 
 namespace tps {
 
-constexpr int kPage = 64;
-constexpr int kAttnThreads = 128;
-constexpr int kAttnStages = 3;
 constexpr int kMinPagesPerSplit = 2;
 constexpr int kMaxAttnSplits = 128;
-
-__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-  return *reinterpret_cast<uint32_t*>(&v);
-}
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* g) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(g) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-__device__ __forceinline__ void ldmatrix_x4_trans(uint32_t (&r)[4], const void* smem) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-               : "r"(smem_u32(smem)));
-}
+int attn_fixed_splits(int B, int nkv, int max_pages);
 
 template <int D>
 __global__ void __launch_bounds__(kAttnThreads) paged_attn_kernel(
@@ -188,15 +157,7 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_kernel(
         qa[ks][3] = *reinterpret_cast<const uint32_t*>(sq + (g + 8) * D + d0 + 8);
       }
     } else {
-      const __nv_bfloat16* q0 = q + ((size_t)b * nq + head0) * D;
-#pragma unroll
-      for (int ks = 0; ks < D / 16; ++ks) {
-        const int d0 = ks * 16 + 2 * c;
-        qa[ks][0] = (g < G) ? *reinterpret_cast<const uint32_t*>(q0 + g * D + d0) : 0u;
-        qa[ks][1] = (g + 8 < G) ? *reinterpret_cast<const uint32_t*>(q0 + (g + 8) * D + d0) : 0u;
-        qa[ks][2] = (g < G) ? *reinterpret_cast<const uint32_t*>(q0 + g * D + d0 + 8) : 0u;
-        qa[ks][3] = (g + 8 < G) ? *reinterpret_cast<const uint32_t*>(q0 + (g + 8) * D + d0 + 8) : 0u;
-      }
+      load_q_frags<D>(qa, q + ((size_t)b * nq + head0) * D, G);
     }
 
     float m_r[2] = {-INFINITY, -INFINITY};
@@ -225,87 +186,7 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_kernel(
         }
         __syncthreads();
       }
-      const __nv_bfloat16* K = sk + st * TILE;
-      const __nv_bfloat16* V = sv + st * TILE;
-
-      // S = Q K^T for this warp's 16 tokens (two 8-token n-tiles)
-      float s[2][4];
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
-        const int t = warp * 16 + nt * 8 + g;
-        const __nv_bfloat16* krow = K + t * D + 2 * c;
-#pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks) {
-          const uint32_t b0 = *reinterpret_cast<const uint32_t*>(krow + (((2 * ks) ^ (t & 7)) * 8));
-          const uint32_t b1 = *reinterpret_cast<const uint32_t*>(krow + (((2 * ks + 1) ^ (t & 7)) * 8));
-          mma16816(s[nt], qa[ks], b0, b1);
-        }
-      }
-      const int tok0 = (p0 + it) * kPage + warp * 16;
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int tok = tok0 + nt * 8 + 2 * c + (e & 1);
-          s[nt][e] = (tok < ctx) ? s[nt][e] * scale_log2 : -INFINITY;
-        }
-
-      // online softmax (rows g and g+8), per-warp running state
-      float mx[2];
-      mx[0] = fmaxf(fmaxf(s[0][0], s[0][1]), fmaxf(s[1][0], s[1][1]));
-      mx[1] = fmaxf(fmaxf(s[0][2], s[0][3]), fmaxf(s[1][2], s[1][3]));
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
-        mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
-      }
-      float alpha[2], mnew[2];
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        mnew[r] = fmaxf(m_r[r], mx[r]);
-        alpha[r] = (mnew[r] == -INFINITY) ? 1.f : exp2f(m_r[r] - mnew[r]);
-        m_r[r] = mnew[r];
-      }
-      float rs[2] = {0.f, 0.f};
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int r = e >> 1;
-          const float p = (mnew[r] == -INFINITY) ? 0.f : exp2f(s[nt][e] - mnew[r]);
-          s[nt][e] = p;
-          rs[r] += p;
-        }
-      l_r[0] = l_r[0] * alpha[0] + rs[0];
-      l_r[1] = l_r[1] * alpha[1] + rs[1];
-      // once the running max has settled (the common case after the first pages)
-      // the rescale is the identity: skip its D/2 multiplies per thread
-      if (!__all_sync(0xffffffffu, alpha[0] == 1.f && alpha[1] == 1.f)) {
-#pragma unroll
-        for (int i = 0; i < D / 8; ++i) {
-          o[i][0] *= alpha[0];
-          o[i][1] *= alpha[0];
-          o[i][2] *= alpha[1];
-          o[i][3] *= alpha[1];
-        }
-      }
-
-      // O += P V
-      uint32_t pa[4];
-      pa[0] = pack_bf16(s[0][0], s[0][1]);
-      pa[1] = pack_bf16(s[0][2], s[0][3]);
-      pa[2] = pack_bf16(s[1][0], s[1][1]);
-      pa[3] = pack_bf16(s[1][2], s[1][3]);
-      const int vrow = warp * 16 + (lane & 15);
-#pragma unroll
-      for (int dn2 = 0; dn2 < D / 16; ++dn2) {
-        const int chunk = 2 * dn2 + (lane >> 4);
-        uint32_t r[4];
-        ldmatrix_x4_trans(r, V + vrow * D + ((chunk ^ (vrow & 7)) * 8));
-        mma16816(o[2 * dn2], pa, r[0], r[1]);
-        mma16816(o[2 * dn2 + 1], pa, r[2], r[3]);
-      }
+      attend_page<D>(sk + st * TILE, sv + st * TILE, qa, (p0 + it) * kPage, ctx, scale_log2, m_r, l_r, o);
     }
     cp_async_wait<0>();
 
@@ -461,7 +342,15 @@ static constexpr int attn_smem() {
   return 2 * kAttnStages * kPage * D * 2;
 }
 
+int paged_attention_balanced(const void* q, const void* k_cache, const void* v_cache, const int* row_slot,
+                             const int* pos_by_slot, const int* row_pos, const int* page_table, int max_pages,
+                             int B, int nq, int nkv, int D, float* part_m, float* part_l, float* part_o,
+                             unsigned int* merge_ctr, void* out, cudaStream_t st);
+int configure_attention_balanced();
+
 int configure_attention() {
+  int rc = configure_attention_balanced();
+  if (rc) return rc;
   TPS_CUDA_TRY(cudaFuncSetAttribute(paged_attn_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     attn_smem<128>()));
   TPS_CUDA_TRY(cudaFuncSetAttribute(paged_attn_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -469,8 +358,16 @@ int configure_attention() {
   return kOk;
 }
 
+// Split policy: 0 = page-balanced schedule (when the (row, kv head) segments alone
+// give a few hundred units of parallel work), else the fixed split count that
+// keeps the grid within one wave of resident CTAs (2 per SM).
 int attn_splits(int B, int nkv, int max_pages) {
-  int want = (2 * kNumSMs + B * nkv - 1) / (B * nkv);
+  if (B * nkv >= 64 && B <= kBalMaxRows) return 0;
+  return attn_fixed_splits(B, nkv, max_pages);
+}
+
+int attn_fixed_splits(int B, int nkv, int max_pages) {
+  int want = (2 * kNumSMs) / (B * nkv);
   const int cap = (max_pages + kMinPagesPerSplit - 1) / kMinPagesPerSplit;
   if (want > cap) want = cap;
   if (want > 32) want = 32;  // the last-CTA merge reads active x G x D partials: keep it short
@@ -479,8 +376,8 @@ int attn_splits(int B, int nkv, int max_pages) {
 }
 
 int paged_attention(const void* q, const void* k_cache, const void* v_cache, const int* row_slot,
-                    const int* pos_by_slot, const int* row_pos, const int* page_table, int max_pages, int B, int nq,
-                    int nkv, int D,
+                    const int* pos_by_slot, const int* row_pos, const int* page_table, int max_pages,
+                    int B, int nq, int nkv, int D,
                     int nsplit, float* part_m, float* part_l, float* part_o, unsigned int* merge_ctr, void* out,
                     const Src& qkv, const void* qkv_bias, const float* cos_t, const float* sin_t,
                     cudaStream_t st) {
@@ -490,7 +387,11 @@ int paged_attention(const void* q, const void* k_cache, const void* v_cache, con
   const auto* bias = reinterpret_cast<const __nv_bfloat16*>(qkv_bias);
   const int G = nq / nkv;
   TPS_CHECK_ARG(G <= 16, "paged_attention: at most 16 query heads per KV head");
-  TPS_CHECK_ARG(nsplit >= 1 && nsplit <= kMaxAttnSplits, "paged_attention: 1 <= nsplit <= 128");
+  TPS_CHECK_ARG(nsplit >= 0 && nsplit <= kMaxAttnSplits, "paged_attention: 0 <= nsplit <= 128");
+  TPS_CHECK_ARG(nsplit > 0 || qkv.n == 0, "paged_attention: the fused QKV form needs an explicit split count");
+  if (nsplit == 0)
+    return paged_attention_balanced(q, k_cache, v_cache, row_slot, pos_by_slot, row_pos, page_table, max_pages, B,
+                                    nq, nkv, D, part_m, part_l, part_o, merge_ctr, out, st);
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)D);
   const dim3 grid(nkv, B, nsplit);
   const auto* qq = reinterpret_cast<const __nv_bfloat16*>(q);

@@ -147,10 +147,13 @@ class InferExecutor:
             for n, k in self._proj_shapes():
                 ws = max(ws, nat.lib().tps_linear_splits(n, k, B) * B * n)
         self.ws = torch.zeros(ws, dtype=torch.float32, device=dev)
-        att = max(nat.lib().tps_attn_splits(B, self.nkv, slots.max_pages) * B for B in sizes)
-        self.att_m = torch.zeros(att * self.nq, dtype=torch.float32, device=dev)
+        # attention partial states: the page-balanced schedule (nsplit 0) and, for the
+        # fused-RoPE form, the fixed split count of every bucket
+        att = max(nat.lib().tps_attn_workspace(B, self.nq, D, s) for B in sizes
+                  for s in (0, self._attn_splits(B, True)))
+        self.att_o = torch.zeros(att, dtype=torch.float32, device=dev)
+        self.att_m = torch.zeros(att // D, dtype=torch.float32, device=dev)
         self.att_l = torch.zeros_like(self.att_m)
-        self.att_o = torch.zeros(att * self.nq * D, dtype=torch.float32, device=dev)
         self.att_ctr = torch.zeros(rows * self.nkv, dtype=torch.int32, device=dev)
         self.local_cand = torch.zeros((max_batch, 64, 2), dtype=torch.int32, device=dev)
         self.out_tok = torch.zeros(max_batch, dtype=torch.int32, device=dev)
@@ -188,6 +191,11 @@ class InferExecutor:
         bn = 16 if B <= 16 else 32 if B <= 32 else 64 if B <= 64 else 128 if B <= 128 else 256
         units = (2 * self.F // 128) * (-(-B // bn))
         return units >= 120
+
+    def _attn_splits(self, B: int, fused: bool) -> int:
+        """tps_attn_splits policy (0 = page-balanced); the fused-RoPE form needs a fixed count."""
+        s = nat.lib().tps_attn_splits(B, self.nkv, self.slots.max_pages)
+        return max(1, min(32, 2 * 148 // (B * self.nkv))) if (fused and s == 0) else s
 
     def _linear(self, st, stats, w: torch.Tensor, x: torch.Tensor, B: int) -> tuple[int, int, int]:
         """Projection into the split-K workspace; returns the strided source (base, n, stride)."""
@@ -230,12 +238,13 @@ class InferExecutor:
         nat.check(lib.tps_add_norm(self.resid.data_ptr(), None, 0, 0, None, W.tensor_ptr(0, "ln1"), eps,
                                    H, B, self.xn.data_ptr(), H, st), "tps_add_norm")
         stats.add("add_norm")
-        nsplit = lib.tps_attn_splits(B, self.nkv, sl.max_pages)
+        fuse = self.fuse_rope and not prefill
+        nsplit = self._attn_splits(B, fuse)
         for l in range(L):
             srcs = self._linear(st, stats, W[(l, "w_qkv")], self.xn, B)
             kc, vc = self.kv.layer_ptrs(l)
             bias = W.tensor_ptr(l, "b_qkv") if g.qkv_bias else None
-            if prefill or not self.fuse_rope:
+            if not fuse:
                 # separate bias+RoPE+append launch (always for prefill: many rows of one
                 # sample per launch need every row's K/V appended before attention)
                 nat.check(lib.tps_qkv_rope_append(*srcs, bias, rs, pos, rp,
@@ -254,7 +263,7 @@ class InferExecutor:
                                               self.att_o.data_ptr(), self.att_ctr.data_ptr(),
                                               self.attn.data_ptr(), *fused, st),
                       "tps_paged_attention")
-            stats.add("paged_attention", 1 if nsplit <= 4 else 2)  # + split-merge kernel
+            stats.add("paged_attention", 1 if nsplit <= 4 else 2)  # (+ split-merge kernel)
             srcs = self._linear(st, stats, W[(l, "w_o")], self.attn, B)
             yield from self._allreduce_norm(st, stats, 2 * l, srcs, B, W.tensor_ptr(l, "ln2"))
             w_gu = W[(l, "w_gu")]

@@ -81,6 +81,7 @@ def _ref_attention(q, kc, vc, page_table, pos, G):
     (128, 7, 1, [1, 64, 65, 300]), (128, 28, 4, [5000, 17]), (64, 4, 2, [130, 1]),
     (128, 4, 1, [2049]), (128, 16, 1, [100, 1000])])
 def test_paged_attention_matches_fp32(D, nq, nkv, ctxs):
+    """Page-balanced schedule (nsplit 0) and fixed split counts (in-kernel and combine merge)."""
     torch.manual_seed(D + nq + len(ctxs))
     B = len(ctxs)
     max_pages = max((c + 63) // 64 for c in ctxs) + 1
@@ -94,10 +95,11 @@ def test_paged_attention_matches_fp32(D, nq, nkv, ctxs):
     q = torch.randn(B, nq, D, device="cuda").bfloat16()
     lib = nat.lib()
     ctr = torch.zeros(B * nkv, dtype=torch.int32, device="cuda")
-    for nsplit in (1, lib.tps_attn_splits(B, nkv, max_pages), 7):
-        pm = torch.empty(B * nq * nsplit, device="cuda")
+    for nsplit in (0, 1, lib.tps_attn_splits(B, nkv, max_pages), 7):
+        ws = lib.tps_attn_workspace(B, nq, D, nsplit)
+        pm = torch.empty(ws // D, device="cuda")
         pl = torch.empty_like(pm)
-        po = torch.empty(B * nq * nsplit * D, device="cuda")
+        po = torch.empty(ws, device="cuda")
         out = torch.empty(B, nq, D, device="cuda", dtype=torch.bfloat16)
         nat.check(lib.tps_paged_attention(q.data_ptr(), kc.data_ptr(), vc.data_ptr(), row_slot.data_ptr(),
                                           pos.data_ptr(), None, page_table.data_ptr(), max_pages, B, nq, nkv, D,
@@ -111,7 +113,8 @@ def test_paged_attention_matches_fp32(D, nq, nkv, ctxs):
         assert int(ctr.sum()) == 0  # merge counters re-armed by the last CTA
 
 
-def test_padding_rows_are_inert():
+@pytest.mark.parametrize("nsplit", [0, 3])
+def test_padding_rows_are_inert(nsplit):
     D, nq, nkv = 128, 4, 1
     kc = torch.randn(4, nkv, 64, D, device="cuda").bfloat16()
     vc = torch.randn_like(kc)
@@ -119,17 +122,66 @@ def test_padding_rows_are_inert():
     row_slot = torch.tensor([-1, 0], dtype=torch.int32, device="cuda")
     pos = torch.tensor([10], dtype=torch.int32, device="cuda")
     q = torch.randn(2, nq, D, device="cuda").bfloat16()
-    pm = torch.empty(2 * nq * 3, device="cuda")
-    pl, po = torch.empty_like(pm), torch.empty(2 * nq * 3 * D, device="cuda")
+    ws = nat.lib().tps_attn_workspace(2, nq, D, nsplit)
+    pm = torch.empty(ws // D, device="cuda")
+    pl, po = torch.empty_like(pm), torch.empty(ws, device="cuda")
     out = torch.full((2, nq, D), 7.0, device="cuda", dtype=torch.bfloat16)
     ctr = torch.zeros(2 * nkv, dtype=torch.int32, device="cuda")
     nat.check(nat.lib().tps_paged_attention(q.data_ptr(), kc.data_ptr(), vc.data_ptr(), row_slot.data_ptr(),
-                                            pos.data_ptr(), None, page_table.data_ptr(), 2, 2, nq, nkv, D, 3,
+                                            pos.data_ptr(), None, page_table.data_ptr(), 2, 2, nq, nkv, D, nsplit,
                                             pm.data_ptr(), pl.data_ptr(), po.data_ptr(), ctr.data_ptr(), out.data_ptr(), None, 0, 0, None, None, None,
                                             _stream()))
     torch.cuda.synchronize()
     assert (out[0] == 0).all()
     assert torch.isfinite(out[1].float()).all()
+
+
+@pytest.mark.parametrize("B,max_ctx,prefill", [(200, 3000, False), (3, 20000, False), (512, 700, True)])
+def test_balanced_attention_ragged(B, max_ctx, prefill):
+    """Page-balanced schedule on ragged batches: segments cut across many CTAs, one
+    very long row next to short ones, and the prefill form (row_pos, 512 rows)."""
+    torch.manual_seed(B)
+    D, nq, nkv = 128, 28, 4
+    lib = nat.lib()
+    ctxs = torch.randint(1, max_ctx + 1, (B,)).tolist()
+    ctxs[0] = max_ctx
+    max_pages = (max_ctx + 63) // 64
+    nslots = B if not prefill else 4
+    num_pages = nslots * max_pages
+    kc = torch.randn(num_pages, nkv, 64, D, device="cuda").bfloat16()
+    vc = torch.randn(num_pages, nkv, 64, D, device="cuda").bfloat16()
+    perm = torch.randperm(num_pages).view(nslots, max_pages).int()
+    if prefill:  # rows = (slot, position) pairs; several rows per slot
+        row_slot = torch.randint(0, nslots, (B,), dtype=torch.int32)
+        row_slot[5] = -1  # a padding row
+        row_pos = torch.tensor([c - 1 for c in ctxs], dtype=torch.int32)
+        pos = torch.zeros(nslots, dtype=torch.int32)
+    else:
+        row_slot = torch.arange(B, dtype=torch.int32)
+        row_pos = None
+        pos = torch.tensor([c - 1 for c in ctxs], dtype=torch.int32)
+    q = torch.randn(B, nq, D, device="cuda").bfloat16()
+    ws = lib.tps_attn_workspace(B, nq, D, 0)
+    pm, po = torch.empty(ws // D, device="cuda"), torch.empty(ws, device="cuda")
+    pl = torch.empty_like(pm)
+    ctr = torch.zeros(B * nkv, dtype=torch.int32, device="cuda")
+    out = torch.full((B, nq, D), 3.0, device="cuda", dtype=torch.bfloat16)
+    rs_d, pos_d, pt_d = row_slot.cuda(), pos.cuda(), perm.cuda()
+    rp_d = row_pos.cuda() if prefill else None
+    for _ in range(2):  # second launch checks the merge counters re-armed
+        nat.check(lib.tps_paged_attention(q.data_ptr(), kc.data_ptr(), vc.data_ptr(), rs_d.data_ptr(), pos_d.data_ptr(),
+                                          rp_d.data_ptr() if prefill else None, pt_d.data_ptr(), max_pages, B, nq,
+                                          nkv, D, 0, pm.data_ptr(), pl.data_ptr(), po.data_ptr(), ctr.data_ptr(),
+                                          out.data_ptr(), None, 0, 0, None, None, None, _stream()))
+        torch.cuda.synchronize()
+        assert int(ctr.sum()) == 0
+    valid = [b for b in range(B) if int(row_slot[b]) >= 0]
+    tables = [perm[int(row_slot[b])].tolist() for b in valid]
+    ref = _ref_attention(q.cpu()[valid], kc.cpu(), vc.cpu(), tables, [ctxs[b] - 1 for b in valid], nq // nkv)
+    err = (out.float().cpu()[valid] - ref).abs().max().item()
+    assert err < 2e-2, err
+    if prefill:
+        assert (out[5] == 0).all()
 
 
 @pytest.mark.parametrize("mode", [0, 1])
