@@ -40,7 +40,7 @@ from .models import DecoderGeometry, rank_shard
 from .shards import RankWeights
 from .switch_executor import (KVSource, KVTarget, Layout, Pieces, check, nvlink_bytes, plan_history_pulls,
                               plan_kv_pulls, plan_weight_pulls, to_items, verify_cover)
-from .switchcost import RECOMPUTE, SwitchCostBreakdown
+from .switchcost import MIGRATE, RECOMPUTE, SwitchCostBreakdown
 
 
 PREFILL_ROWS = 512  # (sample, prompt position) rows per chunked-prefill step
@@ -68,6 +68,7 @@ class SwitchTiming:
     weight_bytes: int
     host_plan_s: float
     host_capture_s: float
+    state_method: str = MIGRATE
 
 
 class B200Backend:
@@ -77,8 +78,11 @@ class B200Backend:
 
     def __init__(self, spec: ScenarioSpec, geom: DecoderGeometry, world: World, seed: int = 0,
                  use_graphs: bool = True, copy_mode: int = 0, prompts: np.ndarray | None = None,
-                 host_io: bool = False):
+                 host_io: bool = False, state_method: str | None = None):
         self.spec, self.geom, self.world = spec, geom, world
+        # None: each switch handles KV state as Algorithm 1 priced it (migrate or
+        # recompute); MIGRATE / RECOMPUTE force one method (measurement, tests)
+        self.state_method = state_method
         self.use_graphs = use_graphs
         self.copy_mode = copy_mode
         self.host_io = host_io
@@ -123,19 +127,20 @@ class B200Backend:
         lay = lay or self.layout
         return sorted({lay.group_of(r) for r in self.world.local_ranks})
 
-    def _build_layout(self, lay: Layout, weights_seed: int | None, per_group: dict[int, int] | None = None):
+    def _build_layout(self, lay: Layout, weights_seed: int | None, per_group: dict[int, int] | None = None,
+                      prefill: bool = True):
         comms = self.cache.get(lay.tp)
         ranks = {}
         for r in self.world.local_ranks:
             n = self.max_batch if per_group is None else per_group.get(lay.group_of(r), 0)
-            ranks[r] = self._make_rank(lay, r, max(1, n), weights_seed, comms[r])
+            ranks[r] = self._make_rank(lay, r, max(1, n), weights_seed, comms[r], prefill)
         self.ranks = ranks
         self.runners = {}
         for g in self.local_groups(lay):
             exs = [ranks[r].executor for r in lay.ranks_of_group(g) if r in ranks]
             self.runners[g] = GroupRunner(exs, use_graphs=self.use_graphs)
 
-    def _make_rank(self, lay: Layout, r: int, slots: int, weights_seed, comm) -> RankState:
+    def _make_rank(self, lay: Layout, r: int, slots: int, weights_seed, comm, prefill: bool) -> RankState:
         dev = self.world.devices[r]
         nat.init_device(dev.index or 0)
         sh = rank_shard(self.geom, lay.tp, lay.tp_rank(r))
@@ -144,7 +149,7 @@ class B200Backend:
             w.fill_random(weights_seed)
         kv = KVPool(self.geom.num_layers, sh.n_kv, self.geom.head_dim, slots * pages_for(self.max_len), dev)
         st = SlotTable(slots, self.max_len, dev)
-        pf = slots * max(1, PREFILL_ROWS // slots) if self.epoch == 0 else 0
+        pf = slots * max(1, PREFILL_ROWS // slots) if prefill else 0
         ex = InferExecutor(self.geom, sh, w, kv, st, slots, dev, comm=comm, prefill_rows=pf)
         return RankState(w, kv, st, ex, comm)
 
@@ -252,11 +257,12 @@ class B200Backend:
 
     def realize_switch(self, node: NodeState, decision, statuses, merged, naive_mode: bool):
         quote = decision.breakdown
-        if quote.state_method == RECOMPUTE and not naive_mode:
-            raise NotImplementedError("recompute state handling (prefill under the target TP) is the next "
-                                      "component (SURVEY 8(f) rank 1); the B200 path executes migration")
-        self._execute_switch(decision.target.tp, merged)
-        return quote
+        method = self.state_method or quote.state_method
+        self._execute_switch(decision.target.tp, merged, recompute=method == RECOMPUTE)
+        # host-side placeholder with the realised method; the reported clocks come from
+        # the recorded events (RecordedBackend)
+        return SwitchCostBreakdown.build(quote.t_state_handling, method, quote.t_weight_reshard,
+                                         quote.t_graph_recapture, quote.t_comm_group_init, quote.t_fixed_control)
 
     def switch_record_extra(self, node: NodeState) -> dict:
         t = self.switches[-1]
@@ -270,7 +276,12 @@ class B200Backend:
         pass
 
     # -------------------------------------------------------------- switch ---
-    def _execute_switch(self, tp_new: int, merged: list[list]) -> None:
+    def _execute_switch(self, tp_new: int, merged: list[list], recompute: bool = False) -> None:
+        """Weights are always pulled (canonical slices of the new layout). KV state is
+        either migrated (page pulls, tpshift/reshard.py:113-151) or recomputed: only
+        the token histories move, and every sample's KV is rebuilt by a chunked
+        prefill over its prompt + generated tokens under the new TP
+        (tpshift/switchcost.py:203-219, engine.py:187-203)."""
         old, new = self.layout, Layout(tp_new, self.world.gpus)
         old_ranks = self.ranks
         # where every live sample sits now: {id: (old group, slot, pages)}, gathered across processes
@@ -291,7 +302,8 @@ class B200Backend:
         self._device_barrier()  # every rank has finished decoding on the old layout
         self.epoch += 1
         self.layout = new
-        self._build_layout(new, weights_seed=None, per_group={g: len(m) for g, m in enumerate(merged)})
+        self._build_layout(new, weights_seed=None, per_group={g: len(m) for g, m in enumerate(merged)},
+                           prefill=recompute)
         stats = dict(nv=0, loc=0, kv=0, w=0)
         t_plan = 0.0
         for r in self.world.local_ranks:
@@ -330,7 +342,7 @@ class B200Backend:
             by_pool: dict[int, list[int]] = {}
             for i, s in enumerate(srcs):
                 by_pool.setdefault(npg[s.old_group * old.tp], []).append(i)
-            for n_old, idxs in by_pool.items():
+            for n_old, idxs in (by_pool.items() if not recompute else ()):
                 p = plan_kv_pulls(self.geom, old, new, r, [srcs[i] for i in idxs], [tgts[i] for i in idxs],
                                   [kvlen[i] for i in idxs], n_old, rs.kv.num_pages)
                 kp.add(*p.arrays())
@@ -347,9 +359,19 @@ class B200Backend:
             self._copy(w_items, st)
             marks[r].append(_event(st))
             self._copy(items, st)
-            marks[r].append(_event(st))
+            if not recompute:
+                marks[r].append(_event(st))
             for s, t in zip(mine, tgts):
                 self.slot_of[s.id] = t.slot
+        if recompute:
+            # rebuild each new group's KV from the pulled histories: positions < pos
+            for g in self.local_groups(new):
+                mine = merged[g] if g < len(merged) else []
+                if mine:
+                    self.kernels_launched += self.runners[g].prefill(
+                        [self.slot_of[s.id] for s in mine], [s.context_len - 1 for s in mine])
+            for r in self.world.local_ranks:
+                marks[r].append(_event(self.stream(r)))
         self._device_barrier()  # every rank has finished pulling: old buffers may be released
         for r in self.world.local_ranks:
             marks[r].append(_event(self.stream(r)))
@@ -357,7 +379,8 @@ class B200Backend:
         self.capture_all()
         self.switches.append(SwitchTiming(marks=marks, nvlink_bytes=stats["nv"], local_bytes=stats["loc"],
                                           kv_bytes=stats["kv"], weight_bytes=stats["w"], host_plan_s=t_plan,
-                                          host_capture_s=time.perf_counter() - tc))
+                                          host_capture_s=time.perf_counter() - tc,
+                                          state_method=RECOMPUTE if recompute else MIGRATE))
         self._keep.append(old_ranks)  # released after the stage (stream-ordered frees would also do)
 
     def _copy(self, items: np.ndarray, st) -> None:
@@ -403,7 +426,8 @@ class B200Backend:
             out["switches"].append({
                 "ranks": {r: [self.start[r].elapsed_time(e) / 1e3 for e in ev] for r, ev in t.marks.items()},
                 "nvlink_bytes": t.nvlink_bytes, "local_bytes": t.local_bytes, "kv_bytes": t.kv_bytes,
-                "weight_bytes": t.weight_bytes, "host_plan_s": t.host_plan_s, "host_capture_s": t.host_capture_s})
+                "weight_bytes": t.weight_bytes, "host_plan_s": t.host_plan_s, "host_capture_s": t.host_capture_s,
+                "state_method": t.state_method})
         self._keep.clear()
         return out
 
@@ -419,7 +443,7 @@ class RecordedBackend:
             self.groups.update(m["groups"])
         self.switch_meas = []
         for i in range(max((len(m["switches"]) for m in meas), default=0)):
-            agg = dict(ranks={}, nv=0, loc=0, kv=0, w=0, plan=0.0, cap=0.0)
+            agg = dict(ranks={}, nv=0, loc=0, kv=0, w=0, plan=0.0, cap=0.0, method=MIGRATE)
             for m in meas:
                 if i < len(m["switches"]):
                     s = m["switches"][i]
@@ -430,6 +454,7 @@ class RecordedBackend:
                     agg["w"] += s["weight_bytes"]
                     agg["plan"] = max(agg["plan"], s["host_plan_s"])
                     agg["cap"] = max(agg["cap"], s["host_capture_s"])
+                    agg["method"] = s.get("state_method", MIGRATE)
             self.switch_meas.append(agg)
         self.epoch = 0
         self.cursor: dict[str, int] = {}
@@ -456,14 +481,14 @@ class RecordedBackend:
         w = min(w, total)
         kv = min(kv, total - w)
         self.nswitch += 1
-        return SwitchCostBreakdown.build(kv, decision.breakdown.state_method, w, 0.0, 0.0, total - w - kv)
+        return SwitchCostBreakdown.build(kv, m["method"], w, 0.0, 0.0, total - w - kv)
 
     def switch_record_extra(self, node) -> dict:
         m = self.switch_meas[self.nswitch - 1]
         marks = list(m["ranks"].values())
         copy_s = max(v[2] for v in marks) - min(v[0] for v in marks)
         moved = m["nv"] + m["loc"]
-        return {"measured": True, "nvlink_bytes_total": m["nv"], "local_copy_bytes": m["loc"],
+        return {"measured": True, "state_method": m["method"], "nvlink_bytes_total": m["nv"], "local_copy_bytes": m["loc"],
                 "kv_bytes": m["kv"], "weight_bytes": m["w"], "copy_seconds": copy_s,
                 "copy_gbps_per_gpu": (moved / max(1, len(marks))) / copy_s / 1e9 if copy_s > 0 else None,
                 "host_plan_s": m["plan"], "host_capture_s": m["cap"]}
@@ -479,14 +504,15 @@ class GlobalCoordinator:
     """Run one generation stage on B200 and report it in the reference's SimReport schema."""
 
     def __init__(self, spec: ScenarioSpec, geom: DecoderGeometry, world: World | None = None, seed: int = 0,
-                 table=None, use_graphs: bool = True, copy_mode: int = 0, host_io: bool = False):
+                 table=None, use_graphs: bool = True, copy_mode: int = 0, host_io: bool = False,
+                 state_method: str | None = None):
         self.spec = spec
         self.geom = geom
         self.world = world or World.virtual(spec.cluster.gpus_per_node)
         self.table = table
         self.seed = seed
         self.backend = B200Backend(spec, geom, self.world, seed=seed, use_graphs=use_graphs,
-                                   copy_mode=copy_mode, host_io=host_io)
+                                   copy_mode=copy_mode, host_io=host_io, state_method=state_method)
         self.setup_capture_s = self.backend.capture_all()
         self.runs = 0
         self.last_wall_s = 0.0

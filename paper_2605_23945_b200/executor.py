@@ -23,6 +23,7 @@ from __future__ import annotations
 import ctypes
 from dataclasses import dataclass, field
 
+import numpy as np
 import torch
 
 from . import _native as nat
@@ -426,31 +427,46 @@ class GroupRunner:
         return self.stats[B].kernels if B in self.stats else 0
 
     # ------------------------------------------------------ chunked prefill ---
-    def prefill(self, slots: list[int], prompt_len: int) -> int:
-        """Process prompt positions 0 .. prompt_len-2 of `slots` through the decode kernels,
-        `prefill_rows // len(slots)` positions per step (each step's K/V appended before its
-        attention, so rows attend causally). Position prompt_len-1 is left for decode
-        round 1, matching the reference's round accounting. Returns kernels launched."""
+    def prefill(self, slots: list[int], lengths) -> int:
+        """Process positions 0 .. n_i-1 of every slot through the decode kernels
+        (n_i = lengths[i], or lengths - 1 for every slot when an int prompt length is
+        given: the last prompt position is decode round 1, matching the reference's
+        round accounting). Rows are (slot, position) pairs in position-major order,
+        `prefill_rows` per step; each step's K/V are appended before its attention, so
+        every row attends causally. The tokens must already be in the history table.
+        Afterwards every slot's decode position is n_i. Returns kernels launched.
+
+        The ragged form is the recompute path of a switch (tpshift/switchcost.py:203-219):
+        a migrated sample's KV is rebuilt from its prompt + generated tokens under the
+        target TP instead of being copied."""
         R = self.ex[0].prefill_rows
-        todo = prompt_len - 1
-        if todo <= 0 or not slots:
+        if isinstance(lengths, (int, np.integer)):
+            lengths = [int(lengths) - 1] * len(slots)
+        lengths = [max(0, int(n)) for n in lengths]
+        if not slots or max(lengths, default=0) == 0:
             return 0
-        if R < len(slots):
-            raise ValueError(f"prefill_rows={R} < {len(slots)} samples")
-        chunk = R // len(slots)
+        if R <= 0:
+            raise ValueError("this executor was built without prefill rows")
+        rows_s, rows_p = [], []
+        for p in range(max(lengths)):
+            for s, n in zip(slots, lengths):
+                if p < n:
+                    rows_s.append(s)
+                    rows_p.append(p)
+        rows_s = torch.tensor(rows_s, dtype=torch.int32)
+        rows_p = torch.tensor(rows_p, dtype=torch.int32)
         key = ("prefill", R)
         kernels = 0
-        sl = torch.tensor(slots, dtype=torch.int32)
-        for p0 in range(0, todo, chunk):
-            n = min(chunk, todo - p0)
+        for k0 in range(0, len(rows_s), R):
+            k = min(R, len(rows_s) - k0)
             rs = torch.full((R,), -1, dtype=torch.int32)
             rp = torch.zeros(R, dtype=torch.int32)
-            k = n * len(slots)          # position-major rows: (p0 + j, slot)
-            rs[:k] = sl.repeat(n)
-            rp[:k] = torch.arange(p0, p0 + n, dtype=torch.int32).repeat_interleave(len(slots))
+            rs[:k] = rows_s[k0:k0 + k]
+            rp[:k] = rows_p[k0:k0 + k]
+            rs, rp = rs.pin_memory(), rp.pin_memory()
             for e in self.ex:
-                e.row_slot[R].copy_(rs.pin_memory(), non_blocking=True)
-                e.row_pos[R].copy_(rp.pin_memory(), non_blocking=True)
+                e.row_slot[R].copy_(rs, non_blocking=True)
+                e.row_pos[R].copy_(rp, non_blocking=True)
             if self.use_graphs:
                 if key not in self.graphs:
                     self._capture_key(key, lambda st: self._issue_prefill(R, st))
@@ -458,9 +474,9 @@ class GroupRunner:
             else:
                 self.stats[key] = self._issue_prefill(R, torch.cuda.current_stream().cuda_stream)
             kernels += self.kernels_per_step(key)
-        idx = sl.long().pin_memory()
-        val = torch.full((len(slots),), prompt_len - 1, dtype=torch.int32).pin_memory()
-        for e in self.ex:  # decode round 1 processes the last prompt token
+        idx = torch.tensor(slots, dtype=torch.long).pin_memory()
+        val = torch.tensor(lengths, dtype=torch.int32).pin_memory()
+        for e in self.ex:  # the next decode round processes position n_i
             e.slots.pos.index_copy_(0, idx.to(e.device, non_blocking=True), val.to(e.device, non_blocking=True))
         return kernels
 

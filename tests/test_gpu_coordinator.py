@@ -96,6 +96,25 @@ def test_adaptive_stage_switches_and_matches_oracle(name):
     assert agree == checked, f"{checked - agree} of {checked} confident tokens disagree with the oracle"
 
 
+@pytest.mark.parametrize("name", ["tiny", "mini-qwen"])
+def test_recompute_switch_matches_oracle(name):
+    """State handling by recomputation: only token histories move; every sample's KV
+    is rebuilt under the target TP by the ragged chunked prefill."""
+    from paper_2605_23945_b200.switchcost import RECOMPUTE
+    geom = geometry(name)
+    spec = tiny_spec(geom)
+    coord = GlobalCoordinator(spec, geom, World.virtual(4), seed=7, state_method=RECOMPUTE)
+    report, meas = coord.run()
+    sw = [s for nr in report.node_reports for s in nr["switches"]]
+    assert len(sw) >= 1
+    for s in sw:
+        assert s["state_method"] == RECOMPUTE and s["breakdown"]["state_method"] == RECOMPUTE
+        assert s["kv_bytes"] > 0  # histories only
+    checked, agree = oracle_check(geom, 7, coord, spec)
+    assert checked > 50
+    assert agree == checked, f"{checked - agree} of {checked} confident tokens disagree with the oracle"
+
+
 def test_static_single_group_matches_adaptive_tokens_before_switch():
     geom = geometry("tiny")
     spec = tiny_spec(geom, mode="static", gpus=1, batch=6, initial_tp=1)
