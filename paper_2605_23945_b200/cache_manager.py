@@ -45,7 +45,9 @@ class World:
         n = int(os.environ.get("WORLD_SIZE", "1"))
         rank = int(os.environ.get("RANK", "0"))
         local = int(os.environ.get("LOCAL_RANK", str(rank)))
-        d = torch.device(f"cuda:{local}")
+        # TPS_SHARE_DEVICE=1: every rank's process on cuda:0 (the IPC/peer-counter path of a
+        # multi-GPU node exercised on one device; the kernels time-slice between processes)
+        d = torch.device("cuda:0" if os.environ.get("TPS_SHARE_DEVICE") == "1" else f"cuda:{local}")
         torch.cuda.set_device(d)
         if n > 1 and not dist.is_initialized():
             dist.init_process_group(backend="gloo")

@@ -113,6 +113,7 @@ class B200Backend:
         self.kernels_launched = 0
         self.h2d_bytes = 0
         self.d2h_bytes = 0
+        self.retired_here: list[int] = []  # samples whose tokens this process wrote to out_host
         self.start: dict[int, torch.cuda.Event] = {}
         self._keep: list = []
         self._barrier_epoch = 0
@@ -165,6 +166,7 @@ class B200Backend:
         self.timeline = {}
         self.switches = []
         self.slot_of = {}
+        self.retired_here = []
         self.kernels_launched = 0
         self.h2d_bytes = self.d2h_bytes = 0
         self.start = {}
@@ -250,6 +252,7 @@ class B200Backend:
             if lead:
                 n = min(s.target_response_len, self.spec.l_max)
                 self.out_host[s.id, :n].copy_(grp[0].slots.history[slot, lo:lo + n], non_blocking=True)
+                self.retired_here.append(s.id)
                 self.d2h_bytes += 4 * n
             for r in grp:
                 r.kv.release(r.slots.pages.get(slot, []))

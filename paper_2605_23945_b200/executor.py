@@ -120,6 +120,8 @@ class InferExecutor:
         # finishing q/k/v inside the attention kernel saves a launch but every split CTA
         # recomputes its group's queries; measured slower at B >= 1 on B200 (off by default)
         self.fuse_rope = False
+        # launch kinds left out of the step program (timing probes only: results are garbage)
+        self.skip: frozenset = frozenset()
         self.device = torch.device(device)
         self.comm = comm
         self.tp = shard.tp
@@ -202,6 +204,8 @@ class InferExecutor:
         """Projection into the split-K workspace; returns the strided source (base, n, stride)."""
         n, k = w.shape
         s = self._splits(n, k, B)
+        if "linear" in self.skip:
+            return (self.ws.data_ptr(), s, B * n)
         nat.check(nat.lib().tps_linear(w.data_ptr(), n, k, k, x.data_ptr(), B, x.shape[0],
                                        x.shape[1], self.ws.data_ptr(), s, st), "tps_linear")
         stats.add("linear")
@@ -245,7 +249,11 @@ class InferExecutor:
             srcs = self._linear(st, stats, W[(l, "w_qkv")], self.xn, B)
             kc, vc = self.kv.layer_ptrs(l)
             bias = W.tensor_ptr(l, "b_qkv") if g.qkv_bias else None
-            if not fuse:
+            fused = (None, 0, 0, None, None, None)
+            if fuse:
+                # decode: bias + RoPE + KV append are finished inside the attention kernel
+                fused = (*srcs, bias, self.cos.data_ptr(), self.sin.data_ptr())
+            elif "qkv_rope" not in self.skip:
                 # separate bias+RoPE+append launch (always for prefill: many rows of one
                 # sample per launch need every row's K/V appended before attention)
                 nat.check(lib.tps_qkv_rope_append(*srcs, bias, rs, pos, rp,
@@ -254,17 +262,14 @@ class InferExecutor:
                                                   self.nkv, D, PAGE, self.q.data_ptr(), kc, vc, st),
                           "tps_qkv_rope_append")
                 stats.add("qkv_rope_append")
-                fused = (None, 0, 0, None, None, None)
-            else:
-                # decode: bias + RoPE + KV append are finished inside the attention kernel
-                fused = (*srcs, bias, self.cos.data_ptr(), self.sin.data_ptr())
-            nat.check(lib.tps_paged_attention(self.q.data_ptr(), kc, vc, rs, pos, rp, sl.page_table.data_ptr(),
-                                              sl.max_pages, B, self.nq, self.nkv, D, nsplit,
-                                              self.att_m.data_ptr(), self.att_l.data_ptr(),
-                                              self.att_o.data_ptr(), self.att_ctr.data_ptr(),
-                                              self.attn.data_ptr(), *fused, st),
-                      "tps_paged_attention")
-            stats.add("paged_attention", 1 if nsplit <= 4 else 2)  # (+ split-merge kernel)
+            if "attention" not in self.skip:
+                nat.check(lib.tps_paged_attention(self.q.data_ptr(), kc, vc, rs, pos, rp, sl.page_table.data_ptr(),
+                                                  sl.max_pages, B, self.nq, self.nkv, D, nsplit,
+                                                  self.att_m.data_ptr(), self.att_l.data_ptr(),
+                                                  self.att_o.data_ptr(), self.att_ctr.data_ptr(),
+                                                  self.attn.data_ptr(), *fused, st),
+                          "tps_paged_attention")
+                stats.add("paged_attention", 1 if nsplit <= 4 else 2)  # (+ split-merge kernel)
             srcs = self._linear(st, stats, W[(l, "w_o")], self.attn, B)
             yield from self._allreduce_norm(st, stats, 2 * l, srcs, B, W.tensor_ptr(l, "ln2"))
             w_gu = W[(l, "w_gu")]
@@ -329,9 +334,10 @@ class InferExecutor:
         eps = ctypes.c_float(g.rms_eps)
         cm = self.comm
         if cm is None:
-            nat.check(lib.tps_add_norm(self.resid.data_ptr(), *srcs, None, norm_w, eps, H,
-                                       B, self.xn.data_ptr(), H, st), "tps_add_norm")
-            stats.add("add_norm")
+            if "add_norm" not in self.skip:
+                nat.check(lib.tps_add_norm(self.resid.data_ptr(), *srcs, None, norm_w, eps, H,
+                                           B, self.xn.data_ptr(), H, st), "tps_add_norm")
+                stats.add("add_norm")
             return
         par = phase % 2
         dsts = [cm.recv_slot(base, par, self.rank) for base in cm.peer_recv]
