@@ -24,6 +24,7 @@ Run: python bench.py [--gpus N --steps K --warmup W]; N>1 under torchrun.
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import statistics
@@ -55,6 +56,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=4)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-switch", action="store_true")
+    ap.add_argument("--static-tps", default="1", help="N>1: also time the stage at these fixed TP degrees")
     ap.add_argument("--cpu-threads", type=int, default=0)
     return ap.parse_args()
 
@@ -222,16 +225,20 @@ def main():
                "d2h_bytes_per_step": be.d2h_bytes, "device_clock_s": erep.generation_time}
         coord.backend.host_io = False
     # ---- roofline of the dominant kernel (tcgen05 projection GEMM), weighted by the stage's rounds
-    ex = next(iter(coord.backend.ranks.values())).executor
-    hist = {}
+    # at the initial layout (rounds after a switch run sharded GEMMs of another TP degree)
+    coord.backend.reset(0)
+    ex = coord.backend.ranks[rank].executor
+    dp0 = gpus // spec.initial_tp
+    hist, other_rounds = {}, 0
     for nr in rep.node_reports:
         for ev in nr["events"]:
             if ev["type"] == "step-block":
                 lo, hi = (int(x) for x in ev["detail"].split("=")[1].split(".."))
-                hist[ex.bucket(ev["active"]) if ev["active"] <= ex.max_batch else ex.max_batch] = \
-                    hist.get(ex.bucket(ev["active"]), 0) + (hi - lo) * 1
-    b0 = ex.bucket(min(ex.max_batch, spec.global_batch // gpus))
-    hist[b0] = hist.get(b0, 0) + args.prompt_len - 1  # prefill rounds run the same step
+                if ev["tp"] != spec.initial_tp:
+                    other_rounds += hi - lo
+                    continue
+                bk = ex.bucket(min(ex.max_batch, -(-ev["active"] // dp0)))
+                hist[bk] = hist.get(bk, 0) + (hi - lo)
     probes = {}
     for B in sorted(hist):
         probes[B] = gemm_probe(ex, B)["total"]
@@ -265,11 +272,32 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None, "kernel": "gemm_swapab_kernel (tcgen05)",
                      "peak_source": peak_src,
-                     "per_bucket": {str(B): {"gbps": probes[B]["gbps"], "rounds": hist[B]} for B in sorted(hist)}},
+                     "per_bucket": {str(B): {"gbps": probes[B]["gbps"], "rounds": hist[B]} for B in sorted(hist)},
+                     "rounds_at_other_tp": other_rounds},
         "clocks": clk.summary(),
     }
     if e2e:
         line["e2e"] = e2e
+    tr = traffic_record()
+    if tr:
+        line["roofline"]["traffic"] = tr["dram_bytes"]
+        line["roofline"]["traffic_note"] = (f"ncu dram read+write of one launch ({tr['launch']}) vs its "
+                                            f"{tr['algorithmic_bytes']} algorithmic bytes; profiles/r1/ncu_traffic.json")
+    if gpus > 1 and args.static_tps:
+        # the north-star comparison: the same stage at a fixed TP (no switching), same engine
+        line["fixed_tp"] = {}
+        for tp in (int(x) for x in args.static_tps.split(",")):
+            if gpus % tp:
+                continue
+            ex = coord = None
+            torch.cuda.empty_cache()
+            sspec = dataclasses.replace(spec, mode="static", initial_tp=tp)
+            coord = GlobalCoordinator(sspec, geom, world, seed=0)
+            coord.run()
+            srep, _ = coord.run()
+            line["fixed_tp"][str(tp)] = srep.generation_time
+    if rank == 0 and gpus == 1 and not args.no_switch:
+        line["switch_microbench"] = switch_microbench(args, peak)
     if rank == 0 and gpus == 1 and not args.no_cpu:
         threads = args.cpu_threads or os.cpu_count()
         step_t, raw = cpu_step_model(geom, threads)
@@ -285,6 +313,37 @@ def main():
         print(json.dumps(line), flush=True)
 
 
+def traffic_record():
+    try:
+        with open(os.path.join(HERE, "profiles", "r1", "ncu_traffic.json")) as fh:
+            return json.load(fh)["gemm_swapab_kernel"]
+    except Exception:
+        return None
+
+
+def switch_microbench(args, hbm_peak):
+    """BASELINE config 5 on one device: a real Switch Executor run TP1/DP2 -> TP2/DP1 of the
+    bench model in a virtual 2-rank world (both ranks on this GPU, so every pull is an HBM
+    copy: the bound is the HBM copy peak, read + write). 16 live samples at context 4096."""
+    import dataclasses
+    from paper_2605_23945_b200.cache_manager import World
+    from paper_2605_23945_b200.profiler import switch_probe
+    ns = argparse.Namespace(model=args.model, per_gpu_batch=8, l_max=args.l_max, prompt_len=args.prompt_len,
+                            seed=args.seed)
+    spec, geom = build_spec(ns, 2)
+    spec = dataclasses.replace(spec, initial_tp=1, global_batch=16)
+    r = switch_probe(spec, geom, World.virtual(2), 2, 16, 4096, copy_mode=1)
+    torch.cuda.empty_cache()
+    return {"config": f"c5: {args.model}, virtual TP1/DP2 -> TP2/DP1 on one B200, 16 samples at ctx 4096, "
+                      f"TMA bulk copy engine",
+            "weights_bytes": r["weights_bytes"], "kv_bytes": r["kv_bytes"], "copy_bytes": r["copy_bytes"],
+            "copy_kernel_ms": r["copy_kernel_ms"], "copy_gbps": r["copy_gbps"],
+            "roofline": {"bound": "hbm", "achieved": 2 * r["copy_gbps"], "peak": hbm_peak, "unit": "GB/s",
+                         "frac": 2 * r["copy_gbps"] / hbm_peak, "note": "read+write bytes of the copy kernels"},
+            "switch_device_ms": r["switch_device_ms"], "host_plan_s": r["host_plan_s"],
+            "host_capture_s": r["host_capture_s"]}
+
+
 def reference_arm(args):
     """The reference-side CPU path: the oracle port on the host cores (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
@@ -292,7 +351,7 @@ def reference_arm(args):
         return
     from paper_2605_23945_b200.engine import run as sim_run
     from paper_2605_23945_b200.models import geometry
-    spec, geom = build_spec(args, 1)
+    spec, geom = build_spec(args, max(1, args.gpus))
     threads = args.cpu_threads or os.cpu_count()
     # the stage's round profile (batch per round) comes from the reference's own loop on the
     # analytic model: identical samples, lengths and block structure
@@ -313,7 +372,7 @@ def reference_arm(args):
         vals.append(est)
     value = float(np.mean(vals[args.warmup:]))
     sample = (f"CPU oracle (torch fp32, {threads} threads): 1 decoder layer + LM head at B=1 and B=64, ctx "
-              f"2048, extrapolated to 28 layers and the stage's {sum(hist.values())} rounds")
+              f"2048, extrapolated to {geom.num_layers} layers and the stage's {sum(hist.values())} rounds")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False,

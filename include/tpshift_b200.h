@@ -79,6 +79,18 @@ int tps_linear_splits(int64_t n, int64_t k, int64_t b);
 int tps_linear(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,
                int64_t x_rows, int64_t ldx, float* out, int splits, void* stream);
 
+/* Row-parallel projection with the TP allreduce fused into its epilogue (O and
+ * down projections; the comm term of oracle_decode_latency, tpshift/latency.py:125-126):
+ * every split-K partial tile is stored straight into each destination -- this
+ * rank's slots in every TP peer's receive area, NVLink P2P stores -- at
+ * dsts[d] + split * split_stride + i * n + j (fp32); the last CTA of the launch
+ * then adds 1 to every sig_ctrs[] counter (release, system scope; `done` is the
+ * launch site's CTA counter). The consumer (tps_add_norm with a counter wait)
+ * sums the tp x splits slots in (rank, split) order. */
+int tps_linear_push(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,
+                    int64_t x_rows, int64_t ldx, float* const* dsts, int ndst, int64_t split_stride,
+                    int splits, uint64_t* const* sig_ctrs, int nsig, unsigned int* done, void* stream);
+
 /* Gate/up projection with the SwiGLU fused into the epilogue (no split-K):
  * W rows are 64-row blocks [gate c | up c] (n = 2F, F % 64 == 0);
  * act[i][f] = bf16(silu(gate_f . x_i) * (up_f . x_i)), act: bf16 [b][ld_act]. */

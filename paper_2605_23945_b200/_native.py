@@ -35,6 +35,8 @@ SIGNATURES = {
     "tps_set_pdl": (None, [_i32]),
     "tps_linear_splits": (_i32, [_i64, _i64, _i64]),
     "tps_linear": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _vp, _i32, _vp]),
+    "tps_linear_push": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _pp, _i32, _i64, _i32, _pp, _i32,
+                                _vp, _vp]),
     "tps_linear_silu": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _vp, _i64, _vp]),
     "tps_embed": (_i32, [_vp, _vp, _vp, _vp, _i32, _vp, _i32, _i32, _vp, _vp]),
     "tps_add_norm": (_i32, [_vp, _vp, _i32, _i64, _vp, _vp, _f32, _i32, _i32, _vp, _i32, _vp]),

@@ -38,8 +38,8 @@ from .group import RankState, admit, h2d, n_phases
 from .kvcache import KVPool, SlotTable, pages_for
 from .models import DecoderGeometry, rank_shard
 from .shards import RankWeights
-from .switch_executor import (KVSource, KVTarget, Layout, Pieces, check, nvlink_bytes, plan_history_pulls,
-                              plan_kv_pulls, plan_weight_pulls, to_items, verify_cover)
+from .switch_executor import (KVSource, KVTarget, Layout, Pieces, cached_weight_pulls, check, nvlink_bytes,
+                              plan_history_pulls, plan_kv_pulls, to_items, verify_cover)
 from .switchcost import MIGRATE, RECOMPUTE, SwitchCostBreakdown
 
 
@@ -69,6 +69,7 @@ class SwitchTiming:
     host_plan_s: float
     host_capture_s: float
     state_method: str = MIGRATE
+    host_build_s: float = 0.0
 
 
 class B200Backend:
@@ -114,6 +115,7 @@ class B200Backend:
         self.h2d_bytes = 0
         self.d2h_bytes = 0
         self.retired_here: list[int] = []  # samples whose tokens this process wrote to out_host
+        self.copy_events: list | None = None  # (start event, bytes, end event) per copy launch (probes)
         self.start: dict[int, torch.cuda.Event] = {}
         self._keep: list = []
         self._barrier_epoch = 0
@@ -303,17 +305,18 @@ class B200Backend:
             npg.update(part)
         marks = {r: [_event(self.stream(r))] for r in self.world.local_ranks}
         self._device_barrier()  # every rank has finished decoding on the old layout
+        tb = time.perf_counter()
         self.epoch += 1
         self.layout = new
         self._build_layout(new, weights_seed=None, per_group={g: len(m) for g, m in enumerate(merged)},
                            prefill=recompute)
         stats = dict(nv=0, loc=0, kv=0, w=0)
+        t_build = time.perf_counter() - tb
         t_plan = 0.0
         for r in self.world.local_ranks:
             rs, st = self.ranks[r], self.stream(r)
             t0 = time.perf_counter()
-            wp = plan_weight_pulls(self.geom, old, new, r)
-            check(verify_cover(wp, rs.weights.nbytes, allow_gaps=True), "weight pull plan")
+            wp = cached_weight_pulls(self.geom, old, new, r)  # verified once when first planned
             w_items = to_items(wp, {k: v["w"] for k, v in ptrs.items()}, rs.weights.arena.data_ptr())
             nv, loc = nvlink_bytes(wp, r)
             stats["nv"] += nv
@@ -383,7 +386,8 @@ class B200Backend:
         self.switches.append(SwitchTiming(marks=marks, nvlink_bytes=stats["nv"], local_bytes=stats["loc"],
                                           kv_bytes=stats["kv"], weight_bytes=stats["w"], host_plan_s=t_plan,
                                           host_capture_s=time.perf_counter() - tc,
-                                          state_method=RECOMPUTE if recompute else MIGRATE))
+                                          state_method=RECOMPUTE if recompute else MIGRATE,
+                                          host_build_s=t_build))
         self._keep.append(old_ranks)  # released after the stage (stream-ordered frees would also do)
 
     def _copy(self, items: np.ndarray, st) -> None:
@@ -391,8 +395,12 @@ class B200Backend:
             return
         host = torch.from_numpy(np.ascontiguousarray(items, dtype=np.int64)).pin_memory()
         dev = host.to(st.device, non_blocking=True)
+        if self.copy_events is not None:
+            self.copy_events.append((_event(st), int(items[:, 2].sum())))
         nat.check(nat.lib().tps_copy_items(dev.data_ptr(), len(items), self.copy_mode, 0, st.cuda_stream),
                   "tps_copy_items")
+        if self.copy_events is not None:
+            self.copy_events[-1] += (_event(st),)
         self.kernels_launched += 1
         self._keep.append(dev)
 

@@ -22,6 +22,9 @@ int fail(int code, const std::string& msg) {
 // launchers (defined in the kernel translation units)
 void set_pdl(bool on);
 int linear_splits(int64_t n, int64_t k, int64_t b);
+int linear_push(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
+                int64_t ldx, const DstList& dst, int64_t split_stride, int splits, const SignalSpec& sig,
+                cudaStream_t stream);
 int linear_silu(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
                 int64_t ldx, void* act, int64_t ld_act, cudaStream_t stream);
 int linear(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
@@ -46,6 +49,7 @@ int copy_items(const void*, int, int, int, cudaStream_t);
 int configure_gemm();
 int configure_attention();
 int configure_copy();
+int configure_decode_ops();
 int barrier(uint64_t* const*, int, uint64_t*, uint64_t, cudaStream_t);
 int ipc_get_handle(const void*, void*, int64_t*);
 int ipc_open(const void*, void**);
@@ -104,6 +108,7 @@ int tps_init(int device, int* sm_count) {
   int rc = configure_gemm();
   if (!rc) rc = configure_attention();
   if (!rc) rc = configure_copy();
+  if (!rc) rc = configure_decode_ops();
   return rc;
 }
 
@@ -114,6 +119,19 @@ int tps_linear_splits(int64_t n, int64_t k, int64_t b) { return linear_splits(n,
 int tps_linear(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
                int64_t ldx, float* out, int splits, void* stream) {
   return linear(w, n, k, ldw, x, b, x_rows, ldx, out, splits, S(stream));
+}
+
+int tps_linear_push(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
+                    int64_t ldx, float* const* dsts, int ndst, int64_t split_stride, int splits,
+                    uint64_t* const* sig_ctrs, int nsig, unsigned int* done, void* stream) {
+  TPS_CHECK_ARG(ndst >= 1 && ndst <= kMaxPeers && dsts, "linear_push: 1..8 destinations");
+  DstList dl;
+  dl.n = ndst;
+  for (int i = 0; i < ndst; ++i) dl.p[i] = dsts[i];
+  SignalSpec sg;
+  int rc = make_sig(sig_ctrs, nsig, done, &sg);
+  if (rc) return rc;
+  return linear_push(w, n, k, ldw, x, b, x_rows, ldx, dl, split_stride, splits, sg, S(stream));
 }
 
 int tps_linear_silu(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,

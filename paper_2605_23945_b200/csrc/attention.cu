@@ -51,8 +51,8 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_kernel(
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, c = lane & 3;
 
+  pdl_launch_dependents();  // dependents may launch now: they read our outputs only after their own wait
   pdl_wait();
-  pdl_launch_dependents();
 
   const int slot = row_slot[b];
   const int ctx = slot >= 0 ? (row_pos ? row_pos[b] : pos_by_slot[slot]) + 1 : 0;
@@ -297,8 +297,8 @@ __global__ void __launch_bounds__(D) attn_combine_kernel(const int* __restrict__
                                                          __nv_bfloat16* __restrict__ out) {
   __shared__ float fac[kMaxAttnSplits];
   __shared__ float s_inv;
+  pdl_launch_dependents();  // dependents may launch now: they read our outputs only after their own wait
   pdl_wait();
-  pdl_launch_dependents();
   const int b = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
   const int slot = row_slot[b];
   const int ctx = slot >= 0 ? (row_pos ? row_pos[b] : pos_by_slot[slot]) + 1 : 0;
@@ -355,6 +355,10 @@ int configure_attention() {
                                     attn_smem<128>()));
   TPS_CUDA_TRY(cudaFuncSetAttribute(paged_attn_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     attn_smem<64>()));
+  TPS_MAX_CARVEOUT(paged_attn_kernel<128>);
+  TPS_MAX_CARVEOUT(paged_attn_kernel<64>);
+  TPS_MAX_CARVEOUT(attn_combine_kernel<128>);
+  TPS_MAX_CARVEOUT(attn_combine_kernel<64>);
   return kOk;
 }
 

@@ -62,6 +62,7 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_balanced_kernel(
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, c4 = lane & 3;
   const bool decode = row_pos == nullptr;
+  pdl_launch_dependents();  // the O projection may launch and prefetch its weights now
   if (!decode) pdl_wait();  // prefill: earlier rows of this chunk were appended by the previous kernel
 
   // ---- unit prefix over rows: row b owns nkv * ceil(ctx_b / 64) units ----
@@ -161,7 +162,6 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_balanced_kernel(
     cp_async_commit();
   }
   if (decode) pdl_wait();
-  pdl_launch_dependents();
 
   // padding rows (slot < 0) have no units: CTA 0 zeroes their output
   if (cta == 0) {
@@ -381,6 +381,8 @@ int configure_attention_balanced() {
                                     bal_smem<128>()));
   TPS_CUDA_TRY(cudaFuncSetAttribute(paged_attn_balanced_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     bal_smem<64>()));
+  TPS_MAX_CARVEOUT(paged_attn_balanced_kernel<128>);
+  TPS_MAX_CARVEOUT(paged_attn_balanced_kernel<64>);
   int occ = 0;
   TPS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, paged_attn_balanced_kernel<64>, kAttnThreads,
                                                              bal_smem<64>()));

@@ -42,6 +42,17 @@ int fail(int code, const std::string& msg);
       return ::tps::fail(::tps::kCuda, std::string(#expr ": ") + cudaGetErrorString(_e)); \
   } while (0)
 
+// Every decode-step kernel asks for the maximum shared-memory carveout, so consecutive
+// kernels of a step never force an SM to drain and re-split L1/shared memory between
+// launches (which would also serialise programmatic-dependent launches).
+bool carveout_enabled();
+#define TPS_MAX_CARVEOUT(kernel)                                                                   \
+  do {                                                                                             \
+    if (carveout_enabled())                                                                        \
+      TPS_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,   \
+                                        (int)cudaSharedmemCarveoutMaxShared));                     \
+  } while (0)
+
 #define TPS_LAUNCH_CHECK()                                                          \
   do {                                                                              \
     cudaError_t _e = cudaGetLastError();                                            \

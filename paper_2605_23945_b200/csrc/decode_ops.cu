@@ -13,12 +13,19 @@
 // (position, page table, token history) stays where it is when the batch is
 // compacted after completions, so a CUDA-graph replay only needs a new
 // row_slot vector. row_slot[b] < 0 marks a padding row of a graph bucket.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "decode_ops.cuh"
 
 namespace tps {
 
 static bool g_pdl = true;
+static bool g_carveout = [] {
+  const char* e = getenv("TPS_CARVEOUT");
+  return !(e && e[0] == '0');
+}();
+bool carveout_enabled() { return g_carveout; }
 bool pdl_enabled() { return g_pdl; }
 void set_pdl(bool on) { g_pdl = on; }
 
@@ -31,33 +38,22 @@ __device__ __forceinline__ void do_wait(const WaitSpec& w) {
   __syncthreads();
 }
 
-__device__ __forceinline__ void do_signal(const SignalSpec& s) {
-  if (s.n == 0) return;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();  // this CTA's (possibly remote) stores are visible system-wide
-    const unsigned int nblocks = gridDim.x * gridDim.y * gridDim.z;
-    const unsigned int prev = atomicAdd(s.done, 1u);
-    if (prev == nblocks - 1) {
-      *s.done = 0u;  // re-arm for the next launch / graph replay
-      __threadfence_system();
-      for (int i = 0; i < s.n; ++i) red_release_sys_add(s.ctr[i], 1ull);
-    }
-  }
-}
+__device__ __forceinline__ void do_signal(const SignalSpec& s) { signal_last_cta(s); }
 
-// sum_{i<n} base[i*stride + off] in index order, loads batched 8 at a time
+// sum_{i<n} base[i*stride + off] in index order, loads batched NB at a time (one L2
+// round trip for up to NB split / rank partials)
+template <int NB = 8>
 __device__ __forceinline__ float4 src_sum4(const Src& s, long long off4) {
   const float4* b = reinterpret_cast<const float4*>(s.base) + off4;
   const long long st4 = s.stride / 4;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int i0 = 0; i0 < s.n; i0 += 8) {
-    float4 v[8];
+  for (int i0 = 0; i0 < s.n; i0 += NB) {
+    float4 v[NB];
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
+    for (int j = 0; j < NB; ++j)
       if (i0 + j < s.n) v[j] = b[(long long)(i0 + j) * st4];
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
+    for (int j = 0; j < NB; ++j)
       if (i0 + j < s.n) {
         acc.x += v[j].x; acc.y += v[j].y; acc.z += v[j].z; acc.w += v[j].w;
       }
@@ -100,8 +96,8 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 __global__ void embed_kernel(const int* __restrict__ row_slot, const int* __restrict__ pos_by_slot,
                              const int* __restrict__ row_pos, const int* __restrict__ history, int hist_ld,
                              const __nv_bfloat16* __restrict__ table, int H, float* __restrict__ resid) {
+  pdl_launch_dependents();  // dependents may launch now: they read our outputs only after their own wait
   pdl_wait();
-  pdl_launch_dependents();
   const int b = blockIdx.x;
   const int slot = row_slot[b];
   int tok = 0;
@@ -115,14 +111,15 @@ __global__ void embed_kernel(const int* __restrict__ row_slot, const int* __rest
 // resid[b] += sum_i src_i[b] (index order); out[b] = bf16(resid * rstd * w)
 constexpr int kNormThreads = 512;
 constexpr int kNormVec = 4;  // float4 per thread held in registers (H <= 8192)
+template <int NB>
 __global__ void __launch_bounds__(kNormThreads) add_norm_kernel(float* __restrict__ resid, Src src,
                                                                 WaitSpec wait,
                                                                 const __nv_bfloat16* __restrict__ w, float eps,
                                                                 int H, __nv_bfloat16* __restrict__ out, int ldo) {
   __shared__ float red[32];
   const int b = blockIdx.x;
+  pdl_launch_dependents();  // dependents may launch now: they read our outputs only after their own wait
   pdl_wait();
-  pdl_launch_dependents();
   do_wait(wait);
   float4* r4 = reinterpret_cast<float4*>(resid + (size_t)b * H);
   const int H4 = H / 4;
@@ -134,7 +131,7 @@ __global__ void __launch_bounds__(kNormThreads) add_norm_kernel(float* __restric
     if (i < H4) {
       float4 x = r4[i];
       if (src.n > 0) {
-        const float4 p = src_sum4(src, (long long)b * H4 + i);
+        const float4 p = src_sum4<NB>(src, (long long)b * H4 + i);
         x.x += p.x; x.y += p.y; x.z += p.z; x.w += p.w;
         r4[i] = x;
       }
@@ -163,8 +160,8 @@ __global__ void __launch_bounds__(kNormThreads) add_norm_kernel(float* __restric
 // rank's slot of every TP peer's receive area (NVLink P2P stores), then signal.
 constexpr int kPushBlocks = 64;
 __global__ void __launch_bounds__(256) reduce_push_kernel(Src src, DstList dst, long long n4, SignalSpec sig) {
+  pdl_launch_dependents();  // dependents may launch now: they read our outputs only after their own wait
   pdl_wait();
-  pdl_launch_dependents();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
        i += (long long)gridDim.x * blockDim.x) {
     const float4 v = src_sum4(src, i);
@@ -184,8 +181,8 @@ __global__ void __launch_bounds__(128) qkv_rope_append_kernel(
     int max_pages,
     const float* __restrict__ cos_t, const float* __restrict__ sin_t, int B, int nq, int nkv, int D, int P,
     __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ k_cache, __nv_bfloat16* __restrict__ v_cache) {
+  pdl_launch_dependents();  // dependents may launch now: they read our outputs only after their own wait
   pdl_wait();
-  pdl_launch_dependents();
   const int heads = nq + nkv;
   const int task = blockIdx.x * 4 + (threadIdx.x >> 5);
   if (task >= B * heads) return;
@@ -229,8 +226,8 @@ __global__ void __launch_bounds__(128) qkv_rope_append_kernel(
 // ------------------------------------------------------------- SiLU * up ---
 // partial layout [split][B][2F] = [gate rows | up rows]; out[b][f] = bf16(silu(g) * u)
 __global__ void silu_mul_kernel(Src src, int B, int F, __nv_bfloat16* __restrict__ out, int ldo) {
+  pdl_launch_dependents();  // dependents may launch now: they read our outputs only after their own wait
   pdl_wait();
-  pdl_launch_dependents();
   const int F4 = F / 4;
   const long long total = (long long)B * F4;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
@@ -262,8 +259,8 @@ __global__ void __launch_bounds__(kArgmaxThreads) argmax_stage1_kernel(Src src, 
                                                                       SignalSpec sig) {
   __shared__ float sv[kArgmaxThreads / 32];
   __shared__ int si[kArgmaxThreads / 32];
+  pdl_launch_dependents();  // dependents may launch now: they read our outputs only after their own wait
   pdl_wait();
-  pdl_launch_dependents();
   const int b = blockIdx.x, c = blockIdx.y;
   const int per = ((V + nchunk - 1) / nchunk + 3) & ~3;
   const int lo = c * per, hi = min(V, lo + per);
@@ -306,8 +303,8 @@ __global__ void argmax_finalize_kernel(CandList cands, int nchunk, WaitSpec wait
                                        int* __restrict__ pos_by_slot, const int* __restrict__ prompt_len,
                                        int* __restrict__ history, int hist_ld, int* __restrict__ out_tok) {
   const int b = blockIdx.x;
+  pdl_launch_dependents();  // dependents may launch now: they read our outputs only after their own wait
   pdl_wait();
-  pdl_launch_dependents();
   do_wait(wait);
   float best = -INFINITY;
   int bidx = 0x7fffffff;
@@ -334,8 +331,8 @@ __global__ void argmax_finalize_kernel(CandList cands, int nchunk, WaitSpec wait
 }
 
 __global__ void epoch_advance_kernel(uint64_t* epoch) {
+  pdl_launch_dependents();  // dependents may launch now: they read our outputs only after their own wait
   pdl_wait();
-  pdl_launch_dependents();
   *epoch += 1ull;
 }
 
@@ -366,7 +363,11 @@ int add_norm(float* resid, const Src& src, const WaitSpec& wait, const void* w, 
   TPS_CHECK_ARG(H % 4 == 0 && ldo % 2 == 0 && B > 0, "add_norm: H must be a multiple of 4");
   TPS_CHECK_ARG(H / 4 <= kNormThreads * kNormVec, "add_norm: H > 8192");
   TPS_CHECK_ARG(src.n == 0 || src.stride % 4 == 0, "add_norm: source stride must be a multiple of 4");
-  return launch_k(add_norm_kernel, dim3(B), dim3(kNormThreads), 0, st, true, resid, src, wait,
+  // a fused TP allreduce hands over tp x splits (<= 16) partials: one 16-wide load batch
+  if (src.n > 8)
+    return launch_k(add_norm_kernel<16>, dim3(B), dim3(kNormThreads), 0, st, true, resid, src, wait,
+                    reinterpret_cast<const __nv_bfloat16*>(w), eps, H, reinterpret_cast<__nv_bfloat16*>(out), ldo);
+  return launch_k(add_norm_kernel<8>, dim3(B), dim3(kNormThreads), 0, st, true, resid, src, wait,
                   reinterpret_cast<const __nv_bfloat16*>(w), eps, H, reinterpret_cast<__nv_bfloat16*>(out), ldo);
 }
 
@@ -418,6 +419,20 @@ int epoch_advance(uint64_t* epoch, cudaStream_t st) {
 
 int sum_src(const Src& src, long long n, float* out, cudaStream_t st) {
   return launch_k(sum_src_kernel, dim3(grid_for(n, 256, 4 * kNumSMs)), dim3(256), 0, st, false, src, n, out);
+}
+
+int configure_decode_ops() {
+  TPS_MAX_CARVEOUT(embed_kernel);
+  TPS_MAX_CARVEOUT(add_norm_kernel<8>);
+  TPS_MAX_CARVEOUT(add_norm_kernel<16>);
+  TPS_MAX_CARVEOUT(reduce_push_kernel);
+  TPS_MAX_CARVEOUT(qkv_rope_append_kernel);
+  TPS_MAX_CARVEOUT(silu_mul_kernel);
+  TPS_MAX_CARVEOUT(argmax_stage1_kernel);
+  TPS_MAX_CARVEOUT(argmax_finalize_kernel);
+  TPS_MAX_CARVEOUT(epoch_advance_kernel);
+  TPS_MAX_CARVEOUT(sum_src_kernel);
+  return kOk;
 }
 
 }  // namespace tps

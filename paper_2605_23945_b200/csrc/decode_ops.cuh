@@ -55,6 +55,23 @@ struct CandList {
   int n;
 };
 
+// The last CTA of the launch to get here (all threads of every CTA must call it)
+// makes the launch's stores visible system-wide and adds 1 to every listed counter.
+__device__ __forceinline__ void signal_last_cta(const SignalSpec& s) {
+  if (s.n == 0) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();  // this CTA's (possibly remote) stores are visible system-wide
+    const unsigned int nblocks = gridDim.x * gridDim.y * gridDim.z;
+    const unsigned int prev = atomicAdd(s.done, 1u);
+    if (prev == nblocks - 1) {
+      *s.done = 0u;  // re-arm for the next launch / graph replay
+      __threadfence_system();
+      for (int i = 0; i < s.n; ++i) red_release_sys_add(s.ctr[i], 1ull);
+    }
+  }
+}
+
 // ----------------------------------------------- programmatic dependent launch
 // Decode-step kernels are launched with the PDL attribute: each calls
 // pdl_launch_dependents() early (the next kernel may start its prologue) and

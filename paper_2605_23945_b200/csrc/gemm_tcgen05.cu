@@ -92,9 +92,9 @@ constexpr int kEpiSiluMul = 1;
 template <int BN, int EPI>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_swapab_kernel(const __grid_constant__ CUtensorMap tmap_w,
-                       const __grid_constant__ CUtensorMap tmap_x, float* __restrict__ out, int N,
-                       int B, int num_tiles, int splits, int chunks, int acts,
-                       __nv_bfloat16* __restrict__ act_out, int ld_act) {
+                       const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ DstList dst,
+                       long long split_stride, int N, int B, int num_tiles, int splits, int chunks, int acts,
+                       __nv_bfloat16* __restrict__ act_out, int ld_act, const __grid_constant__ SignalSpec sig) {
   using Cfg = GemmCfg<BN>;
   constexpr int S = Cfg::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -246,14 +246,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int b0 = act * BN;
       const int rows = min(BN, B - b0);
       if constexpr (EPI == kEpiPartial) {
-        float* dst = out + ((size_t)split * (size_t)B + (size_t)b0) * (size_t)N + (size_t)n;
+        // fp32 partial of (split, rows b0.., column n) into every destination: the local
+        // split-K workspace, or -- the fused TP allreduce -- this rank's slots in each
+        // peer's receive area (NVLink P2P stores), split-major with split_stride. The
+        // consumer sums the partials in a fixed order (deterministic, no atomics).
+        const size_t off = (size_t)split * (size_t)split_stride + (size_t)b0 * (size_t)N + (size_t)n;
         for (int j0 = 0; j0 < rows; j0 += 16) {
           uint32_t r[16];
           tmem_ld16(tmem_base + (uint32_t)(acc * BN + j0) + ((uint32_t)(q * 32) << 16), r);
           if (n < N) {
+            for (int d = 0; d < dst.n; ++d) {
+              float* o = dst.p[d] + off;
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (j0 + j < rows) dst[(size_t)(j0 + j) * N] = __uint_as_float(r[j]);
+              for (int j = 0; j < 16; ++j)
+                if (j0 + j < rows) o[(size_t)(j0 + j) * N] = __uint_as_float(r[j]);
+            }
           }
         }
       } else {
@@ -297,6 +304,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                  "n"(Cfg::kTmemCols));
   }
+  // fused allreduce: the last CTA to finish releases one arrival on every peer's counter
+  signal_last_cta(sig);
 }
 
 // ------------------------------------------------------------------ host ---
@@ -357,7 +366,8 @@ static int pick_bn(int64_t b) {
 }
 
 // Split-K choice: minimise (waves x chunks-per-unit) for a 148-SM persistent grid,
-// plus a small charge for the fp32 partial traffic the consumer has to reduce.
+// plus a small charge for the fp32 partial traffic the consumer has to reduce and
+// one L2 round trip (~35 KB of one SM's weight stream) per 8 partials it sums.
 int linear_splits(int64_t n, int64_t k, int64_t b) {
   const int bn = pick_bn(b);
   const int64_t tiles = ((n + kBM - 1) / kBM) * ((b + bn - 1) / bn);
@@ -371,7 +381,8 @@ int linear_splits(int64_t n, int64_t k, int64_t b) {
     const int64_t cpu = (chunks + s - 1) / s;
     const double weight_cost = (double)waves * (double)cpu * (kBM * kBK * 2);
     const double partial_cost = 0.25 * (double)s * (double)b * (double)n * 8.0 / kNumSMs;
-    const double cost = weight_cost + partial_cost;
+    const double consumer_cost = (double)((s + 7) / 8) * 35.0 * 1024.0;
+    const double cost = weight_cost + partial_cost + consumer_cost;
     if (cost < best_cost * 0.999) {
       best_cost = cost;
       best = s;
@@ -380,15 +391,23 @@ int linear_splits(int64_t n, int64_t k, int64_t b) {
   return best;
 }
 
+struct EpiArgs {
+  DstList dst;
+  long long split_stride;
+  __nv_bfloat16* act_out;
+  int ld_act;
+  SignalSpec sig;
+};
+
 template <int BN, int EPI>
-static int launch_gemm(const CUtensorMap& mw, const CUtensorMap& mx, float* out, int n, int b, int tiles,
-                       int splits, int chunks, __nv_bfloat16* act_out, int ld_act, cudaStream_t stream) {
+static int launch_gemm(const CUtensorMap& mw, const CUtensorMap& mx, const EpiArgs& e, int n, int b, int tiles,
+                       int splits, int chunks, cudaStream_t stream) {
   using Cfg = GemmCfg<BN>;
   const int acts = (b + BN - 1) / BN;
   const int units = tiles * splits * acts;
   const int grid = units < kNumSMs ? units : kNumSMs;
   return launch_k(gemm_swapab_kernel<BN, EPI>, dim3(grid), dim3(kGemmThreads), Cfg::kSmemBytes, stream, true, mw,
-                  mx, out, n, b, tiles, splits, chunks, acts, act_out, ld_act);
+                  mx, e.dst, e.split_stride, n, b, tiles, splits, chunks, acts, e.act_out, e.ld_act, e.sig);
 }
 
 template <int BN>
@@ -397,6 +416,8 @@ static int configure_one() {
                                     GemmCfg<BN>::kSmemBytes));
   TPS_CUDA_TRY(cudaFuncSetAttribute(gemm_swapab_kernel<BN, kEpiSiluMul>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     GemmCfg<BN>::kSmemBytes));
+  TPS_MAX_CARVEOUT((gemm_swapab_kernel<BN, kEpiPartial>));
+  TPS_MAX_CARVEOUT((gemm_swapab_kernel<BN, kEpiSiluMul>));
   return kOk;
 }
 
@@ -411,14 +432,14 @@ int configure_gemm() {
 }
 
 template <int EPI>
-static int dispatch(int bn, const CUtensorMap& mw, const CUtensorMap& mx, float* out, int n, int b, int tiles,
-                    int splits, int chunks, __nv_bfloat16* act_out, int ld_act, cudaStream_t st) {
+static int dispatch(int bn, const CUtensorMap& mw, const CUtensorMap& mx, const EpiArgs& e, int n, int b, int tiles,
+                    int splits, int chunks, cudaStream_t st) {
   switch (bn) {
-    case 16: return launch_gemm<16, EPI>(mw, mx, out, n, b, tiles, splits, chunks, act_out, ld_act, st);
-    case 32: return launch_gemm<32, EPI>(mw, mx, out, n, b, tiles, splits, chunks, act_out, ld_act, st);
-    case 64: return launch_gemm<64, EPI>(mw, mx, out, n, b, tiles, splits, chunks, act_out, ld_act, st);
-    case 128: return launch_gemm<128, EPI>(mw, mx, out, n, b, tiles, splits, chunks, act_out, ld_act, st);
-    default: return launch_gemm<256, EPI>(mw, mx, out, n, b, tiles, splits, chunks, act_out, ld_act, st);
+    case 16: return launch_gemm<16, EPI>(mw, mx, e, n, b, tiles, splits, chunks, st);
+    case 32: return launch_gemm<32, EPI>(mw, mx, e, n, b, tiles, splits, chunks, st);
+    case 64: return launch_gemm<64, EPI>(mw, mx, e, n, b, tiles, splits, chunks, st);
+    case 128: return launch_gemm<128, EPI>(mw, mx, e, n, b, tiles, splits, chunks, st);
+    default: return launch_gemm<256, EPI>(mw, mx, e, n, b, tiles, splits, chunks, st);
   }
 }
 
@@ -433,17 +454,39 @@ static int prepare(const void* w, int64_t n, int64_t k, int64_t ldw, const void*
   return make_tmap_bf16(mx, x, x_rows, k, ldx, *bn);
 }
 
+int linear_push(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
+                int64_t ldx, const DstList& dst, int64_t split_stride, int splits, const SignalSpec& sig,
+                cudaStream_t stream);
+
+// out: fp32 split-K partials [splits][b][n] (the consumer sums them in split order).
 int linear(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,
            int64_t x_rows, int64_t ldx, float* out, int splits, cudaStream_t stream) {
   TPS_CHECK_ARG(out, "linear: null output");
+  DstList dl;
+  dl.n = 1;
+  dl.p[0] = out;
+  SignalSpec none;
+  none.n = 0;
+  none.done = nullptr;
+  return linear_push(w, n, k, ldw, x, b, x_rows, ldx, dl, b * n, splits, none, stream);
+}
+
+// Partial of split s, row i, column j -> dst.p[d][s * split_stride + i * n + j] for every d,
+// then (last CTA of the launch) +1 on every signal counter.
+int linear_push(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
+                int64_t ldx, const DstList& dst, int64_t split_stride, int splits, const SignalSpec& sig,
+                cudaStream_t stream) {
   const int64_t chunks = (k + kBK - 1) / kBK;
   TPS_CHECK_ARG(splits >= 1 && splits <= chunks, "linear: splits must be in [1, ceil(k/64)]");
+  TPS_CHECK_ARG(dst.n >= 1 && dst.n <= kMaxPeers, "linear: 1..8 destinations");
+  TPS_CHECK_ARG(split_stride >= b * n, "linear: split_stride must hold [b][n]");
   CUtensorMap mw, mx;
   int bn;
   int rc = prepare(w, n, k, ldw, x, b, x_rows, ldx, &mw, &mx, &bn);
   if (rc) return rc;
-  return dispatch<kEpiPartial>(bn, mw, mx, out, (int)n, (int)b, (int)((n + kBM - 1) / kBM), splits, (int)chunks,
-                               nullptr, 0, stream);
+  EpiArgs e{dst, (long long)split_stride, nullptr, 0, sig};
+  return dispatch<kEpiPartial>(bn, mw, mx, e, (int)n, (int)b, (int)((n + kBM - 1) / kBM), splits, (int)chunks,
+                               stream);
 }
 
 int linear_silu(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
@@ -455,8 +498,12 @@ int linear_silu(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x,
   int bn;
   int rc = prepare(w, n, k, ldw, x, b, x_rows, ldx, &mw, &mx, &bn);
   if (rc) return rc;
-  return dispatch<kEpiSiluMul>(bn, mw, mx, nullptr, (int)n, (int)b, (int)(n / kBM), 1, (int)chunks,
-                               reinterpret_cast<__nv_bfloat16*>(act), (int)ld_act, stream);
+  EpiArgs e{};
+  e.dst.n = 0;
+  e.act_out = reinterpret_cast<__nv_bfloat16*>(act);
+  e.ld_act = (int)ld_act;
+  e.sig.n = 0;
+  return dispatch<kEpiSiluMul>(bn, mw, mx, e, (int)n, (int)b, (int)(n / kBM), 1, (int)chunks, stream);
 }
 
 }  // namespace tps

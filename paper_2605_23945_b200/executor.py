@@ -28,7 +28,7 @@ import torch
 
 from . import _native as nat
 from .kvcache import PAGE, KVPool, SlotTable
-from .models import DecoderGeometry, RankShard, rope_tables
+from .models import DecoderGeometry, RankShard, rank_shard, rope_tables
 from .shards import RankWeights
 
 BUCKETS = (1, 2, 4, 8, 16, 24, 32, 48, 64, 96, 128, 192, 256)
@@ -45,10 +45,16 @@ def argmax_chunks(B: int) -> int:
     return max(1, min(64, 296 // max(1, B)))
 
 
+FUSE_ROWS = 64     # row-parallel projections push their split partials straight to peers up to this batch
+FUSE_SOURCES = 16  # at most tp x splits partial slots per fused allreduce (one consumer load batch)
+
+
 class GroupComm:
     """Communication state of one TP group as held by one rank.
 
-    recv[parity][src_rank] : fp32 [max_batch][H] receive slots (one-shot allreduce)
+    recv[parity][src_rank] : fp32 [max_batch][H] receive slots (one-shot allreduce push)
+    frecv[parity][src_rank * splits + split] : fp32 [FUSE_ROWS][H] slots the peers' fused
+                             projection epilogues store their split partials into
     cand                   : per-(row, chunk) argmax candidates (8 B each)
     ctr[phase]             : arrival counters, +1 per peer per phase per step
     done[phase]            : last-CTA detectors of this rank's signalling launches
@@ -63,27 +69,37 @@ class GroupComm:
         self.hidden = hidden
         self.n_phases = n_phases
         self.recv = torch.zeros((2, tp, max_batch, hidden), dtype=torch.float32, device=device)
+        self.frecv = torch.zeros((2, FUSE_SOURCES, FUSE_ROWS, hidden), dtype=torch.float32, device=device)
         self.cand = torch.zeros((max_batch, 64, 2), dtype=torch.int32, device=device)
         self.ctr = torch.zeros(n_phases, dtype=torch.int64, device=device)
         self.done = torch.zeros(n_phases, dtype=torch.int32, device=device)
         self.epoch = torch.ones(1, dtype=torch.int64, device=device)
         # peer pointer table, rank order (filled by connect / the Cache Manager)
         self.peer_recv: list[int] = []
+        self.peer_frecv: list[int] = []
         self.peer_ctr: list[int] = []
         self.peer_cand: list[int] = []
 
     # local export for peers
     def export(self) -> dict:
-        return {"recv": self.recv.data_ptr(), "ctr": self.ctr.data_ptr(), "cand": self.cand.data_ptr()}
+        return {"recv": self.recv.data_ptr(), "frecv": self.frecv.data_ptr(), "ctr": self.ctr.data_ptr(),
+                "cand": self.cand.data_ptr()}
 
     def connect(self, tables: list[dict]) -> None:
         assert len(tables) == self.tp
         self.peer_recv = [t["recv"] for t in tables]
+        self.peer_frecv = [t["frecv"] for t in tables]
         self.peer_ctr = [t["ctr"] for t in tables]
         self.peer_cand = [t["cand"] for t in tables]
 
     def recv_slot(self, base: int, parity: int, src_rank: int) -> int:
         return base + ((parity * self.tp + src_rank) * self.max_batch * self.hidden) * 4
+
+    def frecv_slot(self, base: int, parity: int, src_rank: int, splits: int) -> int:
+        """First slot of src_rank in a fused receive area when every rank pushes `splits`
+        partials: slot index src_rank * splits + split, so the tp x splits used slots are
+        contiguous and are read back in (rank, split) order."""
+        return base + ((parity * FUSE_SOURCES + src_rank * splits) * FUSE_ROWS * self.hidden) * 4
 
     def reset(self) -> None:
         self.ctr.zero_()
@@ -270,8 +286,8 @@ class InferExecutor:
                                                   self.attn.data_ptr(), *fused, st),
                           "tps_paged_attention")
                 stats.add("paged_attention", 1 if nsplit <= 4 else 2)  # (+ split-merge kernel)
-            srcs = self._linear(st, stats, W[(l, "w_o")], self.attn, B)
-            yield from self._allreduce_norm(st, stats, 2 * l, srcs, B, W.tensor_ptr(l, "ln2"))
+            yield from self._row_parallel(st, stats, 2 * l, "w_o", W[(l, "w_o")], self.attn, B,
+                                          W.tensor_ptr(l, "ln2"))
             w_gu = W[(l, "w_gu")]
             if self._fuse_silu(B):
                 nat.check(lib.tps_linear_silu(w_gu.data_ptr(), 2 * self.F, H, H, self.xn.data_ptr(), B,
@@ -283,9 +299,8 @@ class InferExecutor:
                 nat.check(lib.tps_silu_mul(*srcs, B, self.F, self.act.data_ptr(), self.F, st),
                           "tps_silu_mul")
                 stats.add("silu_mul")
-            srcs = self._linear(st, stats, W[(l, "w_d")], self.act, B)
             nxt = W.tensor_ptr(l + 1, "ln1") if l + 1 < L else W.tensor_ptr(-1, "ln_f")
-            yield from self._allreduce_norm(st, stats, 2 * l + 1, srcs, B, nxt)
+            yield from self._row_parallel(st, stats, 2 * l + 1, "w_d", W[(l, "w_d")], self.act, B, nxt)
         cm = self.comm
         if prefill:
             if cm is not None:
@@ -326,6 +341,51 @@ class InferExecutor:
         if cm is not None:
             nat.check(lib.tps_epoch_advance(cm.epoch.data_ptr(), st), "tps_epoch_advance")
             stats.add("epoch_advance")
+
+    def fused_splits(self, fam: str, B: int) -> int:
+        """Split-K count of a fused row-parallel projection: the same on every rank of the
+        group (the slots are read as tp x splits partials in one fixed order) and at most
+        FUSE_SOURCES / tp, so the consumer sums every partial in one load batch."""
+        g = self.geom
+        if fam == "w_o":
+            ks = [rank_shard(g, self.tp, r).n_q * g.head_dim for r in range(self.tp)]
+        else:
+            ks = [self.F] * self.tp
+        s = nat.lib().tps_linear_splits(g.hidden, max(ks), B)
+        return max(1, min(FUSE_SOURCES // self.tp, s, min(-(-k // 64) for k in ks)))
+
+    def _row_parallel(self, st, stats, phase: int, fam: str, w: torch.Tensor, x: torch.Tensor, B: int,
+                      norm_w: int):
+        """O / down projection + TP allreduce + residual add + RMSNorm.
+
+        TP > 1 and B <= FUSE_ROWS: the projection epilogue stores its split-K partials
+        straight into every peer's fused receive area and the last CTA signals
+        (tps_linear_push: the allreduce is fused into the projection); add+norm waits
+        for the tp arrivals and sums the tp x splits slots in (rank, split) order.
+        Otherwise: split partials -> tps_reduce_push -> add+norm."""
+        cm = self.comm
+        if cm is None or B > FUSE_ROWS or "fuse_push" in self.skip or "linear" in self.skip:
+            srcs = self._linear(st, stats, w, x, B)
+            yield from self._allreduce_norm(st, stats, phase, srcs, B, norm_w)
+            return
+        lib = nat.lib()
+        g = self.geom
+        H = g.hidden
+        n, k = w.shape
+        S = self.fused_splits(fam, B)
+        par = phase % 2
+        dsts = [cm.frecv_slot(base, par, self.rank, S) for base in cm.peer_frecv]
+        sigs = [p + phase * 8 for p in cm.peer_ctr]
+        nat.check(lib.tps_linear_push(w.data_ptr(), n, k, k, x.data_ptr(), B, x.shape[0], x.shape[1],
+                                      self._arr(dsts), len(dsts), FUSE_ROWS * H, S, self._arr(sigs), len(sigs),
+                                      cm.done.data_ptr() + phase * 4, st), "tps_linear_push")
+        stats.add("linear")
+        yield
+        mine = (cm.frecv_slot(cm.frecv.data_ptr(), par, 0, S), cm.tp * S, FUSE_ROWS * H)
+        wait = nat.wait_spec(cm.ctr.data_ptr() + phase * 8, cm.epoch.data_ptr(), cm.tp, 0)
+        nat.check(lib.tps_add_norm(self.resid.data_ptr(), *mine, wait, norm_w, ctypes.c_float(g.rms_eps), H, B,
+                                   self.xn.data_ptr(), H, st), "tps_add_norm")
+        stats.add("add_norm")
 
     def _allreduce_norm(self, st, stats, phase: int, srcs: tuple[int, int, int], B: int, norm_w: int):
         lib = nat.lib()

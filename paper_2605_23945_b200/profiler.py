@@ -23,6 +23,7 @@ import torch
 
 from . import _native as nat
 from .executor import GroupRunner, InferExecutor
+from .group import admit
 from .latency import PROFILE_DECODE_STEPS, ProfilePoint, profile_batches, profile_lengths, table_from_points
 
 
@@ -64,7 +65,7 @@ def gemm_probe(ex: InferExecutor, B: int, reps: int = 2) -> dict:
         torch.cuda.synchronize()
         nl = reps * len(keys)
         ms = e0.elapsed_time(e1) / nl
-        byt = n * k * 2 + B * k * 2 + s * B * n * 4
+        byt = n * k * 2 + B * k * 2 + s * B * n * 4  # weights + activations + fp32 split partials
         out[fam] = {"ms": ms, "bytes": byt, "n": len(keys) if fam != "lm_head" else 1, "splits": s}
         per_step = g.num_layers if fam != "lm_head" else 1
         tot_ms += ms * per_step
@@ -134,3 +135,71 @@ class OfflineProfiler:
 
 def c_float(x: float):
     return ctypes.c_float(x)
+
+
+def switch_probe(spec, geom, world, tp_to: int, n_samples: int, ctx: int, copy_mode: int = 0,
+                 reps: int = 1) -> dict:
+    """Switch Executor microbench (BASELINE config 5): one real switch of a running decode.
+
+    Builds the layout (spec.initial_tp, world), places `n_samples` live samples at
+    context `ctx` (prompt = spec.prompt_len, the rest generated; KV contents are
+    whatever the pages hold -- the copy is byte-exact regardless), places them
+    with assign_merged_groups exactly as a committed switch does and executes the
+    weight reshard + KV-page + history pulls to TP=tp_to. Returns bytes moved and
+    the device time between the first and last copy event of the switch (the two
+    device barriers excluded), per stream-ordered phase.
+    """
+    from .controller import assign_merged_groups
+    from .coordinator import B200Backend
+    from .workload import BatchStatus, Sample
+
+    out = []
+    for _ in range(reps):
+        be = B200Backend(spec, geom, world, seed=0)
+        lay = be.layout
+        samples = {g: [] for g in range(lay.dp)}
+        prompt = torch.zeros(spec.prompt_len, dtype=torch.int32)
+        for i in range(n_samples):
+            g = i % lay.dp
+            grp = be.group_ranks(g)
+            if not grp:
+                continue
+            slot = admit(grp, i, prompt, max_ctx=be.max_len)
+            be.slot_of[i] = slot
+            for r in grp:
+                r.slots.pos[slot] = ctx - 1
+            samples[g].append(Sample(id=i, prompt_len=spec.prompt_len, target_response_len=spec.l_max,
+                                     generated_len=ctx - spec.prompt_len, intra_dp_group=g))
+        statuses = [BatchStatus(0, g, tuple(v)) for g, v in samples.items()]
+        merged = assign_merged_groups(statuses, tp_to, spec.cluster)
+        for r in world.local_ranks:
+            torch.cuda.synchronize(world.devices[r])
+        be.copy_mode = copy_mode
+        be.copy_events = []
+        be.start = {r: _start_event(be, r) for r in world.local_ranks}
+        be._execute_switch(tp_to, merged)
+        t = be.switches[-1]
+        for r in world.local_ranks:
+            torch.cuda.synchronize(world.devices[r])
+        # copy-kernel device time (launches of one stream are serial; a virtual world
+        # runs every rank's pulls on the one device)
+        kms = sum(e0.elapsed_time(e1) for e0, _, e1 in be.copy_events)
+        kbytes = sum(nb for _, nb, _ in be.copy_events)
+        marks = t.marks
+        t0 = min(be.start[r].elapsed_time(m[0]) for r, m in marks.items())
+        t_end = max(be.start[r].elapsed_time(m[3]) for r, m in marks.items())
+        out.append({"weights_bytes": t.weight_bytes, "kv_bytes": t.kv_bytes, "nvlink_bytes": t.nvlink_bytes,
+                    "local_bytes": t.local_bytes, "copy_bytes": kbytes, "copy_kernel_ms": kms,
+                    "copy_gbps": kbytes / (kms / 1e3) / 1e9, "switch_device_ms": t_end - t0,
+                    "host_plan_s": t.host_plan_s, "host_capture_s": t.host_capture_s,
+                    "host_build_s": t.host_build_s, "copy_launches": len(be.copy_events)})
+        del be
+        torch.cuda.empty_cache()
+    best = min(out, key=lambda d: d["copy_kernel_ms"])
+    return best
+
+
+def _start_event(be, r):
+    e = torch.cuda.Event(enable_timing=True)
+    e.record(be.stream(r))
+    return e

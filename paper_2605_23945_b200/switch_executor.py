@@ -25,6 +25,7 @@ Plans become 32-byte copy items (tps_copy_item) executed by tps_copy_items;
 
 from __future__ import annotations
 
+import bisect
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -72,6 +73,9 @@ class Pieces:
         self.nbytes.append(np.asarray(nbytes, dtype=np.int64).ravel())
 
     def arrays(self):
+        if len(self.src_rank) > 1:  # concatenate once; later adds append to the merged arrays
+            self.src_rank, self.src_off, self.dst_off, self.nbytes = (
+                [np.concatenate(x)] for x in (self.src_rank, self.src_off, self.dst_off, self.nbytes))
         if not self.src_rank:
             z = np.zeros(0, dtype=np.int64)
             return z, z, z, z
@@ -96,11 +100,19 @@ def _pick_source(holders: list[int], dst_rank: int, salt: int) -> int:
 
 
 def plan_weight_pulls(geom: DecoderGeometry, old: Layout, new: Layout, dst_rank: int) -> Pieces:
-    """Pieces that fill `dst_rank`'s new arena from the old arenas (offsets are arena bytes)."""
+    """Pieces that fill `dst_rank`'s new arena from the old arenas (offsets are arena bytes).
+
+    A pure function of (geometry, layouts, rank): the Cache Manager may memoise it
+    (`cached_weight_pulls`). Each target run is intersected with the old tp-ranks'
+    runs of the same family by bisection over the (sorted, disjoint) source runs.
+    """
     new_sh = rank_shard(geom, new.tp, new.tp_rank(dst_rank))
     new_arena = arena_layout(geom, new_sh)
     old_sh = [rank_shard(geom, old.tp, r) for r in range(old.tp)]
     old_arena = [arena_layout(geom, s) for s in old_sh]
+    # an old tp-rank's runs are resident on dst_rank iff dst_rank is that tp-rank in some old group
+    local = [any(g * old.tp + otr == dst_rank for g in range(old.dp)) for otr in range(old.tp)]
+    src_runs: dict[str, list] = {}
     pieces = Pieces()
     salt = 0
     for (layer, fam), (dst_base, dst_shape) in new_arena.entries.items():
@@ -113,19 +125,26 @@ def plan_weight_pulls(geom: DecoderGeometry, old: Layout, new: Layout, dst_rank:
             salt += 1
             continue
         axis, dst_ranges = shard_ranges(geom, fam, new_sh)
+        if fam not in src_runs:  # per family: old tp-rank runs sorted by start (c, d, storage offset)
+            per = []
+            for otr in range(old.tp):
+                runs = sorted(_storage_runs(shard_ranges(geom, fam, old_sh[otr])[1]))
+                per.append((runs, [r[1] for r in runs]))
+            src_runs[fam] = per
         row_elems = full[1] if len(full) == 2 else 1
         for a, b, doff in _storage_runs(dst_ranges):
             # candidate sources: every old tp-rank run intersecting [a, b); replicated
             # KV heads appear on several tp-ranks, so sweep and take each byte once,
             # preferring a run that is resident on the target rank itself
             cands = []
-            for otr in range(old.tp):
-                _, src_ranges = shard_ranges(geom, fam, old_sh[otr])
-                for c, d, soff in _storage_runs(src_ranges):
+            for otr, (runs, ends) in enumerate(src_runs[fam]):
+                i = bisect.bisect_right(ends, a)
+                while i < len(runs) and runs[i][0] < b:
+                    c, d, soff = runs[i]
                     x, y = max(a, c), min(b, d)
                     if x < y:
-                        local = any(g * old.tp + otr == dst_rank for g in range(old.dp))
-                        cands.append((x, 0 if local else 1, y, otr, c, soff))
+                        cands.append((x, 0 if local[otr] else 1, y, otr, c, soff))
+                    i += 1
             cands.sort()
             pos = a
             for x, _, y, otr, c, soff in cands:
@@ -133,23 +152,36 @@ def plan_weight_pulls(geom: DecoderGeometry, old: Layout, new: Layout, dst_rank:
                 if x >= y:
                     continue
                 pos = y
-                if True:
-                    holders = [g * old.tp + otr for g in range(old.dp)]
-                    src = _pick_source(holders, dst_rank, salt)
-                    salt += 1
-                    sbase = old_arena[otr].entries[(layer, fam)][0]
-                    s_lo, d_lo, w = soff + (x - c), doff + (x - a), y - x
-                    if axis == 0 or len(full) == 1:
-                        pieces.add(src, sbase + 2 * s_lo * row_elems, dst_base + 2 * d_lo * row_elems,
-                                   2 * w * row_elems)
-                    else:  # column slice of a row-major [rows][cols] tensor: one piece per row
-                        rows = full[0]
-                        src_ld = old_arena[otr].entries[(layer, fam)][1][1]
-                        dst_ld = dst_shape[1]
-                        r = np.arange(rows, dtype=np.int64)
-                        pieces.add(np.full(rows, src), sbase + 2 * (r * src_ld + s_lo),
-                                   dst_base + 2 * (r * dst_ld + d_lo), np.full(rows, 2 * w))
+                holders = [g * old.tp + otr for g in range(old.dp)]
+                src = _pick_source(holders, dst_rank, salt)
+                salt += 1
+                sbase = old_arena[otr].entries[(layer, fam)][0]
+                s_lo, d_lo, w = soff + (x - c), doff + (x - a), y - x
+                if axis == 0 or len(full) == 1:
+                    pieces.add(src, sbase + 2 * s_lo * row_elems, dst_base + 2 * d_lo * row_elems,
+                               2 * w * row_elems)
+                else:  # column slice of a row-major [rows][cols] tensor: one piece per row
+                    rows = full[0]
+                    src_ld = old_arena[otr].entries[(layer, fam)][1][1]
+                    dst_ld = dst_shape[1]
+                    r = np.arange(rows, dtype=np.int64)
+                    pieces.add(np.full(rows, src), sbase + 2 * (r * src_ld + s_lo),
+                               dst_base + 2 * (r * dst_ld + d_lo), np.full(rows, 2 * w))
     return pieces
+
+
+_WEIGHT_PLANS: dict = {}
+
+
+def cached_weight_pulls(geom: DecoderGeometry, old: Layout, new: Layout, dst_rank: int) -> Pieces:
+    """Memoised plan_weight_pulls (plans depend only on geometry, layouts and rank)."""
+    key = (geom.name, geom.num_layers, geom.hidden, old, new, dst_rank)
+    if key not in _WEIGHT_PLANS:
+        wp = plan_weight_pulls(geom, old, new, dst_rank)
+        total = arena_layout(geom, rank_shard(geom, new.tp, new.tp_rank(dst_rank))).total_bytes
+        check(verify_cover(wp, total, allow_gaps=True), "weight pull plan")
+        _WEIGHT_PLANS[key] = wp
+    return _WEIGHT_PLANS[key]
 
 
 @dataclass(frozen=True)
@@ -225,8 +257,10 @@ def to_items(pieces: Pieces, src_base: dict[int, int], dst_base: int, max_chunk:
     sr, so, do, nb = pieces.arrays()
     if sr.size == 0:
         return np.zeros((0, 4), dtype=np.int64)
-    bases = np.array([src_base[int(r)] for r in sr], dtype=np.int64) if sr.size < 4096 else \
-        np.vectorize(lambda r: src_base[int(r)], otypes=[np.int64])(sr)
+    lut = np.zeros(int(sr.max()) + 1, dtype=np.int64)
+    for r in np.unique(sr):
+        lut[r] = src_base[int(r)]
+    bases = lut[sr]
     nsplit = (nb + max_chunk - 1) // max_chunk
     idx = np.repeat(np.arange(sr.size), nsplit)
     first = np.repeat(np.cumsum(nsplit) - nsplit, nsplit)

@@ -233,3 +233,34 @@ def test_linear_silu_fused_epilogue(F, k, b):
     ref = torch.nn.functional.silu(g) * u
     err = (act.float() - ref).abs() / (ref.abs() + 1.0)
     assert err.max().item() < 2e-2
+
+
+@pytest.mark.parametrize("n,k,b,ndst,splits", [(3584, 512, 1, 8, 2), (256, 128, 7, 2, 2), (3584, 2368, 64, 4, 4),
+                                                 (3584, 512, 16, 8, 1)])
+def test_linear_push_fused_allreduce_epilogue(n, k, b, ndst, splits):
+    """tps_linear_push: every split partial lands in every destination (the peers' receive
+    slots) at split * split_stride + row * n, rows >= b untouched, and the last CTA bumps
+    every counter exactly once per launch (repeated launches / graph replays re-arm)."""
+    torch.manual_seed(n + b)
+    w = (torch.randn(n, k, device="cuda") * 0.05).bfloat16()
+    x = torch.randn(b, k, device="cuda").bfloat16()
+    rows = 64
+    slots = [torch.full((splits, rows, n), float("nan"), device="cuda") for _ in range(ndst)]
+    ctrs = [torch.zeros(4, dtype=torch.int64, device="cuda") for _ in range(ndst)]
+    done = torch.zeros(4, dtype=torch.int32, device="cuda")
+    lib = nat.lib()
+    for rep in range(3):
+        nat.check(lib.tps_linear_push(w.data_ptr(), n, k, k, x.data_ptr(), b, b, k,
+                                      nat.ptr_array([t.data_ptr() for t in slots]), ndst, rows * n, splits,
+                                      nat.ptr_array([c.data_ptr() + 8 for c in ctrs]), ndst,
+                                      done.data_ptr() + 4, _stream()))
+    torch.cuda.synchronize()
+    ref = x.float() @ w.float().T
+    tol = 2e-3 * math.sqrt(k) * 0.05 * 4 + 1e-4
+    for t, c in zip(slots, ctrs):
+        got = t[:, :b].sum(0)
+        assert (got - ref).abs().max().item() <= tol
+        assert torch.equal(t[:, :b], slots[0][:, :b])
+        assert torch.isnan(t[:, b:]).all()
+        assert c.tolist() == [0, 3, 0, 0]
+    assert done.tolist() == [0, 0, 0, 0]

@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
+timeout 900 python bench.py --no-cpu --no-switch > gpurun_out/bench.log 2>&1; head -c 400 gpurun_out/bench.log; echo
+timeout 600 python tools/solo_step.py qwen2.5-7b 1,8 1,16,64 2048 ";fuse_push" 2>&1 | grep -v watchdog
