@@ -1,3 +1,4 @@
+#include <stdlib.h>
 // Paged GQA decode attention (flash-decoding split-KV with in-kernel merge), sm_100a.
 //
 // The reference prices this work as the KV term of oracle_decode_latency,
@@ -365,8 +366,14 @@ int configure_attention() {
 // Split policy: 0 = page-balanced schedule (when the (row, kv head) segments alone
 // give a few hundred units of parallel work), else the fixed split count that
 // keeps the grid within one wave of resident CTAs (2 per SM).
+// TPS_ATTN_MIN_BAL=<n>: use the page-balanced schedule from B * nkv >= n (default 64)
+static int g_min_bal = [] {
+  const char* e = getenv("TPS_ATTN_MIN_BAL");
+  return e ? atoi(e) : 64;
+}();
+
 int attn_splits(int B, int nkv, int max_pages) {
-  if (B * nkv >= 64 && B <= kBalMaxRows) return 0;
+  if (B * nkv >= g_min_bal && B <= kBalMaxRows) return 0;
   return attn_fixed_splits(B, nkv, max_pages);
 }
 

@@ -95,6 +95,12 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
 __device__ __forceinline__ void red_release_sys_add(uint64_t* p, uint64_t v) {
   asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// Relaxed system-scope add. Preceded in program order by a fence.sc.sys
+// (__threadfence_system) it forms a release pattern: signalling n peers costs one
+// system fence instead of n (each red.release.sys is a fence of its own).
+__device__ __forceinline__ void red_relaxed_sys_add(uint64_t* p, uint64_t v) {
+  asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 
 // Spin (one thread) until *p >= target; traps after the watchdog budget.
 __device__ __forceinline__ void wait_counter_geq(const uint64_t* p, uint64_t target) {

@@ -144,7 +144,7 @@ struct PeerPtrs {
 __global__ void barrier_kernel_v(PeerPtrs peers, int npeers, uint64_t* my_ctr, uint64_t target) {
   if (threadIdx.x != 0) return;
   __threadfence_system();
-  for (int i = 0; i < npeers; ++i) red_release_sys_add(peers.p[i], 1ull);
+  for (int i = 0; i < npeers; ++i) red_relaxed_sys_add(peers.p[i], 1ull);
   wait_counter_geq(my_ctr, target);
   __threadfence_system();
 }

@@ -61,13 +61,16 @@ __device__ __forceinline__ void signal_last_cta(const SignalSpec& s) {
   if (s.n == 0) return;
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence_system();  // this CTA's (possibly remote) stores are visible system-wide
+    // this CTA's (possibly remote) stores are ordered before its arrival at gpu scope; the
+    // last CTA's system fence below is cumulative over everything it has observed, so one
+    // fence.sc.sys per launch (not per CTA) publishes them to the peers
+    __threadfence();
     const unsigned int nblocks = gridDim.x * gridDim.y * gridDim.z;
     const unsigned int prev = atomicAdd(s.done, 1u);
     if (prev == nblocks - 1) {
       *s.done = 0u;  // re-arm for the next launch / graph replay
-      __threadfence_system();
-      for (int i = 0; i < s.n; ++i) red_release_sys_add(s.ctr[i], 1ull);
+      asm volatile("fence.acq_rel.sys;" ::: "memory");  // one system fence + relaxed adds = release per peer
+      for (int i = 0; i < s.n; ++i) red_relaxed_sys_add(s.ctr[i], 1ull);
     }
   }
 }

@@ -296,9 +296,10 @@ class InferExecutor:
                 stats.add("linear")
             else:
                 srcs = self._linear(st, stats, w_gu, self.xn, B)
-                nat.check(lib.tps_silu_mul(*srcs, B, self.F, self.act.data_ptr(), self.F, st),
-                          "tps_silu_mul")
-                stats.add("silu_mul")
+                if "silu" not in self.skip:
+                    nat.check(lib.tps_silu_mul(*srcs, B, self.F, self.act.data_ptr(), self.F, st),
+                              "tps_silu_mul")
+                    stats.add("silu_mul")
             nxt = W.tensor_ptr(l + 1, "ln1") if l + 1 < L else W.tensor_ptr(-1, "ln_f")
             yield from self._row_parallel(st, stats, 2 * l + 1, "w_d", W[(l, "w_d")], self.act, B, nxt)
         cm = self.comm
@@ -381,6 +382,8 @@ class InferExecutor:
                                       cm.done.data_ptr() + phase * 4, st), "tps_linear_push")
         stats.add("linear")
         yield
+        if "add_norm" in self.skip:
+            return
         mine = (cm.frecv_slot(cm.frecv.data_ptr(), par, 0, S), cm.tp * S, FUSE_ROWS * H)
         wait = nat.wait_spec(cm.ctr.data_ptr() + phase * 8, cm.epoch.data_ptr(), cm.tp, 0)
         nat.check(lib.tps_add_norm(self.resid.data_ptr(), *mine, wait, norm_w, ctypes.c_float(g.rms_eps), H, B,

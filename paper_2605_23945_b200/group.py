@@ -36,7 +36,7 @@ def n_phases(geom: DecoderGeometry) -> int:
 
 def build_rank(geom: DecoderGeometry, tp: int, rank: int, max_batch: int, num_slots: int, max_len: int,
                device, seed: int | None = 0, kv_pages: int | None = None,
-               weights: RankWeights | None = None) -> RankState:
+               weights: RankWeights | None = None, prefill_rows: int = 0) -> RankState:
     nat.init_device(torch.device(device).index or 0)
     sh = rank_shard(geom, tp, rank)
     if weights is None:
@@ -49,8 +49,8 @@ def build_rank(geom: DecoderGeometry, tp: int, rank: int, max_batch: int, num_sl
     slots = SlotTable(num_slots, max_len, device)
     comm = None
     if tp > 1:
-        comm = GroupComm(tp, rank, max_batch, geom.hidden, n_phases(geom), torch.device(device))
-    ex = InferExecutor(geom, sh, weights, kv, slots, max_batch, device, comm=comm)
+        comm = GroupComm(tp, rank, max(max_batch, prefill_rows), geom.hidden, n_phases(geom), torch.device(device))
+    ex = InferExecutor(geom, sh, weights, kv, slots, max_batch, device, comm=comm, prefill_rows=prefill_rows)
     return RankState(weights, kv, slots, ex, comm)
 
 

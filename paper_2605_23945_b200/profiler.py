@@ -203,3 +203,130 @@ def _start_event(be, r):
     e = torch.cuda.Event(enable_timing=True)
     e.record(be.stream(r))
     return e
+
+
+# ------------------------------------------------------------------------------------------
+# Offline Profiler on one B200 for every TP degree (tpshift/latency.py:229-250)
+# ------------------------------------------------------------------------------------------
+
+NVLINK_GBPS = 770.0       # measured peer-copy bandwidth per direction (B200_PROFILING.md)
+NVLINK_HOP_S = 1.5e-6     # remote-store + release/acquire flag latency of one allreduce hop
+
+
+def loopback_rank(geom, tp: int, max_batch: int, num_slots: int, max_len: int, kv_pages: int,
+                  prefill_rows: int = 0, device="cuda:0", seed: int = 0):
+    """One rank of a TP-`tp` group alone on the device: its peer table points at itself,
+    so every allreduce push lands in its own receive area and every signal list holds its
+    own counter tp times. The rank runs exactly the kernels, shapes and counter protocol
+    of a real TP-`tp` rank; only the NVLink hop is missing (added back by the model in
+    `nvlink_adjust`). Numerics are not meaningful -- this is a timing harness."""
+    from .executor import GroupRunner
+    from .group import build_rank
+    r = build_rank(geom, tp, 0, max_batch, num_slots, max_len, device, seed=seed, kv_pages=kv_pages,
+                   prefill_rows=prefill_rows)
+    if r.comm is not None:
+        r.comm.connect([r.comm.export()] * tp)
+    return r, GroupRunner([r.executor])
+
+
+def nvlink_adjust(geom, tp: int, batch: int) -> float:
+    """Seconds per decode step that a real TP group adds over the loopback rank: for each
+    of the 2L allreduces one NVLink hop plus the bytes this rank pushes to its tp-1 peers."""
+    if tp == 1:
+        return 0.0
+    from .executor import FUSE_ROWS, FUSE_SOURCES
+    per_row = geom.hidden * 4 * (tp - 1) * (max(1, FUSE_SOURCES // tp) if batch <= FUSE_ROWS else 1)
+    return 2 * geom.num_layers * (NVLINK_HOP_S + batch * per_row / (NVLINK_GBPS * 1e9))
+
+
+def profile_rank(geom, tp: int, token_cap: int, max_ctx: int, batches=None, lengths=None,
+                 prefill_rows: int = 512, time_budget_s: float = 900.0, log=None):
+    """Measured ProfilePoints of one TP degree on this device.
+
+    decode: the reference's protocol (tpshift/latency.py:229-250) on the real engine --
+    `batch` sequences at context L, 60 graph-replayed steps (contexts grow by one per
+    step), mean step time, plus `nvlink_adjust` for tp > 1.
+    prefill: the chunked prefill this engine runs (prompt positions through the decode
+    kernels, `prefill_rows` rows per step): ceil(batch * (L - 1) / rows) steps, each
+    timed at the mean context L / 2 (interpolated over a few measured contexts)."""
+    from .latency import ProfilePoint
+    batches = batches or [b for b in profile_batches()]
+    lengths = lengths or [l for l in profile_lengths() if l + PROFILE_DECODE_STEPS + 2 <= max_ctx]
+    grid = [(b, l) for b in batches for l in lengths if b * l <= token_cap]
+    max_b = max(b for b, _ in grid)
+    need = max(b * pages_for_tokens(l + PROFILE_DECODE_STEPS + 2) for b, l in grid)
+    r, runner = loopback_rank(geom, tp, max_b, max_b, max_ctx, need, prefill_rows=prefill_rows)
+    ex = r.executor
+    st = r.slots
+    t0 = time.perf_counter()
+    dec = {}
+    for b, l in grid:
+        if time.perf_counter() - t0 > time_budget_s:
+            break
+        ppl = pages_for_tokens(l + PROFILE_DECODE_STEPS + 2)
+        pt = torch.arange(b * ppl, dtype=torch.int32).view(b, ppl)
+        st.page_table[:b, :ppl].copy_(pt)
+        st.pos[:b] = l - 1
+        bk = ex.bucket(b)
+        runner.set_rows(bk, list(range(b)))
+        ms = step_probe(runner, bk, PROFILE_DECODE_STEPS)
+        dec[(b, l)] = ms / 1e3 + nvlink_adjust(geom, tp, b)
+        if log:
+            log(f"tp={tp} B={b} L={l}: {ms:.3f} ms")
+    # prefill step time at `prefill_rows` rows vs context (rows spread over samples)
+    pf = {}
+    R = prefill_rows
+    for ctx in [c for c in (64, 512, 2048, 8192) if c + 2 <= max_ctx]:
+        nb = max(1, min(max_b, R))
+        ppl = pages_for_tokens(ctx + 2)
+        if nb * ppl > need:
+            nb = max(1, need // ppl)
+        pt = torch.arange(nb * ppl, dtype=torch.int32).view(nb, ppl)
+        st.page_table[:nb, :ppl].copy_(pt)
+        rs = torch.tensor([i % nb for i in range(R)], dtype=torch.int32)
+        rp = torch.tensor([min(ctx, (i // nb) + ctx - (R // nb)) for i in range(R)], dtype=torch.int32)
+        ex.row_slot[R].copy_(rs)
+        ex.row_pos[R].copy_(rp)
+        key = ("prefill", R)
+        if key not in runner.graphs:
+            runner._capture_key(key, lambda s_, rr=runner: rr._issue_prefill(R, s_))
+        g = runner.graphs[key]
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = _events()
+        e0.record()
+        for _ in range(5):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        pf[ctx] = e0.elapsed_time(e1) / 5 / 1e3 + nvlink_adjust(geom, tp, min(R, 64))
+        if log:
+            log(f"tp={tp} prefill step R={R} ctx={ctx}: {pf[ctx] * 1e3:.3f} ms")
+    cs = np.array(sorted(pf), dtype=float)
+    ts = np.array([pf[c] for c in sorted(pf)], dtype=float)
+    pts = []
+    for (b, l), d in dec.items():
+        steps = -(-b * max(1, l - 1) // R)
+        pts.append(ProfilePoint(tp, b, l, d, float(steps * np.interp(l / 2, cs, ts))))
+    del runner, r
+    torch.cuda.empty_cache()
+    return pts
+
+
+def pages_for_tokens(n: int) -> int:
+    from .kvcache import PAGE
+    return -(-n // PAGE)
+
+
+def profile_b200(geom, tps=(1, 2, 4, 8), token_cap: int = 1 << 20, max_ctx: int = 16384 + 128,
+                 time_budget_s: float = 900.0, log=None):
+    """ProfileTable (the reference's CSV schema) measured on this B200 for every TP degree."""
+    pts = []
+    for tp in tps:
+        geom.check_tp(tp)
+        pts += profile_rank(geom, tp, token_cap, max_ctx, time_budget_s=time_budget_s / len(tps), log=log)
+    keep = {}
+    for p in pts:
+        keep.setdefault((p.tp, p.batch), []).append(p)
+    pts = [p for v in keep.values() if len(v) >= 2 for p in v]
+    return table_from_points(pts, token_cap)
