@@ -197,8 +197,9 @@ def main():
     rank = world.local_ranks[0]
     dev = world.devices[rank]
     spec, geom = build_spec(args, gpus)
+    table = measured_table(args.model)
     t_setup = time.perf_counter()
-    coord = GlobalCoordinator(spec, geom, world, seed=0)
+    coord = GlobalCoordinator(spec, geom, world, seed=0, table=table)
     setup_s = time.perf_counter() - t_setup
     for _ in range(args.warmup):
         coord.run()
@@ -259,7 +260,8 @@ def main():
                                f"{list(spec.controller.tp_list)}",
                    "model": args.model, "global_batch": spec.global_batch, "seq_len": args.prompt_len + args.l_max,
                    "parallelism": f"tp1->adaptive,dp{gpus}", "l2": "inputs > L2 (15.2 GB weights streamed per step)",
-                   "step": "one generation stage (prefill via decode path + decode to last sample)"},
+                   "step": "one generation stage (prefill via decode path + decode to last sample)",
+                   "predictor": "B200-measured profile table" if table is not None else "analytic b200.cfg"},
         "tokens_generated": rep.tokens_generated,
         "tokens_per_s": rep.tokens_generated / value,
         "switches": [{"from": s["from_tp"], "to": s["to_tp"], "round": s["round"],
@@ -292,7 +294,7 @@ def main():
             ex = coord = None
             torch.cuda.empty_cache()
             sspec = dataclasses.replace(spec, mode="static", initial_tp=tp)
-            coord = GlobalCoordinator(sspec, geom, world, seed=0)
+            coord = GlobalCoordinator(sspec, geom, world, seed=0, table=table)
             coord.run()
             srep, _ = coord.run()
             line["fixed_tp"][str(tp)] = srep.generation_time
@@ -311,6 +313,15 @@ def main():
                                           f"stage's {sum(hist.values())} rounds and prefill"}
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def measured_table(model: str):
+    """The B200 Offline Profiler's table for this model (presets/b200_<model>_profile.csv,
+    measured by tools/profile_b200.py): Algorithm 1's Latency Predictor is fitted to it.
+    None (the analytic b200.cfg calibration) when the model has not been profiled."""
+    from paper_2605_23945_b200.latency import load_table
+    path = os.path.join(HERE, "paper_2605_23945_b200", "presets", f"b200_{model}_profile.csv")
+    return load_table(path) if os.path.exists(path) else None
 
 
 def traffic_record():

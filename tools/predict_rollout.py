@@ -1,0 +1,32 @@
+"""Predict the N-GPU generation stage on B200 from the measured Offline-Profiler table.
+
+The reference's engine loop runs with TableBackend (measured B200 step/prefill times as
+the ground truth) and the planner fitted to the same table: adaptive (Algorithm 1) vs
+every fixed TP. Writes one JSON line per N.
+"""
+import argparse, dataclasses, json, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench
+from paper_2605_23945_b200.engine import TableBackend, run
+from paper_2605_23945_b200.latency import load_table
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--table", default=os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                                 "paper_2605_23945_b200", "presets", "b200_qwen2.5-7b_profile.csv"))
+ap.add_argument("--gpus", default="1,2,4,8")
+ap.add_argument("--per-gpu-batch", type=int, default=64)
+ap.add_argument("--l-max", type=int, default=8192)
+a = ap.parse_args()
+tab = load_table(a.table)
+for n in (int(x) for x in a.gpus.split(",")):
+    ns = argparse.Namespace(model="qwen2.5-7b", per_gpu_batch=a.per_gpu_batch, l_max=a.l_max, prompt_len=512, seed=4)
+    spec, geom = bench.build_spec(ns, n)
+    rep = run(spec, tab, TableBackend(spec, tab))
+    out = {"gpus": n, "adaptive_s": round(rep.generation_time, 3),
+           "switches": [[s["from_tp"], s["to_tp"], s["round"], round(s["breakdown"]["total"], 3)]
+                        for nr in rep.node_reports for s in nr["switches"]], "static_s": {}}
+    for tp in (1, 2, 4, 8):
+        if n % tp == 0:
+            s2 = dataclasses.replace(spec, mode="static", initial_tp=tp)
+            out["static_s"][tp] = round(run(s2, tab, TableBackend(s2, tab)).generation_time, 3)
+    print(json.dumps(out), flush=True)

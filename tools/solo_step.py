@@ -34,7 +34,9 @@ if __name__ == "__main__":
             bk = r.executor.bucket(B)
             runner.set_rows(bk, slots[:B])
             for v in variants:
-                r.executor.skip = frozenset(x for x in v.split(",") if x)
+                toks = [x for x in v.split(",") if x]
+                r.executor.fuse_rope = "+fuse_rope" in toks
+                r.executor.skip = frozenset(x for x in toks if not x.startswith("+"))
                 r.slots.pos[:] = ctx
                 runner.graphs.pop(bk, None)
                 runner.step(bk, 1)
