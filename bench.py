@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-switch", action="store_true")
     ap.add_argument("--static-tps", default="1", help="N>1: also time the stage at these fixed TP degrees")
+    ap.add_argument("--tp-list", default="", help="Algorithm 1 candidates (default: 1 and N, BASELINE config 2)")
     ap.add_argument("--cpu-threads", type=int, default=0)
     return ap.parse_args()
 
@@ -81,7 +82,10 @@ def build_spec(args, gpus):
     cfg = load_config("b200")
     geom = geometry(args.model)
     cluster = dataclasses.replace(cfg.cluster, gpus_per_node=gpus)
-    ctl = ControllerParams(tp_list=tuple(t for t in (1, 2, 4, 8) if gpus % t == 0 and _tp_ok(geom, t)),
+    # BASELINE config 2 switches TP1/DP8 -> TP8/DP1: candidates {1, N}; --tp-list widens it
+    # (config 3's multi-stage TP1 -> 2 -> 4 -> 8)
+    want = [int(x) for x in getattr(args, "tp_list", "").split(",") if x] or sorted({1, gpus})
+    ctl = ControllerParams(tp_list=tuple(t for t in want if gpus % t == 0 and _tp_ok(geom, t)),
                            eval_interval=cfg.controller.eval_interval, chunk_steps=cfg.controller.chunk_steps)
     spec = build_scenario(cfg, prompt_len=args.prompt_len, global_batch=args.per_gpu_batch * gpus,
                           l_max=args.l_max, initial_tp=1, seed=args.seed, controller=ctl)

@@ -91,6 +91,22 @@ int tps_linear_push(const void* w, int64_t n, int64_t k, int64_t ldw, const void
                     int64_t x_rows, int64_t ldx, float* const* dsts, int ndst, int64_t split_stride,
                     int splits, uint64_t* const* sig_ctrs, int nsig, unsigned int* done, void* stream);
 
+/* LL form of tps_linear_push for tail batches: each partial element is one 8-byte
+ * system-scope store {fp32 bits (low), tag (high)}, tag = (*epoch) * tag_mult + tag_add,
+ * at dsts[d] + split * split_stride + i * n + j (uint64 units). No counters, fences or
+ * signal: the consumer (tps_add_norm_ll) polls the tags (NCCL's LL protocol). */
+int tps_linear_push_ll(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,
+                       int64_t x_rows, int64_t ldx, uint64_t* const* dsts, int ndst, int64_t split_stride,
+                       int splits, const uint64_t* epoch, uint32_t tag_mult, uint32_t tag_add, void* stream);
+
+/* resid[b] += sum of the nsrc LL slots (ll + i * stride, uint64 {value, tag}, polled until
+ * every tag == (*epoch) * tag_mult + tag_add), then RMSNorm -> out (bf16). ctr (optional):
+ * this phase's arrival counter, advanced by `bump` (= tp) so it stays at epoch * tp as if
+ * the counter protocol had run (a layout's steps may use either protocol). */
+int tps_add_norm_ll(float* resid, const uint64_t* ll, int nsrc, int64_t stride, const uint64_t* epoch,
+                    uint32_t tag_mult, uint32_t tag_add, const void* w, float eps, int H, int B, void* out,
+                    int ldo, uint64_t* ctr, uint64_t bump, void* stream);
+
 /* Gate/up projection with the SwiGLU fused into the epilogue (no split-K):
  * W rows are 64-row blocks [gate c | up c] (n = 2F, F % 64 == 0);
  * act[i][f] = bf16(silu(gate_f . x_i) * (up_f . x_i)), act: bf16 [b][ld_act]. */
@@ -196,6 +212,11 @@ int tps_barrier(uint64_t* const* peer_ctrs, int npeers, uint64_t* my_ctr, uint64
 int tps_ipc_get_handle(const void* ptr, void* handle_out, int64_t* offset_out);
 int tps_ipc_open(const void* handle, void** base_out);
 int tps_ipc_close(void* base);
+
+/* Device step tracer (probe): while registered, thread 0 of block 0 of every decode
+ * kernel appends a record [kind, t_entry, t_after_wait, t_exit] (uint64, %globaltimer ns)
+ * at records[4 * atomicAdd(counter, 1)] (up to `capacity` records). NULL, NULL disables. */
+int tps_trace_enable(uint64_t* records, unsigned int* counter, unsigned int capacity);
 
 #ifdef __cplusplus
 }

@@ -37,6 +37,10 @@ SIGNATURES = {
     "tps_linear": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _vp, _i32, _vp]),
     "tps_linear_push": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _pp, _i32, _i64, _i32, _pp, _i32,
                                 _vp, _vp]),
+    "tps_linear_push_ll": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _pp, _i32, _i64, _i32, _vp,
+                                   ctypes.c_uint32, ctypes.c_uint32, _vp]),
+    "tps_add_norm_ll": (_i32, [_vp, _vp, _i32, _i64, _vp, ctypes.c_uint32, ctypes.c_uint32, _vp, _f32, _i32, _i32,
+                               _vp, _i32, _vp, ctypes.c_uint64, _vp]),
     "tps_linear_silu": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _vp, _i64, _vp]),
     "tps_embed": (_i32, [_vp, _vp, _vp, _vp, _i32, _vp, _i32, _i32, _vp, _vp]),
     "tps_add_norm": (_i32, [_vp, _vp, _i32, _i64, _vp, _vp, _f32, _i32, _i32, _vp, _i32, _vp]),
@@ -57,6 +61,7 @@ SIGNATURES = {
     "tps_ipc_get_handle": (_i32, [_vp, _vp, ctypes.POINTER(_i64)]),
     "tps_ipc_open": (_i32, [_vp, ctypes.POINTER(_vp)]),
     "tps_ipc_close": (_i32, [_vp]),
+    "tps_trace_enable": (_i32, [_vp, _vp, ctypes.c_uint]),
 }
 
 

@@ -50,6 +50,16 @@ int configure_gemm();
 int configure_attention();
 int configure_copy();
 int configure_decode_ops();
+int linear_push_ll(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
+                   int64_t ldx, const DstList& dst, int64_t split_stride, int splits, const uint64_t* tag_epoch,
+                   uint32_t tag_mult, uint32_t tag_add, cudaStream_t stream);
+int add_norm_ll(float* resid, const uint64_t* ll, int nsrc, long long stride, const uint64_t* epoch, uint32_t mult,
+                uint32_t add, const void* w, float eps, int H, int B, void* out, int ldo, uint64_t* ctr,
+                uint64_t bump, cudaStream_t st);
+int trace_register_decode(uint64_t*, unsigned int*, unsigned int);
+int trace_register_attention(uint64_t*, unsigned int*, unsigned int);
+int trace_register_attention_bal(uint64_t*, unsigned int*, unsigned int);
+int trace_register_gemm(uint64_t*, unsigned int*, unsigned int);
 int barrier(uint64_t* const*, int, uint64_t*, uint64_t, cudaStream_t);
 int ipc_get_handle(const void*, void*, int64_t*);
 int ipc_open(const void*, void**);
@@ -132,6 +142,25 @@ int tps_linear_push(const void* w, int64_t n, int64_t k, int64_t ldw, const void
   int rc = make_sig(sig_ctrs, nsig, done, &sg);
   if (rc) return rc;
   return linear_push(w, n, k, ldw, x, b, x_rows, ldx, dl, split_stride, splits, sg, S(stream));
+}
+
+int tps_linear_push_ll(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
+                       int64_t ldx, uint64_t* const* dsts, int ndst, int64_t split_stride, int splits,
+                       const uint64_t* epoch, uint32_t tag_mult, uint32_t tag_add, void* stream) {
+  TPS_CHECK_ARG(ndst >= 1 && ndst <= kMaxPeers && dsts, "linear_push_ll: 1..8 destinations");
+  DstList dl;
+  dl.n = ndst;
+  for (int i = 0; i < ndst; ++i) dl.p[i] = reinterpret_cast<float*>(dsts[i]);
+  return linear_push_ll(w, n, k, ldw, x, b, x_rows, ldx, dl, split_stride, splits, epoch, tag_mult, tag_add,
+                        S(stream));
+}
+
+int tps_add_norm_ll(float* resid, const uint64_t* ll, int nsrc, int64_t stride, const uint64_t* epoch,
+                    uint32_t tag_mult, uint32_t tag_add, const void* w, float eps, int H, int B, void* out, int ldo,
+                    uint64_t* ctr, uint64_t bump, void* stream) {
+  TPS_CHECK_ARG(resid && w && out, "add_norm_ll: null pointer");
+  return add_norm_ll(resid, ll, nsrc, stride, epoch, tag_mult, tag_add, w, eps, H, B, out, ldo, ctr, bump,
+                     S(stream));
 }
 
 int tps_linear_silu(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
@@ -264,5 +293,13 @@ int tps_ipc_get_handle(const void* ptr, void* handle_out, int64_t* offset_out) {
 }
 int tps_ipc_open(const void* handle, void** base_out) { return ipc_open(handle, base_out); }
 int tps_ipc_close(void* base) { return ipc_close(base); }
+
+int tps_trace_enable(uint64_t* records, unsigned int* counter, unsigned int capacity) {
+  TPS_CHECK_ARG((records && counter) || (!records && !counter), "trace: records and counter together");
+  if (trace_register_decode(records, counter, capacity) || trace_register_attention(records, counter, capacity) ||
+      trace_register_attention_bal(records, counter, capacity) || trace_register_gemm(records, counter, capacity))
+    return fail(kCuda, "trace: cudaMemcpyToSymbol failed");
+  return kOk;
+}
 
 }  // extern "C"

@@ -53,7 +53,9 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_kernel(
   const int g = lane >> 2, c = lane & 3;
 
   pdl_launch_dependents();  // dependents may launch now: they read our outputs only after their own wait
+  const unsigned int trs = trace_begin(kTrAttnSplit);
   pdl_wait();
+  trace_mark(trs, 2);
 
   const int slot = row_slot[b];
   const int ctx = slot >= 0 ? (row_pos ? row_pos[b] : pos_by_slot[slot]) + 1 : 0;
@@ -283,6 +285,7 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_kernel(
     out[((size_t)b * nq + head0 + h) * D + d] = f2bf(acc * inv_l[h]);
   }
   if (tid == 0) merge_ctr[b * nkv + kvh] = 0u;  // re-arm for the next launch / graph replay
+  trace_mark(trs, 3);
 }
 
 // Many-split merge (long contexts at small batch): one CTA per (row, query head), one
@@ -299,7 +302,9 @@ __global__ void __launch_bounds__(D) attn_combine_kernel(const int* __restrict__
   __shared__ float fac[kMaxAttnSplits];
   __shared__ float s_inv;
   pdl_launch_dependents();  // dependents may launch now: they read our outputs only after their own wait
+  const unsigned int trs = trace_begin(kTrAttnCombine);
   pdl_wait();
+  trace_mark(trs, 2);
   const int b = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
   const int slot = row_slot[b];
   const int ctx = slot >= 0 ? (row_pos ? row_pos[b] : pos_by_slot[slot]) + 1 : 0;
@@ -334,6 +339,7 @@ __global__ void __launch_bounds__(D) attn_combine_kernel(const int* __restrict__
       if (s0 + j < active) acc += v[j] * fac[s0 + j];
   }
   out[((size_t)b * nq + h) * D + d] = f2bf(acc * s_inv);
+  trace_mark(trs, 3);
 }
 
 constexpr int kInKernelMergeMaxSplits = 4;
@@ -429,5 +435,7 @@ int paged_attention(const void* q, const void* k_cache, const void* v_cache, con
   return launch_k(attn_combine_kernel<64>, dim3(B, nq), dim3(64), 0, st, true, row_slot, pos_by_slot, row_pos, nq,
                   nsplit, (const float*)part_m, (const float*)part_l, (const float*)part_o, oo);
 }
+
+int trace_register_attention(uint64_t* p, unsigned int* c, unsigned int n) { return trace_register(p, c, n); }
 
 }  // namespace tps

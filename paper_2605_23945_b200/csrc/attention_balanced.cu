@@ -63,6 +63,7 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_balanced_kernel(
   const int g = lane >> 2, c4 = lane & 3;
   const bool decode = row_pos == nullptr;
   pdl_launch_dependents();  // the O projection may launch and prefetch its weights now
+  const unsigned int trs = trace_begin(kTrAttnBal);
   if (!decode) pdl_wait();  // prefill: earlier rows of this chunk were appended by the previous kernel
 
   // ---- unit prefix over rows: row b owns nkv * ceil(ctx_b / 64) units ----
@@ -162,6 +163,7 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_balanced_kernel(
     cp_async_commit();
   }
   if (decode) pdl_wait();
+  trace_mark(trs, 2);
 
   // padding rows (slot < 0) have no units: CTA 0 zeroes their output
   if (cta == 0) {
@@ -369,6 +371,7 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_balanced_kernel(
     }
   }
   cp_async_wait<0>();
+  trace_mark(trs, 3);
 }
 
 static int g_bal_grid[2] = {0, 0};  // resident CTA capacity for D = 64, 128
@@ -423,6 +426,10 @@ int paged_attention_balanced(const void* q, const void* k_cache, const void* v_c
                     row_slot, pos_by_slot, row_pos, page_table, max_pages, B, nq, nkv, G, scale_log2, part_m,
                     part_l, part_o, merge_ctr, oo);
   return fail(kInvalid, "paged_attention: head_dim must be 64 or 128");
+}
+
+int trace_register_attention_bal(uint64_t* p, unsigned int* c, unsigned int n) {
+  return trace_register(p, c, n);
 }
 
 }  // namespace tps

@@ -102,6 +102,16 @@ __device__ __forceinline__ void red_relaxed_sys_add(uint64_t* p, uint64_t v) {
   asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// Single-copy-atomic 8-byte system-scope stores / loads for the LL {value, tag} protocol.
+__device__ __forceinline__ void st_relaxed_sys_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ ulonglong2 ld_relaxed_sys_v2u64(const uint64_t* p) {
+  ulonglong2 v;
+  asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
+  return v;
+}
+
 // Spin (one thread) until *p >= target; traps after the watchdog budget.
 __device__ __forceinline__ void wait_counter_geq(const uint64_t* p, uint64_t target) {
   if (ld_acquire_sys(p) >= target) return;

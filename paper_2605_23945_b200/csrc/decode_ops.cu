@@ -15,6 +15,8 @@
 // row_slot vector. row_slot[b] < 0 marks a padding row of a graph bucket.
 #include <stdlib.h>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "decode_ops.cuh"
 
@@ -97,7 +99,9 @@ __global__ void embed_kernel(const int* __restrict__ row_slot, const int* __rest
                              const int* __restrict__ row_pos, const int* __restrict__ history, int hist_ld,
                              const __nv_bfloat16* __restrict__ table, int H, float* __restrict__ resid) {
   pdl_launch_dependents();  // dependents may launch now: they read our outputs only after their own wait
+  const unsigned int trs = trace_begin(kTrEmbed);
   pdl_wait();
+  trace_mark(trs, 2);
   const int b = blockIdx.x;
   const int slot = row_slot[b];
   int tok = 0;
@@ -105,6 +109,7 @@ __global__ void embed_kernel(const int* __restrict__ row_slot, const int* __rest
   const __nv_bfloat162* src = reinterpret_cast<const __nv_bfloat162*>(table + (size_t)tok * H);
   float2* dst = reinterpret_cast<float2*>(resid + (size_t)b * H);
   for (int i = threadIdx.x; i < H / 2; i += blockDim.x) dst[i] = __bfloat1622float2(src[i]);
+  trace_mark(trs, 3);
 }
 
 // ------------------------------------------------- residual add + RMSNorm ---
@@ -119,8 +124,10 @@ __global__ void __launch_bounds__(kNormThreads) add_norm_kernel(float* __restric
   __shared__ float red[32];
   const int b = blockIdx.x;
   pdl_launch_dependents();  // dependents may launch now: they read our outputs only after their own wait
+  const unsigned int trs = trace_begin(kTrAddNorm);
   pdl_wait();
   do_wait(wait);
+  trace_mark(trs, 2);
   float4* r4 = reinterpret_cast<float4*>(resid + (size_t)b * H);
   const int H4 = H / 4;
   float4 v[kNormVec];
@@ -153,6 +160,189 @@ __global__ void __launch_bounds__(kNormThreads) add_norm_kernel(float* __restric
       o[2 * i + 1] = __floats2bfloat162_rn(v[j].z * rstd * w23.x, v[j].w * rstd * w23.y);
     }
   }
+  trace_mark(trs, 3);
+}
+
+// ------------------------------------- residual add + RMSNorm, LL sources ---
+// Same as add_norm_kernel, but the n sources are the TP peers' fused-projection slots in
+// LL form: uint64 {fp32 bits, tag} written by the producers' epilogues. Each thread polls
+// its own elements until every tag equals (*epoch) * mult + add (watchdog-bounded), then
+// sums the sources in index order: no counters, no fences on the critical path.
+__device__ __forceinline__ bool ll_ok(const ulonglong2& a, const ulonglong2& c, uint32_t want) {
+  return (uint32_t)(a.x >> 32) == want && (uint32_t)(a.y >> 32) == want && (uint32_t)(c.x >> 32) == want &&
+         (uint32_t)(c.y >> 32) == want;
+}
+
+// Loads of 8 sources are issued together (one L2 round trip per batch when the data is
+// already there); a source whose tags are not yet current is re-polled on its own.
+__device__ __forceinline__ float4 ll_sum4(const uint64_t* base, int n, long long stride, long long off4,
+                                          uint32_t want) {
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int i0 = 0; i0 < n; i0 += 8) {
+    ulonglong2 a[8], c[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (i0 + j < n) {
+        const uint64_t* p = base + (long long)(i0 + j) * stride + off4 * 4;
+        a[j] = ld_relaxed_sys_v2u64(p);
+        c[j] = ld_relaxed_sys_v2u64(p + 2);
+      }
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (i0 + j < n) {
+        if (!ll_ok(a[j], c[j], want)) {
+          const uint64_t* p = base + (long long)(i0 + j) * stride + off4 * 4;
+          const uint64_t t0 = globaltimer_ns();
+          do {
+            if (globaltimer_ns() - t0 > kWatchdogNs) {
+              printf("tps watchdog: LL source %d of %d (base %p, element %lld) tag %u != %u\n", i0 + j, n,
+                     (const void*)base, off4 * 4, (unsigned)(a[j].x >> 32), want);
+              __trap();
+            }
+            a[j] = ld_relaxed_sys_v2u64(p);
+            c[j] = ld_relaxed_sys_v2u64(p + 2);
+          } while (!ll_ok(a[j], c[j], want));
+        }
+        acc.x += __uint_as_float((uint32_t)a[j].x);
+        acc.y += __uint_as_float((uint32_t)a[j].y);
+        acc.z += __uint_as_float((uint32_t)c[j].x);
+        acc.w += __uint_as_float((uint32_t)c[j].y);
+      }
+  }
+  return acc;
+}
+
+__global__ void __launch_bounds__(kNormThreads) add_norm_ll_kernel(float* __restrict__ resid,
+                                                                   const uint64_t* __restrict__ ll, int nsrc,
+                                                                   long long stride, const uint64_t* epoch,
+                                                                   uint32_t mult, uint32_t add,
+                                                                   const __nv_bfloat16* __restrict__ w, float eps,
+                                                                   int H, __nv_bfloat16* __restrict__ out, int ldo,
+                                                                   unsigned long long* ctr, unsigned long long bump) {
+  __shared__ float red[32];
+  const int b = blockIdx.x;
+  pdl_launch_dependents();  // dependents may launch now: they read our outputs only after their own wait
+  const unsigned int trs = trace_begin(kTrAddNorm);
+  pdl_wait();
+  trace_mark(trs, 2);
+  const uint32_t want = (uint32_t)(*(volatile const uint64_t*)epoch * mult + add);
+  // keep this phase's arrival counter at epoch * tp as if the counter protocol had run
+  // (steps of one TP layout may use either protocol: B > 64 and chunked prefill push)
+  if (ctr && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(ctr, bump);
+  float4* r4 = reinterpret_cast<float4*>(resid + (size_t)b * H);
+  const int H4 = H / 4;
+  float4 v[kNormVec];
+  float ss = 0.f;
+#pragma unroll
+  for (int j = 0; j < kNormVec; ++j) {
+    const int i = threadIdx.x + j * kNormThreads;
+    if (i < H4) {
+      float4 x = r4[i];
+      const float4 p = ll_sum4(ll, nsrc, stride, (long long)b * H4 + i, want);
+      x.x += p.x; x.y += p.y; x.z += p.z; x.w += p.w;
+      r4[i] = x;
+      v[j] = x;
+      ss += x.x * x.x + x.y * x.y + x.z * x.z + x.w * x.w;
+    }
+  }
+  ss = block_sum<kNormThreads>(ss, red);
+  const float rstd = rsqrtf(ss / (float)H + eps);
+  __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(out + (size_t)b * ldo);
+  const __nv_bfloat162* wp = reinterpret_cast<const __nv_bfloat162*>(w);
+#pragma unroll
+  for (int j = 0; j < kNormVec; ++j) {
+    const int i = threadIdx.x + j * kNormThreads;
+    if (i < H4) {
+      const float2 w01 = __bfloat1622float2(wp[2 * i]);
+      const float2 w23 = __bfloat1622float2(wp[2 * i + 1]);
+      o[2 * i] = __floats2bfloat162_rn(v[j].x * rstd * w01.x, v[j].y * rstd * w01.y);
+      o[2 * i + 1] = __floats2bfloat162_rn(v[j].z * rstd * w23.x, v[j].w * rstd * w23.y);
+    }
+  }
+  trace_mark(trs, 3);
+}
+
+// ------------------------------- residual add + RMSNorm, cluster of 8 CTAs ---
+// One row is split over a cluster of kNormCluster CTAs (each owns H / 8 columns), so the
+// partial sums -- split-K partials, or the tp x splits slots of a fused TP allreduce,
+// plain fp32 or LL {value, tag} -- are read by 8 SMs instead of one; the row's sum of
+// squares is reduced through distributed shared memory in fixed rank order (identical on
+// every CTA and every TP rank). LL: see add_norm_ll_kernel.
+constexpr int kNormCluster = 8;
+constexpr int kNormCThreads = 128;
+constexpr int kNormCVec = 2;  // float4 per thread: H <= 8 * 128 * 2 * 4 = 8192
+template <bool LL>
+__global__ void __launch_bounds__(kNormCThreads)
+    add_norm_cluster_kernel(float* __restrict__ resid, Src src, WaitSpec wait, const uint64_t* __restrict__ ll,
+                            int nll, long long ll_stride, const uint64_t* epoch, uint32_t mult, uint32_t add,
+                            unsigned long long* ctr, unsigned long long bump, const __nv_bfloat16* __restrict__ w,
+                            float eps, int H, __nv_bfloat16* __restrict__ out, int ldo) {
+  __shared__ float red[kNormCThreads / 32];
+  __shared__ float s_part;
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int crank = (int)cluster.block_rank();
+  const int b = blockIdx.y;
+  pdl_launch_dependents();  // dependents may launch now: they read our outputs only after their own wait
+  const unsigned int trs = trace_begin(kTrAddNorm);
+  pdl_wait();
+  if constexpr (!LL) do_wait(wait);
+  trace_mark(trs, 2);
+  uint32_t want = 0;
+  if constexpr (LL) {
+    want = (uint32_t)(*(volatile const uint64_t*)epoch * mult + add);
+    if (ctr && crank == 0 && b == 0 && threadIdx.x == 0) atomicAdd(ctr, bump);
+  }
+  const int H4 = H / 4;
+  const int per = (H4 + kNormCluster - 1) / kNormCluster;
+  const int lo = crank * per, hi = min(H4, lo + per);
+  float4* r4 = reinterpret_cast<float4*>(resid + (size_t)b * H);
+  float4 v[kNormCVec];
+  float ss = 0.f;
+#pragma unroll
+  for (int j = 0; j < kNormCVec; ++j) {
+    const int i = lo + threadIdx.x + j * kNormCThreads;
+    if (i < hi) {
+      float4 x = r4[i];
+      float4 p;
+      if constexpr (LL) p = ll_sum4(ll, nll, ll_stride, (long long)b * H4 + i, want);
+      else p = src.n > 0 ? src_sum4<16>(src, (long long)b * H4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (LL || src.n > 0) {
+        x.x += p.x; x.y += p.y; x.z += p.z; x.w += p.w;
+        r4[i] = x;
+      }
+      v[j] = x;
+      ss += x.x * x.x + x.y * x.y + x.z * x.z + x.w * x.w;
+    }
+  }
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < kNormCThreads / 32; ++i) t += red[i];
+    s_part = t;
+  }
+  cluster.sync();
+  float tot = 0.f;
+#pragma unroll
+  for (int r = 0; r < kNormCluster; ++r) tot += *cluster.map_shared_rank(&s_part, r);
+  const float rstd = rsqrtf(tot / (float)H + eps);
+  __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(out + (size_t)b * ldo);
+  const __nv_bfloat162* wp = reinterpret_cast<const __nv_bfloat162*>(w);
+#pragma unroll
+  for (int j = 0; j < kNormCVec; ++j) {
+    const int i = lo + threadIdx.x + j * kNormCThreads;
+    if (i < hi) {
+      const float2 w01 = __bfloat1622float2(wp[2 * i]);
+      const float2 w23 = __bfloat1622float2(wp[2 * i + 1]);
+      o[2 * i] = __floats2bfloat162_rn(v[j].x * rstd * w01.x, v[j].y * rstd * w01.y);
+      o[2 * i + 1] = __floats2bfloat162_rn(v[j].z * rstd * w23.x, v[j].w * rstd * w23.y);
+    }
+  }
+  cluster.sync();  // peers may still be reading this CTA's partial
+  trace_mark(trs, 3);
 }
 
 // ------------------------------------------- TP one-shot allreduce (push) ---
@@ -161,13 +351,16 @@ __global__ void __launch_bounds__(kNormThreads) add_norm_kernel(float* __restric
 constexpr int kPushBlocks = 64;
 __global__ void __launch_bounds__(256) reduce_push_kernel(Src src, DstList dst, long long n4, SignalSpec sig) {
   pdl_launch_dependents();  // dependents may launch now: they read our outputs only after their own wait
+  const unsigned int trs = trace_begin(kTrReducePush);
   pdl_wait();
+  trace_mark(trs, 2);
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
        i += (long long)gridDim.x * blockDim.x) {
     const float4 v = src_sum4(src, i);
     for (int d = 0; d < dst.n; ++d) reinterpret_cast<float4*>(dst.p[d])[i] = v;
   }
   do_signal(sig);
+  trace_mark(trs, 3);
 }
 
 // ---------------------------------------------- QKV bias + RoPE + KV append ---
@@ -182,7 +375,9 @@ __global__ void __launch_bounds__(128) qkv_rope_append_kernel(
     const float* __restrict__ cos_t, const float* __restrict__ sin_t, int B, int nq, int nkv, int D, int P,
     __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ k_cache, __nv_bfloat16* __restrict__ v_cache) {
   pdl_launch_dependents();  // dependents may launch now: they read our outputs only after their own wait
+  const unsigned int trs = trace_begin(kTrQkvRope);
   pdl_wait();
+  trace_mark(trs, 2);
   const int heads = nq + nkv;
   const int task = blockIdx.x * 4 + (threadIdx.x >> 5);
   if (task >= B * heads) return;
@@ -221,13 +416,16 @@ __global__ void __launch_bounds__(128) qkv_rope_append_kernel(
       v_cache[off + i + half] = f2bf(v2);
     }
   }
+  trace_mark(trs, 3);
 }
 
 // ------------------------------------------------------------- SiLU * up ---
 // partial layout [split][B][2F] = [gate rows | up rows]; out[b][f] = bf16(silu(g) * u)
 __global__ void silu_mul_kernel(Src src, int B, int F, __nv_bfloat16* __restrict__ out, int ldo) {
   pdl_launch_dependents();  // dependents may launch now: they read our outputs only after their own wait
+  const unsigned int trs = trace_begin(kTrSilu);
   pdl_wait();
+  trace_mark(trs, 2);
   const int F4 = F / 4;
   const long long total = (long long)B * F4;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
@@ -242,6 +440,7 @@ __global__ void silu_mul_kernel(Src src, int B, int F, __nv_bfloat16* __restrict
     o[0] = __floats2bfloat162_rn(g.x / (1.f + __expf(-g.x)) * u.x, g.y / (1.f + __expf(-g.y)) * u.y);
     o[1] = __floats2bfloat162_rn(g.z / (1.f + __expf(-g.z)) * u.z, g.w / (1.f + __expf(-g.w)) * u.w);
   }
+  trace_mark(trs, 3);
 }
 
 // ------------------------------------------------------- greedy argmax ---
@@ -260,7 +459,9 @@ __global__ void __launch_bounds__(kArgmaxThreads) argmax_stage1_kernel(Src src, 
   __shared__ float sv[kArgmaxThreads / 32];
   __shared__ int si[kArgmaxThreads / 32];
   pdl_launch_dependents();  // dependents may launch now: they read our outputs only after their own wait
+  const unsigned int trs = trace_begin(kTrArgmax1);
   pdl_wait();
+  trace_mark(trs, 2);
   const int b = blockIdx.x, c = blockIdx.y;
   const int per = ((V + nchunk - 1) / nchunk + 3) & ~3;
   const int lo = c * per, hi = min(V, lo + per);
@@ -295,6 +496,7 @@ __global__ void __launch_bounds__(kArgmaxThreads) argmax_stage1_kernel(Src src, 
     cand[(size_t)b * nchunk + c] = ArgmaxCand{best, bidx};
   }
   do_signal(sig);
+  trace_mark(trs, 3);
 }
 
 // Stage 2: reduce the candidates of every TP rank (list order = rank order),
@@ -304,8 +506,10 @@ __global__ void argmax_finalize_kernel(CandList cands, int nchunk, WaitSpec wait
                                        int* __restrict__ history, int hist_ld, int* __restrict__ out_tok) {
   const int b = blockIdx.x;
   pdl_launch_dependents();  // dependents may launch now: they read our outputs only after their own wait
+  const unsigned int trs = trace_begin(kTrArgmax2);
   pdl_wait();
   do_wait(wait);
+  trace_mark(trs, 2);
   float best = -INFINITY;
   int bidx = 0x7fffffff;
   for (int k = threadIdx.x; k < cands.n * nchunk; k += blockDim.x) {
@@ -328,6 +532,7 @@ __global__ void argmax_finalize_kernel(CandList cands, int nchunk, WaitSpec wait
       pos_by_slot[slot] = pos + 1;
     }
   }
+  trace_mark(trs, 3);
 }
 
 __global__ void epoch_advance_kernel(uint64_t* epoch) {
@@ -358,8 +563,21 @@ int embed(const int* row_slot, const int* pos_by_slot, const int* row_pos, const
                   reinterpret_cast<const __nv_bfloat16*>(table), H, resid);
 }
 
+static bool g_norm_cluster = [] {
+  const char* e = getenv("TPS_NORM_CLUSTER");
+  return !(e && e[0] == '0');
+}();
+
 int add_norm(float* resid, const Src& src, const WaitSpec& wait, const void* w, float eps, int H, int B,
              void* out, int ldo, cudaStream_t st) {
+  // tail batches: spread each row over a cluster (measured: TP8 B=1 step 1.93 -> 1.58 ms); at
+  // B >= 32 one 512-thread CTA per row is faster (TP1 B=64: 4.67 vs 4.95 ms)
+  if (g_norm_cluster && B <= 16 && H % 4 == 0 && H / 4 <= kNormCluster * kNormCThreads * kNormCVec &&
+      src.n <= 16 && ldo % 2 == 0 && B > 0 && (src.n == 0 || src.stride % 4 == 0))
+    return launch_kc(add_norm_cluster_kernel<false>, dim3(kNormCluster, B), dim3(kNormCThreads), kNormCluster, st,
+                     true, resid, src, wait, (const uint64_t*)nullptr, 0, 0LL, (const uint64_t*)nullptr, 0u, 0u,
+                     (unsigned long long*)nullptr, 0ULL, reinterpret_cast<const __nv_bfloat16*>(w), eps, H,
+                     reinterpret_cast<__nv_bfloat16*>(out), ldo);
   TPS_CHECK_ARG(H % 4 == 0 && ldo % 2 == 0 && B > 0, "add_norm: H must be a multiple of 4");
   TPS_CHECK_ARG(H / 4 <= kNormThreads * kNormVec, "add_norm: H > 8192");
   TPS_CHECK_ARG(src.n == 0 || src.stride % 4 == 0, "add_norm: source stride must be a multiple of 4");
@@ -369,6 +587,26 @@ int add_norm(float* resid, const Src& src, const WaitSpec& wait, const void* w, 
                     reinterpret_cast<const __nv_bfloat16*>(w), eps, H, reinterpret_cast<__nv_bfloat16*>(out), ldo);
   return launch_k(add_norm_kernel<8>, dim3(B), dim3(kNormThreads), 0, st, true, resid, src, wait,
                   reinterpret_cast<const __nv_bfloat16*>(w), eps, H, reinterpret_cast<__nv_bfloat16*>(out), ldo);
+}
+
+int add_norm_ll(float* resid, const uint64_t* ll, int nsrc, long long stride, const uint64_t* epoch, uint32_t mult,
+                uint32_t add, const void* w, float eps, int H, int B, void* out, int ldo, uint64_t* ctr,
+                uint64_t bump, cudaStream_t st) {
+  TPS_CHECK_ARG(H % 4 == 0 && ldo % 2 == 0 && B > 0 && nsrc >= 1 && ll && epoch, "add_norm_ll: bad arguments");
+  TPS_CHECK_ARG(H / 4 <= kNormThreads * kNormVec, "add_norm_ll: H > 8192");
+  TPS_CHECK_ARG(stride % 4 == 0 && (reinterpret_cast<uintptr_t>(ll) & 15) == 0, "add_norm_ll: 16B-aligned slots");
+  if (g_norm_cluster && H / 4 <= kNormCluster * kNormCThreads * kNormCVec) {
+    Src none{nullptr, 0, 0};
+    WaitSpec nowait{nullptr, nullptr, 0, 0};
+    return launch_kc(add_norm_cluster_kernel<true>, dim3(kNormCluster, B), dim3(kNormCThreads), kNormCluster, st,
+                     true, resid, none, nowait, ll, nsrc, (long long)stride, epoch, mult, add,
+                     reinterpret_cast<unsigned long long*>(ctr), (unsigned long long)bump,
+                     reinterpret_cast<const __nv_bfloat16*>(w), eps, H, reinterpret_cast<__nv_bfloat16*>(out), ldo);
+  }
+  return launch_k(add_norm_ll_kernel, dim3(B), dim3(kNormThreads), 0, st, true, resid, ll, nsrc, stride, epoch,
+                  mult, add, reinterpret_cast<const __nv_bfloat16*>(w), eps, H,
+                  reinterpret_cast<__nv_bfloat16*>(out), ldo, reinterpret_cast<unsigned long long*>(ctr),
+                  (unsigned long long)bump);
 }
 
 int reduce_push(const Src& src, const DstList& dst, long long n, const SignalSpec& sig, cudaStream_t st) {
@@ -421,10 +659,15 @@ int sum_src(const Src& src, long long n, float* out, cudaStream_t st) {
   return launch_k(sum_src_kernel, dim3(grid_for(n, 256, 4 * kNumSMs)), dim3(256), 0, st, false, src, n, out);
 }
 
+int trace_register_decode(uint64_t* p, unsigned int* c, unsigned int n) { return trace_register(p, c, n); }
+
 int configure_decode_ops() {
   TPS_MAX_CARVEOUT(embed_kernel);
   TPS_MAX_CARVEOUT(add_norm_kernel<8>);
   TPS_MAX_CARVEOUT(add_norm_kernel<16>);
+  TPS_MAX_CARVEOUT(add_norm_ll_kernel);
+  TPS_MAX_CARVEOUT(add_norm_cluster_kernel<false>);
+  TPS_MAX_CARVEOUT(add_norm_cluster_kernel<true>);
   TPS_MAX_CARVEOUT(reduce_push_kernel);
   TPS_MAX_CARVEOUT(qkv_rope_append_kernel);
   TPS_MAX_CARVEOUT(silu_mul_kernel);

@@ -75,6 +75,45 @@ __device__ __forceinline__ void signal_last_cta(const SignalSpec& s) {
   }
 }
 
+// ----------------------------------------------------- device step tracer (probe) ---
+// When a trace buffer is registered (tps_trace_enable), thread 0 of block 0 of every traced
+// launch writes [kind, t_entry, t_after_wait, t_exit] (%globaltimer ns) into the next free
+// record; records land in launch order, so a graph replay reads back as an in-chain timeline
+// (the latency each kernel adds inside a real step, PDL overlap included). Disabled: one
+// load of a null pointer by one thread.
+struct TraceBuf {
+  uint64_t* p;
+  unsigned int* ctr;
+  unsigned int cap;
+};
+static __device__ TraceBuf g_trace_buf;  // one per translation unit, set by trace_register()
+enum TraceKind : int {
+  kTrEmbed = 1, kTrAddNorm, kTrReducePush, kTrQkvRope, kTrSilu, kTrArgmax1, kTrArgmax2, kTrEpoch,
+  kTrGemm, kTrGemmSilu, kTrAttnSplit, kTrAttnCombine, kTrAttnBal
+};
+__device__ __forceinline__ uint64_t trace_now() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned int trace_begin(int kind) {
+  if (blockIdx.x | blockIdx.y | blockIdx.z | threadIdx.x) return ~0u;
+  const TraceBuf t = g_trace_buf;
+  if (t.p == nullptr) return ~0u;
+  const unsigned int slot = atomicAdd(t.ctr, 1u);
+  if (slot >= t.cap) return ~0u;
+  t.p[4 * slot] = (uint64_t)kind;
+  t.p[4 * slot + 1] = trace_now();
+  return slot;
+}
+__device__ __forceinline__ void trace_mark(unsigned int slot, int field) {
+  if (slot != ~0u) g_trace_buf.p[4 * slot + field] = trace_now();
+}
+static inline int trace_register(uint64_t* p, unsigned int* ctr, unsigned int cap) {
+  TraceBuf t{p, ctr, cap};
+  return cudaMemcpyToSymbol(g_trace_buf, &t, sizeof(t)) == cudaSuccess ? 0 : -1;
+}
+
 // ----------------------------------------------- programmatic dependent launch
 // Decode-step kernels are launched with the PDL attribute: each calls
 // pdl_launch_dependents() early (the next kernel may start its prologue) and
@@ -99,6 +138,29 @@ int launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaS
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = (pdl && pdl_enabled()) ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+  if (e != cudaSuccess) return fail(kCuda, std::string("launch: ") + cudaGetErrorString(e));
+  return kOk;
+}
+
+// launch_k with a thread-block cluster of cluster_x CTAs along x (DSMEM reductions).
+template <typename... KArgs, typename... Args>
+int launch_kc(void (*kernel)(KArgs...), dim3 grid, dim3 block, int cluster_x, cudaStream_t st, bool pdl,
+              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster_x;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (pdl && pdl_enabled()) ? 2 : 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
   if (e != cudaSuccess) return fail(kCuda, std::string("launch: ") + cudaGetErrorString(e));
   return kOk;

@@ -94,7 +94,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_swapab_kernel(const __grid_constant__ CUtensorMap tmap_w,
                        const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ DstList dst,
                        long long split_stride, int N, int B, int num_tiles, int splits, int chunks, int acts,
-                       __nv_bfloat16* __restrict__ act_out, int ld_act, const __grid_constant__ SignalSpec sig) {
+                       __nv_bfloat16* __restrict__ act_out, int ld_act, const __grid_constant__ SignalSpec sig,
+                       const uint64_t* __restrict__ tag_epoch, uint32_t tag_mult, uint32_t tag_add) {
   using Cfg = GemmCfg<BN>;
   constexpr int S = Cfg::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -109,6 +110,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* tmem_empty = bars + 2 * S + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
 
+  const unsigned int trs = trace_begin(EPI == kEpiPartial ? kTrGemm : kTrGemmSilu);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   // unit u = ((tile * splits + split) * acts + act): the activation tiles of one weight
@@ -173,6 +175,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           tma_load_2d(smem_a + i * Cfg::kABytes, &tmap_w, &full[i], (c0 + i) * kBK, tile * kBM, pol_w);
         }
         pdl_wait();
+        trace_mark(trs, 2);
         for (int i = 0; i < pre; ++i)
           tma_load_2d(smem_b + i * Cfg::kBBytes, &tmap_x, &full[i], (c0 + i) * kBK, act * BN, pol_x);
         stage = pre % S;
@@ -250,16 +253,28 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         // split-K workspace, or -- the fused TP allreduce -- this rank's slots in each
         // peer's receive area (NVLink P2P stores), split-major with split_stride. The
         // consumer sums the partials in a fixed order (deterministic, no atomics).
+        // LL mode (tag_epoch set): every element goes out as one 8-byte {value, tag} store
+        // (tag = epoch * mult + add), so the consumer polls the data itself -- no fence,
+        // counter or last-CTA signal on the critical path (NCCL's LL protocol).
         const size_t off = (size_t)split * (size_t)split_stride + (size_t)b0 * (size_t)N + (size_t)n;
+        const uint64_t tag = tag_epoch ? ((uint64_t)((uint32_t)(*(volatile const uint64_t*)tag_epoch * tag_mult +
+                                                                tag_add)) << 32) : 0ull;
         for (int j0 = 0; j0 < rows; j0 += 16) {
           uint32_t r[16];
           tmem_ld16(tmem_base + (uint32_t)(acc * BN + j0) + ((uint32_t)(q * 32) << 16), r);
           if (n < N) {
             for (int d = 0; d < dst.n; ++d) {
-              float* o = dst.p[d] + off;
+              if (tag_epoch) {
+                uint64_t* o = reinterpret_cast<uint64_t*>(dst.p[d]) + off;
 #pragma unroll
-              for (int j = 0; j < 16; ++j)
-                if (j0 + j < rows) o[(size_t)(j0 + j) * N] = __uint_as_float(r[j]);
+                for (int j = 0; j < 16; ++j)
+                  if (j0 + j < rows) st_relaxed_sys_u64(o + (size_t)(j0 + j) * N, tag | r[j]);
+              } else {
+                float* o = dst.p[d] + off;
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                  if (j0 + j < rows) o[(size_t)(j0 + j) * N] = __uint_as_float(r[j]);
+              }
             }
           }
         }
@@ -304,6 +319,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                  "n"(Cfg::kTmemCols));
   }
+  trace_mark(trs, 3);
   // fused allreduce: the last CTA to finish releases one arrival on every peer's counter
   signal_last_cta(sig);
 }
@@ -397,6 +413,9 @@ struct EpiArgs {
   __nv_bfloat16* act_out;
   int ld_act;
   SignalSpec sig;
+  const uint64_t* tag_epoch = nullptr;
+  uint32_t tag_mult = 0;
+  uint32_t tag_add = 0;
 };
 
 template <int BN, int EPI>
@@ -407,7 +426,8 @@ static int launch_gemm(const CUtensorMap& mw, const CUtensorMap& mx, const EpiAr
   const int units = tiles * splits * acts;
   const int grid = units < kNumSMs ? units : kNumSMs;
   return launch_k(gemm_swapab_kernel<BN, EPI>, dim3(grid), dim3(kGemmThreads), Cfg::kSmemBytes, stream, true, mw,
-                  mx, e.dst, e.split_stride, n, b, tiles, splits, chunks, acts, e.act_out, e.ld_act, e.sig);
+                  mx, e.dst, e.split_stride, n, b, tiles, splits, chunks, acts, e.act_out, e.ld_act, e.sig,
+                  e.tag_epoch, e.tag_mult, e.tag_add);
 }
 
 template <int BN>
@@ -489,6 +509,28 @@ int linear_push(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x,
                                stream);
 }
 
+// LL push: partial (split, i, j) -> dst.p[d][split * split_stride + i * n + j] as a uint64
+// {fp32 bits, tag}, tag = (*tag_epoch) * tag_mult + tag_add (no counters, no signal).
+int linear_push_ll(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
+                   int64_t ldx, const DstList& dst, int64_t split_stride, int splits, const uint64_t* tag_epoch,
+                   uint32_t tag_mult, uint32_t tag_add, cudaStream_t stream) {
+  const int64_t chunks = (k + kBK - 1) / kBK;
+  TPS_CHECK_ARG(splits >= 1 && splits <= chunks, "linear: splits must be in [1, ceil(k/64)]");
+  TPS_CHECK_ARG(dst.n >= 1 && dst.n <= kMaxPeers, "linear: 1..8 destinations");
+  TPS_CHECK_ARG(split_stride >= b * n, "linear: split_stride must hold [b][n]");
+  TPS_CHECK_ARG(tag_epoch != nullptr, "linear_push_ll: null epoch");
+  for (int d = 0; d < dst.n; ++d)
+    TPS_CHECK_ARG((reinterpret_cast<uintptr_t>(dst.p[d]) & 7) == 0, "linear_push_ll: destinations must be 8B aligned");
+  CUtensorMap mw, mx;
+  int bn;
+  int rc = prepare(w, n, k, ldw, x, b, x_rows, ldx, &mw, &mx, &bn);
+  if (rc) return rc;
+  EpiArgs e{dst, (long long)split_stride, nullptr, 0, SignalSpec{}, tag_epoch, tag_mult, tag_add};
+  e.sig.n = 0;
+  return dispatch<kEpiPartial>(bn, mw, mx, e, (int)n, (int)b, (int)((n + kBM - 1) / kBM), splits, (int)chunks,
+                               stream);
+}
+
 int linear_silu(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
                 int64_t ldx, void* act, int64_t ld_act, cudaStream_t stream) {
   TPS_CHECK_ARG(act && n % kBM == 0, "linear_silu: N = 2F must be a multiple of 128 (64-row gate/up blocks)");
@@ -505,5 +547,7 @@ int linear_silu(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x,
   e.sig.n = 0;
   return dispatch<kEpiSiluMul>(bn, mw, mx, e, (int)n, (int)b, (int)(n / kBM), 1, (int)chunks, stream);
 }
+
+int trace_register_gemm(uint64_t* p, unsigned int* c, unsigned int n) { return trace_register(p, c, n); }
 
 }  // namespace tps

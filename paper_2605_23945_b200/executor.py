@@ -53,8 +53,8 @@ class GroupComm:
     """Communication state of one TP group as held by one rank.
 
     recv[parity][src_rank] : fp32 [max_batch][H] receive slots (one-shot allreduce push)
-    frecv[parity][src_rank * splits + split] : fp32 [FUSE_ROWS][H] slots the peers' fused
-                             projection epilogues store their split partials into
+    ll[parity][src_rank * splits + split] : uint64 [FUSE_ROWS][H] {fp32, tag} slots the peers'
+                             fused projection epilogues store their split partials into (LL)
     cand                   : per-(row, chunk) argmax candidates (8 B each)
     ctr[phase]             : arrival counters, +1 per peer per phase per step
     done[phase]            : last-CTA detectors of this rank's signalling launches
@@ -69,37 +69,39 @@ class GroupComm:
         self.hidden = hidden
         self.n_phases = n_phases
         self.recv = torch.zeros((2, tp, max_batch, hidden), dtype=torch.float32, device=device)
-        self.frecv = torch.zeros((2, FUSE_SOURCES, FUSE_ROWS, hidden), dtype=torch.float32, device=device)
+        # tags start at 0 and live tags are >= n_phases (epochs start at 1): no stale match
+        self.ll = torch.zeros((2, FUSE_SOURCES, FUSE_ROWS, hidden), dtype=torch.int64, device=device)
         self.cand = torch.zeros((max_batch, 64, 2), dtype=torch.int32, device=device)
         self.ctr = torch.zeros(n_phases, dtype=torch.int64, device=device)
         self.done = torch.zeros(n_phases, dtype=torch.int32, device=device)
         self.epoch = torch.ones(1, dtype=torch.int64, device=device)
         # peer pointer table, rank order (filled by connect / the Cache Manager)
         self.peer_recv: list[int] = []
-        self.peer_frecv: list[int] = []
+        self.peer_ll: list[int] = []
+        self.loopback = False  # timing harness: this rank plays every peer of its group
         self.peer_ctr: list[int] = []
         self.peer_cand: list[int] = []
 
     # local export for peers
     def export(self) -> dict:
-        return {"recv": self.recv.data_ptr(), "frecv": self.frecv.data_ptr(), "ctr": self.ctr.data_ptr(),
+        return {"recv": self.recv.data_ptr(), "ll": self.ll.data_ptr(), "ctr": self.ctr.data_ptr(),
                 "cand": self.cand.data_ptr()}
 
     def connect(self, tables: list[dict]) -> None:
         assert len(tables) == self.tp
         self.peer_recv = [t["recv"] for t in tables]
-        self.peer_frecv = [t["frecv"] for t in tables]
+        self.peer_ll = [t["ll"] for t in tables]
         self.peer_ctr = [t["ctr"] for t in tables]
         self.peer_cand = [t["cand"] for t in tables]
 
     def recv_slot(self, base: int, parity: int, src_rank: int) -> int:
         return base + ((parity * self.tp + src_rank) * self.max_batch * self.hidden) * 4
 
-    def frecv_slot(self, base: int, parity: int, src_rank: int, splits: int) -> int:
-        """First slot of src_rank in a fused receive area when every rank pushes `splits`
+    def ll_slot(self, base: int, parity: int, src_rank: int, splits: int) -> int:
+        """First slot of src_rank in an LL receive area when every rank pushes `splits`
         partials: slot index src_rank * splits + split, so the tp x splits used slots are
         contiguous and are read back in (rank, split) order."""
-        return base + ((parity * FUSE_SOURCES + src_rank * splits) * FUSE_ROWS * self.hidden) * 4
+        return base + ((parity * FUSE_SOURCES + src_rank * splits) * FUSE_ROWS * self.hidden) * 8
 
     def reset(self) -> None:
         self.ctr.zero_()
@@ -360,9 +362,9 @@ class InferExecutor:
         """O / down projection + TP allreduce + residual add + RMSNorm.
 
         TP > 1 and B <= FUSE_ROWS: the projection epilogue stores its split-K partials
-        straight into every peer's fused receive area and the last CTA signals
-        (tps_linear_push: the allreduce is fused into the projection); add+norm waits
-        for the tp arrivals and sums the tp x splits slots in (rank, split) order.
+        straight into every peer's receive area as {value, tag} pairs (tps_linear_push_ll:
+        the allreduce is fused into the projection, LL protocol -- no counters or fences);
+        add+norm polls the tags and sums the tp x splits slots in (rank, split) order.
         Otherwise: split partials -> tps_reduce_push -> add+norm."""
         cm = self.comm
         if cm is None or B > FUSE_ROWS or "fuse_push" in self.skip or "linear" in self.skip:
@@ -375,19 +377,20 @@ class InferExecutor:
         n, k = w.shape
         S = self.fused_splits(fam, B)
         par = phase % 2
-        dsts = [cm.frecv_slot(base, par, self.rank, S) for base in cm.peer_frecv]
-        sigs = [p + phase * 8 for p in cm.peer_ctr]
-        nat.check(lib.tps_linear_push(w.data_ptr(), n, k, k, x.data_ptr(), B, x.shape[0], x.shape[1],
-                                      self._arr(dsts), len(dsts), FUSE_ROWS * H, S, self._arr(sigs), len(sigs),
-                                      cm.done.data_ptr() + phase * 4, st), "tps_linear_push")
+        # LL: {value, tag} stores polled by the consumer; tag = epoch * n_phases + phase
+        # (a loopback timing rank -- profiler.loopback_rank -- fills every rank's slots itself)
+        dsts = [cm.ll_slot(base, par, q if cm.loopback else self.rank, S) for q, base in enumerate(cm.peer_ll)]
+        nat.check(lib.tps_linear_push_ll(w.data_ptr(), n, k, k, x.data_ptr(), B, x.shape[0], x.shape[1],
+                                         self._arr(dsts), len(dsts), FUSE_ROWS * H, S, cm.epoch.data_ptr(),
+                                         cm.n_phases, phase, st), "tps_linear_push_ll")
         stats.add("linear")
         yield
         if "add_norm" in self.skip:
             return
-        mine = (cm.frecv_slot(cm.frecv.data_ptr(), par, 0, S), cm.tp * S, FUSE_ROWS * H)
-        wait = nat.wait_spec(cm.ctr.data_ptr() + phase * 8, cm.epoch.data_ptr(), cm.tp, 0)
-        nat.check(lib.tps_add_norm(self.resid.data_ptr(), *mine, wait, norm_w, ctypes.c_float(g.rms_eps), H, B,
-                                   self.xn.data_ptr(), H, st), "tps_add_norm")
+        nat.check(lib.tps_add_norm_ll(self.resid.data_ptr(), cm.ll_slot(cm.ll.data_ptr(), par, 0, S), cm.tp * S,
+                                      FUSE_ROWS * H, cm.epoch.data_ptr(), cm.n_phases, phase, norm_w,
+                                      ctypes.c_float(g.rms_eps), H, B, self.xn.data_ptr(), H,
+                                      cm.ctr.data_ptr() + phase * 8, cm.tp, st), "tps_add_norm_ll")
         stats.add("add_norm")
 
     def _allreduce_norm(self, st, stats, phase: int, srcs: tuple[int, int, int], B: int, norm_w: int):

@@ -226,6 +226,7 @@ def loopback_rank(geom, tp: int, max_batch: int, num_slots: int, max_len: int, k
                    prefill_rows=prefill_rows)
     if r.comm is not None:
         r.comm.connect([r.comm.export()] * tp)
+        r.comm.loopback = True
     return r, GroupRunner([r.executor])
 
 

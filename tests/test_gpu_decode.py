@@ -103,3 +103,27 @@ def test_graph_replay_matches_eager():
         torch.cuda.synchronize()
         outs.append(ranks[0].slots.history[slots].cpu())
     assert torch.equal(outs[0], outs[1])
+
+
+def test_protocol_mix_ll_counter_prefill_tp2():
+    """One TP layout alternates the LL allreduce (B <= 64), the counter allreduce (B > 64)
+    and a chunked prefill (counter path): every phase counter stays at epoch * tp, so no
+    wait can deadlock (the watchdog would trap) and every step's logits stay finite."""
+    import math
+    geom = geometry("tiny")
+    ranks, runner = build_group(geom, 2, max_batch=96, num_slots=96, max_len=96, seed=4)
+    for r in ranks:
+        r.executor.prefill_rows = 0
+    slots = [admit(ranks, i, [1 + i % 50, 2, 3], max_ctx=64) for i in range(80)]
+    for B, n in ((4, 3), (80, 2), (4, 2), (96, 1), (8, 2)):
+        bk = ranks[0].executor.bucket(B)
+        runner.set_rows(bk, slots[:min(B, 80)])
+        runner.step(bk, n)
+        lg = last_logits(ranks)
+        torch.cuda.synchronize()
+        assert torch.isfinite(lg[:min(B, 80)]).all(), B
+    for r in ranks:
+        cm = r.executor.comm
+        ep = int(cm.epoch.item())
+        L = geom.num_layers
+        assert cm.ctr[:2 * L].tolist() == [(ep - 1) * 2] * (2 * L)

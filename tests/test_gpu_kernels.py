@@ -5,6 +5,7 @@ they are compared with a torch fp32 matmul of the same bf16 inputs at
 |d| <= 1e-3 * sqrt(K) * max|ref| relative slack; copies are bit-exact.
 """
 
+import ctypes
 import math
 
 import pytest
@@ -264,3 +265,41 @@ def test_linear_push_fused_allreduce_epilogue(n, k, b, ndst, splits):
         assert torch.isnan(t[:, b:]).all()
         assert c.tolist() == [0, 3, 0, 0]
     assert done.tolist() == [0, 0, 0, 0]
+
+
+@pytest.mark.parametrize("b,tp,splits", [(1, 8, 2), (5, 2, 4), (64, 4, 3)])
+def test_ll_push_and_norm(b, tp, splits):
+    """LL fused allreduce: tp 'ranks' push {value, tag} partials of their row-parallel
+    projection into one receive area; tps_add_norm_ll polls the tags, sums the tp x splits
+    slots in (rank, split) order, adds the residual and RMS-normalises."""
+    from paper_2605_23945_b200.executor import FUSE_ROWS, FUSE_SOURCES
+    torch.manual_seed(b * tp)
+    H, K = 512, 256
+    lib = nat.lib()
+    ll = torch.zeros((FUSE_SOURCES, FUSE_ROWS, H), dtype=torch.int64, device="cuda")
+    epoch = torch.full((1,), 7, dtype=torch.int64, device="cuda")
+    mult, phase = 11, 3
+    ws = [(torch.randn(H, K, device="cuda") * 0.05).bfloat16() for _ in range(tp)]
+    xs = [torch.randn(b, K, device="cuda").bfloat16() for _ in range(tp)]
+    row = FUSE_ROWS * H * 8
+    for r in range(tp):
+        dst = ll.data_ptr() + r * splits * row
+        nat.check(lib.tps_linear_push_ll(ws[r].data_ptr(), H, K, K, xs[r].data_ptr(), b, b, K,
+                                         nat.ptr_array([dst]), 1, FUSE_ROWS * H, splits, epoch.data_ptr(), mult,
+                                         phase, _stream()))
+    torch.cuda.synchronize()
+    tags = (ll[:tp * splits, :b] >> 32)
+    assert (tags == 7 * mult + phase).all()
+    resid = torch.randn(b, H, device="cuda")
+    ref_resid = resid + sum(xs[r].float() @ ws[r].float().T for r in range(tp))
+    wn = (torch.rand(H, device="cuda") + 0.5).bfloat16()
+    out = torch.zeros(b, H, dtype=torch.bfloat16, device="cuda")
+    ctr = torch.full((1,), 5, dtype=torch.int64, device="cuda")
+    nat.check(lib.tps_add_norm_ll(resid.data_ptr(), ll.data_ptr(), tp * splits, FUSE_ROWS * H, epoch.data_ptr(),
+                                  mult, phase, wn.data_ptr(), ctypes.c_float(1e-6), H, b, out.data_ptr(), H,
+                                  ctr.data_ptr(), tp, _stream()))
+    torch.cuda.synchronize()
+    ref = ref_resid * torch.rsqrt(ref_resid.pow(2).mean(-1, keepdim=True) + 1e-6) * wn.float()
+    assert (resid - ref_resid).abs().max().item() < 2e-3
+    assert (out.float() - ref).abs().max().item() < 3e-2
+    assert ctr.item() == 5 + tp  # the phase counter advanced as if the counter protocol had run

@@ -16,13 +16,15 @@ ap.add_argument("--table", default=os.path.join(os.path.dirname(os.path.dirname(
 ap.add_argument("--gpus", default="1,2,4,8")
 ap.add_argument("--per-gpu-batch", type=int, default=64)
 ap.add_argument("--l-max", type=int, default=8192)
+ap.add_argument("--tp-list", default="", help="Algorithm 1 candidates (default 1,N as bench.py)")
 a = ap.parse_args()
 tab = load_table(a.table)
 for n in (int(x) for x in a.gpus.split(",")):
-    ns = argparse.Namespace(model="qwen2.5-7b", per_gpu_batch=a.per_gpu_batch, l_max=a.l_max, prompt_len=512, seed=4)
+    ns = argparse.Namespace(model="qwen2.5-7b", per_gpu_batch=a.per_gpu_batch, l_max=a.l_max, prompt_len=512, seed=4,
+                            tp_list=a.tp_list)
     spec, geom = bench.build_spec(ns, n)
     rep = run(spec, tab, TableBackend(spec, tab))
-    out = {"gpus": n, "adaptive_s": round(rep.generation_time, 3),
+    out = {"gpus": n, "tp_list": list(spec.controller.tp_list), "adaptive_s": round(rep.generation_time, 3),
            "switches": [[s["from_tp"], s["to_tp"], s["round"], round(s["breakdown"]["total"], 3)]
                         for nr in rep.node_reports for s in nr["switches"]], "static_s": {}}
     for tp in (1, 2, 4, 8):

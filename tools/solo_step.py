@@ -12,11 +12,9 @@ from paper_2605_23945_b200.models import geometry
 
 
 def solo(geom, tp, maxb, ctx, rank=0):
-    r = build_rank(geom, tp, rank, maxb, maxb, ctx + 256, "cuda:0", seed=0)
-    if r.comm is not None:
-        r.comm.connect([r.comm.export()] * tp)
-        r.comm.rank = rank
-    return r, GroupRunner([r.executor])
+    from paper_2605_23945_b200.profiler import loopback_rank
+    from paper_2605_23945_b200.kvcache import pages_for
+    return loopback_rank(geom, tp, maxb, maxb, ctx + 256, maxb * pages_for(ctx + 256))
 
 
 if __name__ == "__main__":
