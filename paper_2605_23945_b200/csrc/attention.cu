@@ -240,6 +240,7 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_kernel(
 
   // ---- split merge by the last CTA of this (row, kv head) ----
   // (with many splits the merge is done by attn_combine_kernel instead: merge_ctr == null)
+  trace_mark(trs, 3);  // (a merging CTA overwrites this with its own exit below)
   if (merge_ctr == nullptr) return;
   __threadfence();
   __syncthreads();
@@ -379,7 +380,9 @@ static int g_min_bal = [] {
 }();
 
 int attn_splits(int B, int nkv, int max_pages) {
-  if (B * nkv >= g_min_bal && B <= kBalMaxRows) return 0;
+  // page-balanced when the (row, kv head) segments give enough parallel work, and for a
+  // single local KV head (TP-sharded GQA tail: measured faster than split + combine)
+  if ((B * nkv >= g_min_bal || nkv == 1) && B <= kBalMaxRows) return 0;
   return attn_fixed_splits(B, nkv, max_pages);
 }
 

@@ -368,6 +368,29 @@ __global__ void __launch_bounds__(256) reduce_push_kernel(Src src, DstList dst, 
 // [q heads | k heads | v heads] (canonical shard layout). RoPE is the
 // rotate-half form used by Llama/Qwen2 with a host-built fp32 cos/sin table.
 // KV cache per layer: [num_pages][nkv][P][D] bf16. One warp per (row, head).
+// NV series of split partials summed together: all NV x 8 loads of a batch are in flight
+// at once (one L2 round trip per 8 splits however many series a thread needs).
+template <int NV>
+__device__ __forceinline__ void src_sum_multi(const Src& s, const long long (&off)[NV], float (&out)[NV]) {
+#pragma unroll
+  for (int k = 0; k < NV; ++k) out[k] = 0.f;
+  for (int i0 = 0; i0 < s.n; i0 += 8) {
+    float v[NV][8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+      for (int k = 0; k < NV; ++k)
+        if (i0 + j < s.n) v[k][j] = s.base[(long long)(i0 + j) * s.stride + off[k]];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+      for (int k = 0; k < NV; ++k)
+        if (i0 + j < s.n) out[k] += v[k][j];
+  }
+}
+
+// One thread per (row, head, rotary pair i < D/2): every split partial of the pair is
+// loaded in one batch, so a TP-sharded QKV with many splits costs one L2 round trip.
 __global__ void __launch_bounds__(128) qkv_rope_append_kernel(
     Src src, const __nv_bfloat16* __restrict__ bias, const int* __restrict__ row_slot,
     const int* __restrict__ pos_by_slot, const int* __restrict__ row_pos, const int* __restrict__ page_table,
@@ -379,41 +402,44 @@ __global__ void __launch_bounds__(128) qkv_rope_append_kernel(
   pdl_wait();
   trace_mark(trs, 2);
   const int heads = nq + nkv;
-  const int task = blockIdx.x * 4 + (threadIdx.x >> 5);
-  if (task >= B * heads) return;
-  const int b = task / heads, h = task % heads;
-  const int lane = threadIdx.x & 31;
   const int half = D / 2;
-  const int slot = row_slot[b];
-  const long long N = (long long)(nq + 2 * nkv) * D;
-  const int pos = slot >= 0 ? (row_pos ? row_pos[b] : pos_by_slot[slot]) : 0;
-  const long long rowoff = (long long)b * N;
-  for (int i = lane; i < half; i += 32) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < (long long)B * heads * half) {
+    const int b = (int)(t / (heads * half));
+    const int rem = (int)(t - (long long)b * heads * half);
+    const int h = rem / half, i = rem % half;
+    const int slot = row_slot[b];
+    const long long N = (long long)(nq + 2 * nkv) * D;
+    const int pos = slot >= 0 ? (row_pos ? row_pos[b] : pos_by_slot[slot]) : 0;
+    const long long rowoff = (long long)b * N;
     const float cs = cos_t[(size_t)pos * half + i];
     const float sn = sin_t[(size_t)pos * half + i];
     if (h < nq) {
       const int c0 = h * D;
-      float x1 = src_sum(src, rowoff + c0 + i), x2 = src_sum(src, rowoff + c0 + i + half);
-      if (bias) { x1 += bf2f(bias[c0 + i]); x2 += bf2f(bias[c0 + i + half]); }
+      const long long off[2] = {rowoff + c0 + i, rowoff + c0 + i + half};
+      float x[2];
+      src_sum_multi<2>(src, off, x);
+      if (bias) { x[0] += bf2f(bias[c0 + i]); x[1] += bf2f(bias[c0 + i + half]); }
       __nv_bfloat16* q = q_out + ((size_t)b * nq + h) * D;
-      q[i] = f2bf(x1 * cs - x2 * sn);
-      q[i + half] = f2bf(x2 * cs + x1 * sn);
+      q[i] = f2bf(x[0] * cs - x[1] * sn);
+      q[i + half] = f2bf(x[1] * cs + x[0] * sn);
     } else if (slot >= 0) {
       const int j = h - nq;
       const int kc0 = nq * D + j * D;
       const int vc0 = (nq + nkv) * D + j * D;
-      float k1 = src_sum(src, rowoff + kc0 + i), k2 = src_sum(src, rowoff + kc0 + i + half);
-      float v1 = src_sum(src, rowoff + vc0 + i), v2 = src_sum(src, rowoff + vc0 + i + half);
-      if (bias) {
-        k1 += bf2f(bias[kc0 + i]); k2 += bf2f(bias[kc0 + i + half]);
-        v1 += bf2f(bias[vc0 + i]); v2 += bf2f(bias[vc0 + i + half]);
-      }
       const int page = page_table[(size_t)slot * max_pages + pos / P];
-      const size_t off = (((size_t)page * nkv + j) * P + (pos % P)) * D;
-      k_cache[off + i] = f2bf(k1 * cs - k2 * sn);
-      k_cache[off + i + half] = f2bf(k2 * cs + k1 * sn);
-      v_cache[off + i] = f2bf(v1);
-      v_cache[off + i + half] = f2bf(v2);
+      const long long off[4] = {rowoff + kc0 + i, rowoff + kc0 + i + half, rowoff + vc0 + i, rowoff + vc0 + i + half};
+      float x[4];
+      src_sum_multi<4>(src, off, x);
+      if (bias) {
+        x[0] += bf2f(bias[kc0 + i]); x[1] += bf2f(bias[kc0 + i + half]);
+        x[2] += bf2f(bias[vc0 + i]); x[3] += bf2f(bias[vc0 + i + half]);
+      }
+      const size_t off_c = (((size_t)page * nkv + j) * P + (pos % P)) * D;
+      k_cache[off_c + i] = f2bf(x[0] * cs - x[1] * sn);
+      k_cache[off_c + i + half] = f2bf(x[1] * cs + x[0] * sn);
+      v_cache[off_c + i] = f2bf(x[2]);
+      v_cache[off_c + i + half] = f2bf(x[3]);
     }
   }
   trace_mark(trs, 3);
@@ -620,8 +646,8 @@ int qkv_rope_append(const Src& src, const void* bias, const int* row_slot, const
                     const float* sin_t, int B, int nq,
                     int nkv, int D, int P, void* q_out, void* k_cache, void* v_cache, cudaStream_t st) {
   TPS_CHECK_ARG(D % 2 == 0 && D <= 256 && B > 0 && nq > 0 && nkv > 0, "qkv_rope_append: bad shape");
-  const int tasks = B * (nq + nkv);
-  return launch_k(qkv_rope_append_kernel, dim3((tasks + 3) / 4), dim3(128), 0, st, true, src,
+  const long long threads = (long long)B * (nq + nkv) * (D / 2);
+  return launch_k(qkv_rope_append_kernel, dim3((unsigned)((threads + 127) / 128)), dim3(128), 0, st, true, src,
                   reinterpret_cast<const __nv_bfloat16*>(bias), row_slot, pos_by_slot, row_pos, page_table,
                   max_pages,
                   cos_t, sin_t, B, nq, nkv, D, P, reinterpret_cast<__nv_bfloat16*>(q_out),

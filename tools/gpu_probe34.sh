@@ -1,0 +1,2 @@
+timeout 300 python tools/trace_step.py qwen2.5-7b 8 1 2048 2>&1 | head -28
+timeout 300 python tools/trace_step.py qwen2.5-7b 1 64 2048 2>&1 | head -12
