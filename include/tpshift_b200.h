@@ -148,8 +148,9 @@ int tps_qkv_rope_append(const float* src, int nsrc, int64_t src_stride, const vo
                         const float* sin_t, int B, int nq, int nkv, int D, int page_size, void* q_out,
                         void* k_cache, void* v_cache, void* stream);
 
-/* Split policy for tps_paged_attention: 0 = page-balanced schedule (B x nkv >= 64,
- * B <= 512), else the fixed split count for this shape. */
+/* Split policy for tps_paged_attention: -1 = one thread-block cluster per (row, kv head)
+ * segment (tail batches, B x nkv <= 16), 0 = page-balanced schedule (B x nkv >= 64 or one
+ * local KV head, B <= 512), else the fixed split count for this shape. */
 int tps_attn_splits(int B, int nkv, int max_pages);
 /* fp32 elements of part_o a tps_paged_attention call needs (part_m / part_l: that / D);
  * nsplit = 0 selects the page-balanced schedule. */
@@ -160,6 +161,8 @@ int64_t tps_attn_workspace(int B, int nq, int D, int nsplit);
  * the launch are divided evenly over a persistent grid of resident CTAs, whatever the
  * context lengths; a (row, kv head) cut between CTAs is merged (log-sum-exp) by its
  * last piece. nsplit > 0: fixed split-KV per (row, kv head), merged by the last CTA.
+ * nsplit = -1: a cluster of 8-16 CTAs per (row, kv head) splits the pages and merges the
+ * softmax states through distributed shared memory (no scratch, no atomics).
  * part_m/part_l/part_o: fp32 scratch of tps_attn_workspace elements (part_o; the
  * others / D); merge_ctr: zero-initialised uint32 [B][nkv] (self re-arming). B <= 512
  * for the balanced form. KV term of tpshift/latency.py:123. */

@@ -17,6 +17,8 @@
 //     fragment loads); the G query heads sharing a KV head form the 16-row
 //     MMA operand, so QK^T and PV run on the tensor pipe and the CTA only
 //     streams bytes.
+#include <cooperative_groups.h>
+
 #include "attention_common.cuh"
 
 namespace tps {
@@ -345,6 +347,147 @@ __global__ void __launch_bounds__(D) attn_combine_kernel(const int* __restrict__
 
 constexpr int kInKernelMergeMaxSplits = 4;
 
+// ------------------------------------------------------------------------------------
+// Tail-batch attention: one thread-block cluster per (row, kv head) segment. Each CTA of
+// the cluster streams its slice of the segment's pages through the cp.async ring and keeps
+// its (max, sum, O) softmax state in shared memory; after a cluster barrier every CTA merges
+// a slice of the G x D output straight out of its peers' shared memory (DSMEM) -- no
+// global partials, atomics or second kernel on the critical path of a 1..16-row step.
+template <int D>
+__global__ void __launch_bounds__(kAttnThreads) paged_attn_cluster_kernel(
+    const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k_cache,
+    const __nv_bfloat16* __restrict__ v_cache, const int* __restrict__ row_slot,
+    const int* __restrict__ pos_by_slot, const int* __restrict__ row_pos, const int* __restrict__ page_table,
+    int max_pages, int nq, int nkv, int G, float scale_log2, __nv_bfloat16* __restrict__ out) {
+  namespace cg = cooperative_groups;
+  constexpr int CPR = D / 8;
+  constexpr int TILE = kPage * D;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  __nv_bfloat16* sk = reinterpret_cast<__nv_bfloat16*>(smem_raw);
+  __nv_bfloat16* sv = sk + kAttnStages * TILE;
+  __shared__ float c_m[16], c_l[16];
+  __shared__ __align__(16) float c_o[16 * D];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CL = (int)cluster.num_blocks();
+  const int crank = (int)cluster.block_rank();
+  const int seg = blockIdx.y;
+  const int b = seg / nkv, kvh = seg % nkv;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, c = lane & 3;
+  pdl_launch_dependents();  // dependents may launch now: they read our outputs only after their own wait
+  const unsigned int trs = trace_begin(kTrAttnSplit);
+  pdl_wait();
+  trace_mark(trs, 2);
+  const int slot = row_slot[b];
+  const int ctx = slot >= 0 ? (row_pos ? row_pos[b] : pos_by_slot[slot]) + 1 : 0;
+  const int npages = (ctx + kPage - 1) / kPage;
+  const int pps = (npages + CL - 1) / CL;
+  const int p0 = min(npages, crank * pps), p1 = min(npages, p0 + pps);
+  const int head0 = kvh * G;
+  float* wm = reinterpret_cast<float*>(smem_raw);
+  float* wl = wm + 4 * 16;
+  float* wo = wl + 4 * 16;  // [warp][16][D]
+  float m_r[2] = {-INFINITY, -INFINITY};
+  float l_r[2] = {0.f, 0.f};
+  float o[D / 8][4];
+#pragma unroll
+  for (int i = 0; i < D / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  if (p0 < p1) {
+    const int* pt = page_table + (size_t)slot * max_pages;
+    auto load_page = [&](int p, int st) {
+      const size_t goff = ((size_t)pt[p] * nkv + kvh) * TILE;
+      const __nv_bfloat16* gk = k_cache + goff;
+      const __nv_bfloat16* gv = v_cache + goff;
+      __nv_bfloat16* dk = sk + st * TILE;
+      __nv_bfloat16* dv = sv + st * TILE;
+#pragma unroll
+      for (int i = tid; i < kPage * CPR; i += kAttnThreads) {
+        const int row = i / CPR, cc = i % CPR;
+        const int sw = row * D + ((cc ^ (row & 7)) * 8);
+        cp_async16(dk + sw, gk + row * D + cc * 8);
+        cp_async16(dv + sw, gv + row * D + cc * 8);
+      }
+    };
+#pragma unroll
+    for (int i = 0; i < kAttnStages - 1; ++i) {
+      if (p0 + i < p1) load_page(p0 + i, i);
+      cp_async_commit();
+    }
+    uint32_t qa[D / 16][4];
+    load_q_frags<D>(qa, q + ((size_t)b * nq + head0) * D, G);
+    for (int it = 0; p0 + it < p1; ++it) {
+      cp_async_wait<kAttnStages - 2>();
+      __syncthreads();
+      {
+        const int nxt = it + kAttnStages - 1;
+        if (p0 + nxt < p1) load_page(p0 + nxt, nxt % kAttnStages);
+        cp_async_commit();
+      }
+      const int st = it % kAttnStages;
+      attend_page<D>(sk + st * TILE, sv + st * TILE, qa, (p0 + it) * kPage, ctx, scale_log2, m_r, l_r, o);
+    }
+    cp_async_wait<0>();
+  }
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    l_r[r] += __shfl_xor_sync(0xffffffffu, l_r[r], 1);
+    l_r[r] += __shfl_xor_sync(0xffffffffu, l_r[r], 2);
+  }
+  // the CTA's own state: merge its 4 warps (as the split kernel does)
+  __syncthreads();
+  if (c == 0) {
+    wm[warp * 16 + g] = m_r[0];
+    wm[warp * 16 + g + 8] = m_r[1];
+    wl[warp * 16 + g] = l_r[0];
+    wl[warp * 16 + g + 8] = l_r[1];
+  }
+#pragma unroll
+  for (int dn = 0; dn < D / 8; ++dn) {
+    const int d = dn * 8 + 2 * c;
+    wo[(warp * 16 + g) * D + d] = o[dn][0];
+    wo[(warp * 16 + g) * D + d + 1] = o[dn][1];
+    wo[(warp * 16 + g + 8) * D + d] = o[dn][2];
+    wo[(warp * 16 + g + 8) * D + d + 1] = o[dn][3];
+  }
+  __syncthreads();
+  for (int i = tid; i < G * D; i += kAttnThreads) {
+    const int h = i / D, d = i % D;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) M = fmaxf(M, wm[w * 16 + h]);
+    float L = 0.f, acc = 0.f;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const float mw = wm[w * 16 + h];
+      const float f = (mw == -INFINITY) ? 0.f : exp2f(mw - M);
+      L += wl[w * 16 + h] * f;
+      acc += wo[(w * 16 + h) * D + d] * f;
+    }
+    c_o[h * D + d] = acc;
+    if (d == 0) {
+      c_m[h] = M;
+      c_l[h] = L;
+    }
+  }
+  cluster.sync();
+  // merge across the cluster: CTA r finishes output elements r, r + CL, ... of the G x D tile
+  for (int i = crank * kAttnThreads + tid; i < G * D; i += CL * kAttnThreads) {
+    const int h = i / D, d = i % D;
+    float M = -INFINITY;
+    for (int r = 0; r < CL; ++r) M = fmaxf(M, *cluster.map_shared_rank(&c_m[h], r));
+    float L = 0.f, acc = 0.f;
+    for (int r = 0; r < CL; ++r) {
+      const float mr = *cluster.map_shared_rank(&c_m[h], r);
+      const float f = (mr == -INFINITY) ? 0.f : exp2f(mr - M);
+      L += *cluster.map_shared_rank(&c_l[h], r) * f;
+      acc += *cluster.map_shared_rank(&c_o[h * D + d], r) * f;
+    }
+    out[((size_t)b * nq + head0 + h) * D + d] = f2bf(L > 0.f ? acc / L : 0.f);
+  }
+  cluster.sync();  // peers may still be reading this CTA's state
+  trace_mark(trs, 3);
+}
+
 template <int D>
 static constexpr int attn_smem() {
   return 2 * kAttnStages * kPage * D * 2;
@@ -363,6 +506,14 @@ int configure_attention() {
                                     attn_smem<128>()));
   TPS_CUDA_TRY(cudaFuncSetAttribute(paged_attn_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     attn_smem<64>()));
+  TPS_CUDA_TRY(cudaFuncSetAttribute(paged_attn_cluster_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    attn_smem<128>()));
+  TPS_CUDA_TRY(cudaFuncSetAttribute(paged_attn_cluster_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    attn_smem<64>()));
+  TPS_CUDA_TRY(cudaFuncSetAttribute(paged_attn_cluster_kernel<128>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  TPS_CUDA_TRY(cudaFuncSetAttribute(paged_attn_cluster_kernel<64>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  TPS_MAX_CARVEOUT(paged_attn_cluster_kernel<128>);
+  TPS_MAX_CARVEOUT(paged_attn_cluster_kernel<64>);
   TPS_MAX_CARVEOUT(paged_attn_kernel<128>);
   TPS_MAX_CARVEOUT(paged_attn_kernel<64>);
   TPS_MAX_CARVEOUT(attn_combine_kernel<128>);
@@ -379,9 +530,16 @@ static int g_min_bal = [] {
   return e ? atoi(e) : 64;
 }();
 
+// TPS_ATTN_MAX_CLUSTER=<n>: the cluster form for B * nkv <= n segments (default 16, 0 = off)
+static int g_max_cluster = [] {
+  const char* e = getenv("TPS_ATTN_MAX_CLUSTER");
+  return e ? atoi(e) : 16;
+}();
+
 int attn_splits(int B, int nkv, int max_pages) {
   // page-balanced when the (row, kv head) segments give enough parallel work, and for a
   // single local KV head (TP-sharded GQA tail: measured faster than split + combine)
+  if (B * nkv <= g_max_cluster) return -1;  // tail: one CTA cluster per (row, kv head)
   if ((B * nkv >= g_min_bal || nkv == 1) && B <= kBalMaxRows) return 0;
   return attn_fixed_splits(B, nkv, max_pages);
 }
@@ -407,8 +565,27 @@ int paged_attention(const void* q, const void* k_cache, const void* v_cache, con
   const auto* bias = reinterpret_cast<const __nv_bfloat16*>(qkv_bias);
   const int G = nq / nkv;
   TPS_CHECK_ARG(G <= 16, "paged_attention: at most 16 query heads per KV head");
-  TPS_CHECK_ARG(nsplit >= 0 && nsplit <= kMaxAttnSplits, "paged_attention: 0 <= nsplit <= 128");
+  TPS_CHECK_ARG(nsplit >= -1 && nsplit <= kMaxAttnSplits, "paged_attention: -1 <= nsplit <= 128");
   TPS_CHECK_ARG(nsplit > 0 || qkv.n == 0, "paged_attention: the fused QKV form needs an explicit split count");
+  TPS_CHECK_ARG(nsplit >= 0 || B * nkv <= 65535, "paged_attention: too many segments for the cluster form");
+  if (nsplit < 0) {
+    // cluster kernel (tail batches): 16 CTAs per segment when there are few segments
+    const int cl = (B * nkv <= 8) ? 16 : 8;
+    const float scale = 1.4426950408889634f / sqrtf((float)D);
+    const auto* qq = reinterpret_cast<const __nv_bfloat16*>(q);
+    const auto* kk = reinterpret_cast<const __nv_bfloat16*>(k_cache);
+    const auto* vv = reinterpret_cast<const __nv_bfloat16*>(v_cache);
+    auto* oo = reinterpret_cast<__nv_bfloat16*>(out);
+    if (D == 128)
+      return launch_kcs(paged_attn_cluster_kernel<128>, dim3(cl, B * nkv), dim3(kAttnThreads), cl,
+                        attn_smem<128>(), st, true, qq, kk, vv, row_slot, pos_by_slot, row_pos, page_table,
+                        max_pages, nq, nkv, G, scale, oo);
+    if (D == 64)
+      return launch_kcs(paged_attn_cluster_kernel<64>, dim3(cl, B * nkv), dim3(kAttnThreads), cl,
+                        attn_smem<64>(), st, true, qq, kk, vv, row_slot, pos_by_slot, row_pos, page_table,
+                        max_pages, nq, nkv, G, scale, oo);
+    return fail(kInvalid, "paged_attention: head_dim must be 64 or 128");
+  }
   if (nsplit == 0)
     return paged_attention_balanced(q, k_cache, v_cache, row_slot, pos_by_slot, row_pos, page_table, max_pages, B,
                                     nq, nkv, D, part_m, part_l, part_o, merge_ctr, out, st);

@@ -145,12 +145,12 @@ int launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaS
 
 // launch_k with a thread-block cluster of cluster_x CTAs along x (DSMEM reductions).
 template <typename... KArgs, typename... Args>
-int launch_kc(void (*kernel)(KArgs...), dim3 grid, dim3 block, int cluster_x, cudaStream_t st, bool pdl,
-              Args... args) {
+int launch_kcs(void (*kernel)(KArgs...), dim3 grid, dim3 block, int cluster_x, size_t smem, cudaStream_t st,
+               bool pdl, Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -164,6 +164,12 @@ int launch_kc(void (*kernel)(KArgs...), dim3 grid, dim3 block, int cluster_x, cu
   cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
   if (e != cudaSuccess) return fail(kCuda, std::string("launch: ") + cudaGetErrorString(e));
   return kOk;
+}
+
+template <typename... KArgs, typename... Args>
+int launch_kc(void (*kernel)(KArgs...), dim3 grid, dim3 block, int cluster_x, cudaStream_t st, bool pdl,
+              Args... args) {
+  return launch_kcs(kernel, grid, block, cluster_x, 0, st, pdl, args...);
 }
 
 }  // namespace tps

@@ -214,9 +214,10 @@ class InferExecutor:
         return units >= 120
 
     def _attn_splits(self, B: int, fused: bool) -> int:
-        """tps_attn_splits policy (0 = page-balanced); the fused-RoPE form needs a fixed count."""
+        """tps_attn_splits policy (-1 = cluster per segment, 0 = page-balanced, n = fixed splits);
+        the fused-RoPE form needs a fixed count."""
         s = nat.lib().tps_attn_splits(B, self.nkv, self.slots.max_pages)
-        return max(1, min(32, 2 * 148 // (B * self.nkv))) if (fused and s == 0) else s
+        return max(1, min(32, 2 * 148 // (B * self.nkv))) if (fused and s <= 0) else s
 
     def _linear(self, st, stats, w: torch.Tensor, x: torch.Tensor, B: int) -> tuple[int, int, int]:
         """Projection into the split-K workspace; returns the strided source (base, n, stride)."""

@@ -82,7 +82,8 @@ def _ref_attention(q, kc, vc, page_table, pos, G):
     (128, 7, 1, [1, 64, 65, 300]), (128, 28, 4, [5000, 17]), (64, 4, 2, [130, 1]),
     (128, 4, 1, [2049]), (128, 16, 1, [100, 1000])])
 def test_paged_attention_matches_fp32(D, nq, nkv, ctxs):
-    """Page-balanced schedule (nsplit 0) and fixed split counts (in-kernel and combine merge)."""
+    """Cluster form (nsplit -1, DSMEM merge), page-balanced schedule (nsplit 0) and fixed split
+    counts (in-kernel and combine merge)."""
     torch.manual_seed(D + nq + len(ctxs))
     B = len(ctxs)
     max_pages = max((c + 63) // 64 for c in ctxs) + 1
@@ -96,7 +97,7 @@ def test_paged_attention_matches_fp32(D, nq, nkv, ctxs):
     q = torch.randn(B, nq, D, device="cuda").bfloat16()
     lib = nat.lib()
     ctr = torch.zeros(B * nkv, dtype=torch.int32, device="cuda")
-    for nsplit in (0, 1, lib.tps_attn_splits(B, nkv, max_pages), 7):
+    for nsplit in (-1, 0, 1, lib.tps_attn_splits(B, nkv, max_pages), 7):
         ws = lib.tps_attn_workspace(B, nq, D, nsplit)
         pm = torch.empty(ws // D, device="cuda")
         pl = torch.empty_like(pm)
@@ -303,3 +304,4 @@ def test_ll_push_and_norm(b, tp, splits):
     assert (resid - ref_resid).abs().max().item() < 2e-3
     assert (out.float() - ref).abs().max().item() < 3e-2
     assert ctr.item() == 5 + tp  # the phase counter advanced as if the counter protocol had run
+
