@@ -59,6 +59,7 @@ def parse():
     ap.add_argument("--no-switch", action="store_true")
     ap.add_argument("--static-tps", default="1", help="N>1: also time the stage at these fixed TP degrees")
     ap.add_argument("--tp-list", default="", help="Algorithm 1 candidates (default: 1 and N, BASELINE config 2)")
+    ap.add_argument("--initial-tp", type=int, default=1, help="starting TP degree (config 4 starts at TP2)")
     ap.add_argument("--cpu-threads", type=int, default=0)
     return ap.parse_args()
 
@@ -84,11 +85,15 @@ def build_spec(args, gpus):
     cluster = dataclasses.replace(cfg.cluster, gpus_per_node=gpus)
     # BASELINE config 2 switches TP1/DP8 -> TP8/DP1: candidates {1, N}; --tp-list widens it
     # (config 3's multi-stage TP1 -> 2 -> 4 -> 8)
-    want = [int(x) for x in getattr(args, "tp_list", "").split(",") if x] or sorted({1, gpus})
+    want = [int(x) for x in getattr(args, "tp_list", "").split(",") if x] or \
+        sorted({int(getattr(args, "initial_tp", 1) or 1), gpus})
     ctl = ControllerParams(tp_list=tuple(t for t in want if gpus % t == 0 and _tp_ok(geom, t)),
                            eval_interval=cfg.controller.eval_interval, chunk_steps=cfg.controller.chunk_steps)
+    init_tp = int(getattr(args, "initial_tp", 1) or 1)
+    if gpus % init_tp:
+        init_tp = 1
     spec = build_scenario(cfg, prompt_len=args.prompt_len, global_batch=args.per_gpu_batch * gpus,
-                          l_max=args.l_max, initial_tp=1, seed=args.seed, controller=ctl)
+                          l_max=args.l_max, initial_tp=init_tp, seed=args.seed, controller=ctl)
     spec = dataclasses.replace(spec, model=geom.model_spec(), cluster=cluster,
                                distribution=LengthDistribution.default().scaled_to_cap(args.l_max))
     return spec, geom
@@ -260,10 +265,10 @@ def main():
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": f"c2-weak: {args.model}-shaped random-init, {args.per_gpu_batch} samples/GPU, "
                                f"prompt {args.prompt_len}, long-tail lengths capped at {args.l_max} (seed "
-                               f"{args.seed}), start TP1/DP{gpus}, Algorithm 1 over tp_list "
+                               f"{args.seed}), start TP{spec.initial_tp}/DP{gpus // spec.initial_tp}, Algorithm 1 over tp_list "
                                f"{list(spec.controller.tp_list)}",
                    "model": args.model, "global_batch": spec.global_batch, "seq_len": args.prompt_len + args.l_max,
-                   "parallelism": f"tp1->adaptive,dp{gpus}", "l2": "inputs > L2 (15.2 GB weights streamed per step)",
+                   "parallelism": f"tp{spec.initial_tp}->adaptive,dp{gpus // spec.initial_tp}", "l2": "inputs > L2 (15.2 GB weights streamed per step)",
                    "step": "one generation stage (prefill via decode path + decode to last sample)",
                    "predictor": "B200-measured profile table" if table is not None else "analytic b200.cfg"},
         "tokens_generated": rep.tokens_generated,

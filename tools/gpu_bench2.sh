@@ -1,0 +1,2 @@
+mkdir -p gpurun_out
+timeout 900 python bench.py > gpurun_out/bench.log 2>&1; tail -c 3500 gpurun_out/bench.log
