@@ -113,6 +113,14 @@ PRESETS: dict[str, DecoderGeometry] = {
     "mini-qwen": DecoderGeometry("mini-qwen", num_layers=2, hidden=512, n_q=14, n_kv=2,
                                  head_dim=128, ffn=1024, vocab=8192, qkv_bias=True,
                                  rope_theta=1000000.0),
+    # small geometries with config 3's and config 4's head structure: Llama-3 (G=4, 8 KV
+    # heads, no QKV bias: TP up to 8 without KV replication) and Qwen2.5-32B (G=5, 8 KV heads)
+    "mini-llama": DecoderGeometry("mini-llama", num_layers=2, hidden=1024, n_q=8 * 4, n_kv=8,
+                                  head_dim=32 * 4, ffn=2048, vocab=8192, qkv_bias=False,
+                                  rope_theta=500000.0, rms_eps=1e-5),
+    "mini-qwen32": DecoderGeometry("mini-qwen32", num_layers=2, hidden=640, n_q=40, n_kv=8,
+                                   head_dim=128, ffn=1536, vocab=8192, qkv_bias=True,
+                                   rope_theta=1000000.0),
 }
 
 

@@ -88,6 +88,14 @@ def test_mini_qwen_gqa_decode_matches_oracle(tp):
     run_parity("mini-qwen", tp, PROMPTS, gen=10)
 
 
+@pytest.mark.parametrize("name,tp", [("mini-llama", 1), ("mini-llama", 4), ("mini-llama", 8),
+                                     ("mini-qwen32", 2), ("mini-qwen32", 8)])
+def test_config3_config4_head_layouts_match_oracle(name, tp):
+    # Llama-3 (G=4, 8 KV heads, no bias) up to TP8 without KV replication; Qwen2.5-32B
+    # (G=5, 8 KV heads) -- the head partitions of BASELINE configs 3 and 4
+    run_parity(name, tp, PROMPTS, gen=8)
+
+
 def test_graph_replay_matches_eager():
     geom = geometry("tiny")
     outs = []

@@ -37,7 +37,9 @@ def test_library_loads_and_reports_version():
     assert b"sm_100a" in lib.tps_version()
     # host-only helpers work without a GPU
     assert lib.tps_linear_splits(4608, 3584, 64) >= 1
-    assert 1 <= lib.tps_attn_splits(1, 4, 136) <= 32
+    assert lib.tps_attn_splits(1, 4, 136) == -1       # tail: one CTA cluster per (row, kv head)
+    assert lib.tps_attn_splits(64, 4, 136) == 0       # page-balanced schedule
+    assert 1 <= lib.tps_attn_splits(6, 4, 136) <= 32  # fixed split-KV
 
 
 def test_status_codes_map_to_tpshift_errors():
