@@ -120,7 +120,13 @@ class B200Backend:
         self._keep: list = []
         self._barrier_epoch = 0
         self._bar = None
+        # built layouts (ranks + runners with their captured graphs) per TP degree, kept for the
+        # life of the backend like the communicator pool: a later switch to the same degree,
+        # or the next stage, reuses the buffers and graphs instead of allocating and capturing
+        self._layouts: dict[int, dict] = {}
         self._build_layout(self.layout, weights_seed=seed)
+        self._layouts[self.layout.tp] = {"ranks": self.ranks, "runners": self.runners,
+                                         "cap": {g: self.max_batch for g in self.local_groups()}}
 
     # ------------------------------------------------------------- layout ---
     def stream(self, r: int):
@@ -156,14 +162,34 @@ class B200Backend:
         ex = InferExecutor(self.geom, sh, w, kv, st, slots, dev, comm=comm, prefill_rows=pf)
         return RankState(w, kv, st, ex, comm)
 
+    def _use_layout(self, lay: Layout, per_group: dict[int, int] | None) -> bool:
+        """Make `lay` current: reuse the cached ranks/runners of this TP degree when every
+        local group's slot capacity suffices (slot tables and page pools reset), else build
+        it (new buffers, weights filled by the switch's pulls) and cache it. True if built."""
+        need = {g: max(1, self.max_batch if per_group is None else per_group.get(g, 0))
+                for g in self.local_groups(lay)}
+        c = self._layouts.get(lay.tp)
+        if c is not None and all(c["cap"].get(g, 0) >= n for g, n in need.items()):
+            for rs in c["ranks"].values():
+                rs.slots.reset()
+                rs.kv.reset()
+            self.ranks, self.runners = c["ranks"], c["runners"]
+            return False
+        cap = {g: max(n, c["cap"].get(g, 0) if c else 0) for g, n in need.items()}
+        self._build_layout(lay, weights_seed=None, per_group=cap)
+        self._layouts[lay.tp] = {"ranks": self.ranks, "runners": self.runners, "cap": cap}
+        return True
+
     def reset(self, seed: int) -> None:
         """Return to the initial layout with no samples (between repeated stages)."""
         init = Layout(self.spec.initial_tp, self.world.gpus)
         rebuild = bool(self.epoch) or self.layout != init
         self.epoch = 0
         if rebuild:
+            # the cached initial layout holds the canonical shards (a switch back to it pulls
+            # bit-identical bytes), so only its slot tables and pages are reset
             self.layout = init
-            self._build_layout(init, weights_seed=seed)
+            self._use_layout(init, None)
             self.capture_all()
         self.timeline = {}
         self.switches = []
@@ -308,8 +334,7 @@ class B200Backend:
         tb = time.perf_counter()
         self.epoch += 1
         self.layout = new
-        self._build_layout(new, weights_seed=None, per_group={g: len(m) for g, m in enumerate(merged)},
-                           prefill=recompute)
+        self._use_layout(new, {g: len(m) for g, m in enumerate(merged)})
         stats = dict(nv=0, loc=0, kv=0, w=0)
         t_build = time.perf_counter() - tb
         t_plan = 0.0
@@ -388,7 +413,7 @@ class B200Backend:
                                           host_capture_s=time.perf_counter() - tc,
                                           state_method=RECOMPUTE if recompute else MIGRATE,
                                           host_build_s=t_build))
-        self._keep.append(old_ranks)  # released after the stage (stream-ordered frees would also do)
+        self._keep.append(old_ranks)  # (cached layouts are reused, never freed mid-stage)
 
     def _copy(self, items: np.ndarray, st) -> None:
         if len(items) == 0:

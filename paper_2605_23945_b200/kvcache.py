@@ -58,6 +58,10 @@ class KVPool:
     def release(self, pages) -> None:
         self._free.extend(reversed(list(pages)))
 
+    def reset(self) -> None:
+        """Every page free again (a cached layout being reused)."""
+        self._free = list(range(self.num_pages - 1, -1, -1))
+
 
 def pages_for(tokens: int) -> int:
     return (tokens + PAGE - 1) // PAGE
@@ -89,3 +93,9 @@ class SlotTable:
         self.sample_of.pop(slot, None)
         self.pages.pop(slot, None)
         self._free.append(slot)
+
+    def reset(self) -> None:
+        """Every slot free again (a cached layout being reused)."""
+        self._free = list(range(self.num_slots - 1, -1, -1))
+        self.pages = {}
+        self.sample_of = {}
