@@ -187,6 +187,17 @@ int tps_argmax_stage1(const float* src, int nsrc, int64_t src_stride, int B, int
                       int nchunk, void* cand, uint64_t* const* sig_ctrs, int nsig, unsigned int* done,
                       void* stream);
 
+/* Stochastic form of tps_argmax_stage1 (the non-greedy sampler state of a sample is its
+ * key seeds[row_slot[b]] and its position): candidates are the argmax over the rank's
+ * vocab slice of logit / temperature + Gumbel(u), u from Philox4x32-10 with counter
+ * (pos + 1, global vocab index, 0, 0) and the 64-bit key -- Gumbel-max, an exact draw
+ * from softmax(logit / temperature), identical for any TP degree
+ * (oracle/sampler_ref.py). pos = row_pos[b] when given, else pos_by_slot[slot]. */
+int tps_sample_stage1(const float* src, int nsrc, int64_t src_stride, int B, int V, int vocab_offset, int nchunk,
+                      void* cand, uint64_t* const* sig_ctrs, int nsig, unsigned int* done, const uint64_t* seeds,
+                      const int* row_slot, const int* pos_by_slot, const int* row_pos, float temperature,
+                      void* stream);
+
 /* Stage 2: reduce candidates of all TP ranks (list = rank order), append the
  * token to history[slot][pos+1] unless pos+1 is still inside the prompt
  * (prompt_len may be NULL), advance pos_by_slot[slot]. out_tok may be NULL. */

@@ -53,6 +53,8 @@ SIGNATURES = {
                                    _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp, _vp]),
     "tps_silu_mul": (_i32, [_vp, _i32, _i64, _i32, _i32, _vp, _i32, _vp]),
     "tps_argmax_stage1": (_i32, [_vp, _i32, _i64, _i32, _i32, _i32, _i32, _vp, _pp, _i32, _vp, _vp]),
+    "tps_sample_stage1": (_i32, [_vp, _i32, _i64, _i32, _i32, _i32, _i32, _vp, _pp, _i32, _vp, _vp, _vp, _vp, _vp,
+                                  _f32, _vp]),
     "tps_argmax_finalize": (_i32, [_pp, _i32, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _i32, _vp, _vp]),
     "tps_epoch_advance": (_i32, [_vp, _vp]),
     "tps_sum_partials": (_i32, [_vp, _i32, _i64, _i64, _vp, _vp]),

@@ -41,6 +41,7 @@ from .shards import RankWeights
 from .switch_executor import (KVSource, KVTarget, Layout, Pieces, cached_weight_pulls, check, nvlink_bytes,
                               plan_history_pulls, plan_kv_pulls, to_items, verify_cover)
 from .switchcost import MIGRATE, RECOMPUTE, SwitchCostBreakdown
+from .workload import as_int64, sampler_seed
 
 
 PREFILL_ROWS = 512  # (sample, prompt position) rows per chunked-prefill step
@@ -79,8 +80,9 @@ class B200Backend:
 
     def __init__(self, spec: ScenarioSpec, geom: DecoderGeometry, world: World, seed: int = 0,
                  use_graphs: bool = True, copy_mode: int = 0, prompts: np.ndarray | None = None,
-                 host_io: bool = False, state_method: str | None = None):
+                 host_io: bool = False, state_method: str | None = None, temperature: float = 0.0):
         self.spec, self.geom, self.world = spec, geom, world
+        self.temperature = temperature  # 0: greedy; > 0: Gumbel-max with per-sample Philox keys
         # None: each switch handles KV state as Algorithm 1 priced it (migrate or
         # recompute); MIGRATE / RECOMPUTE force one method (measurement, tests)
         self.state_method = state_method
@@ -160,6 +162,7 @@ class B200Backend:
         st = SlotTable(slots, self.max_len, dev)
         pf = slots * max(1, PREFILL_ROWS // slots) if prefill else 0
         ex = InferExecutor(self.geom, sh, w, kv, st, slots, dev, comm=comm, prefill_rows=pf)
+        ex.temperature = self.temperature
         return RankState(w, kv, st, ex, comm)
 
     def _use_layout(self, lay: Layout, per_group: dict[int, int] | None) -> bool:
@@ -238,7 +241,7 @@ class B200Backend:
             else:
                 prompt = self.prompts_host[s.id].to(grp[0].slots.device, non_blocking=True)
                 self.h2d_bytes += prompt.numel() * 4
-            slots.append(admit(grp, s.id, prompt, max_ctx=self.max_len))
+            slots.append(admit(grp, s.id, prompt, max_ctx=self.max_len, seed=sampler_seed(self.spec.seed, s.id)))
             self.slot_of[s.id] = slots[-1]
         runner = self.runners[g]
         r = self.first_local(g)
@@ -348,7 +351,7 @@ class B200Backend:
             stats["loc"] += loc
             stats["w"] += nv + loc
             mine = merged[new.group_of(r)] if new.group_of(r) < len(merged) else []
-            tgts, srcs, kvlen, hlen, pos_vals, plen, slot_list = [], [], [], [], [], [], []
+            tgts, srcs, kvlen, hlen, pos_vals, plen, slot_list, seeds = [], [], [], [], [], [], [], []
             for s in mine:
                 slot = rs.slots.alloc(s.id)
                 pages = rs.kv.alloc(pages_for(self.max_len))
@@ -361,6 +364,7 @@ class B200Backend:
                 hlen.append(s.context_len)
                 pos_vals.append(pos)
                 plen.append(s.prompt_len)
+                seeds.append(as_int64(sampler_seed(self.spec.seed, s.id)))  # the sampler state's key
                 slot_list.append(slot)
                 h2d(rs.slots.page_table[slot, :len(pages)], pages)
             if slot_list:
@@ -369,6 +373,8 @@ class B200Backend:
                                          .to(rs.slots.device, non_blocking=True))
                 rs.executor.prompt_len.index_copy_(0, idx, torch.tensor(plen, dtype=torch.int32).pin_memory()
                                                    .to(rs.slots.device, non_blocking=True))
+                rs.slots.seed.index_copy_(0, idx, torch.tensor(seeds, dtype=torch.int64).pin_memory()
+                                          .to(rs.slots.device, non_blocking=True))
             kp = Pieces()
             by_pool: dict[int, list[int]] = {}
             for i, s in enumerate(srcs):
@@ -541,14 +547,15 @@ class GlobalCoordinator:
 
     def __init__(self, spec: ScenarioSpec, geom: DecoderGeometry, world: World | None = None, seed: int = 0,
                  table=None, use_graphs: bool = True, copy_mode: int = 0, host_io: bool = False,
-                 state_method: str | None = None):
+                 state_method: str | None = None, temperature: float = 0.0):
         self.spec = spec
         self.geom = geom
         self.world = world or World.virtual(spec.cluster.gpus_per_node)
         self.table = table
         self.seed = seed
         self.backend = B200Backend(spec, geom, self.world, seed=seed, use_graphs=use_graphs,
-                                   copy_mode=copy_mode, host_io=host_io, state_method=state_method)
+                                   copy_mode=copy_mode, host_io=host_io, state_method=state_method,
+                                   temperature=temperature)
         self.setup_capture_s = self.backend.capture_all()
         self.runs = 0
         self.last_wall_s = 0.0

@@ -35,7 +35,8 @@ int reduce_push(const Src&, const DstList&, long long, const SignalSpec&, cudaSt
 int qkv_rope_append(const Src&, const void*, const int*, const int*, const int*, const int*, int, const float*,
                     const float*, int, int, int, int, int, void*, void*, void*, cudaStream_t);
 int silu_mul(const Src&, int, int, void*, int, cudaStream_t);
-int argmax_stage1(const Src&, int, int, int, int, void*, const SignalSpec&, cudaStream_t);
+int argmax_stage1(const Src&, int, int, int, int, void*, const SignalSpec&, cudaStream_t,
+                  const SamplerSpec* smp = nullptr);
 int argmax_finalize(const CandList&, int, const WaitSpec&, int, const int*, int*, const int*, int*, int, int*,
                     cudaStream_t);
 int epoch_advance(uint64_t*, cudaStream_t);
@@ -254,6 +255,22 @@ int tps_argmax_stage1(const float* src, int nsrc, int64_t src_stride, int B, int
   rc = make_sig(sig_ctrs, nsig, done, &sg);
   if (rc) return rc;
   return argmax_stage1(s, B, V, vocab_offset, nchunk, cand, sg, S(stream));
+}
+
+int tps_sample_stage1(const float* src, int nsrc, int64_t src_stride, int B, int V, int vocab_offset, int nchunk,
+                      void* cand, uint64_t* const* sig_ctrs, int nsig, unsigned int* done, const uint64_t* seeds,
+                      const int* row_slot, const int* pos_by_slot, const int* row_pos, float temperature,
+                      void* stream) {
+  TPS_CHECK_ARG(seeds && row_slot && (pos_by_slot || row_pos), "sample_stage1: null sampler state");
+  TPS_CHECK_ARG(temperature > 0.f, "sample_stage1: temperature must be > 0 (greedy: tps_argmax_stage1)");
+  Src s;
+  int rc = make_src(src, nsrc, src_stride, &s);
+  if (rc) return rc;
+  SignalSpec sg;
+  rc = make_sig(sig_ctrs, nsig, done, &sg);
+  if (rc) return rc;
+  SamplerSpec smp{seeds, row_slot, pos_by_slot, row_pos, 1.f / temperature};
+  return argmax_stage1(s, B, V, vocab_offset, nchunk, cand, sg, S(stream), &smp);
 }
 
 int tps_argmax_finalize(const void* const* cands, int ncand, int nchunk, const tps_wait* wait, int B,

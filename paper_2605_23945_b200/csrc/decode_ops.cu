@@ -481,7 +481,7 @@ __device__ __forceinline__ void cand_merge(float& v, int& i, float v2, int i2) {
 
 __global__ void __launch_bounds__(kArgmaxThreads) argmax_stage1_kernel(Src src, int B, int V, int vocab_offset,
                                                                       int nchunk, ArgmaxCand* __restrict__ cand,
-                                                                      SignalSpec sig) {
+                                                                      SignalSpec sig, SamplerSpec smp) {
   __shared__ float sv[kArgmaxThreads / 32];
   __shared__ int si[kArgmaxThreads / 32];
   pdl_launch_dependents();  // dependents may launch now: they read our outputs only after their own wait
@@ -493,7 +493,19 @@ __global__ void __launch_bounds__(kArgmaxThreads) argmax_stage1_kernel(Src src, 
   const int lo = c * per, hi = min(V, lo + per);
   float best = -INFINITY;
   int bidx = 0x7fffffff;
-  if ((V & 3) == 0) {
+  if (smp.seeds != nullptr) {
+    // stochastic: logit / T + Gumbel(philox(ctr = (pos + 1, global vocab index), key = seed))
+    const int slot = smp.row_slot[b];
+    const uint64_t key = slot >= 0 ? smp.seeds[slot] : 0ull;
+    const uint32_t pnext =
+        slot >= 0 ? (uint32_t)((smp.row_pos ? smp.row_pos[b] : smp.pos_by_slot[slot]) + 1) : 0u;
+    const uint2 k = make_uint2((uint32_t)key, (uint32_t)(key >> 32));
+    for (int j = lo + threadIdx.x; j < hi; j += kArgmaxThreads) {
+      const int gv = j + vocab_offset;
+      const uint4 r = philox4x32_10(make_uint4(pnext, (uint32_t)gv, 0u, 0u), k);
+      cand_merge(best, bidx, src_sum(src, (long long)b * V + j) * smp.inv_temp + gumbel_of(r.x), gv);
+    }
+  } else if ((V & 3) == 0) {
     for (int j = lo + 4 * threadIdx.x; j < hi; j += 4 * kArgmaxThreads) {
       const float4 v = src_sum4(src, ((long long)b * V + j) / 4);
       cand_merge(best, bidx, v.x, j + vocab_offset);
@@ -663,10 +675,11 @@ int silu_mul(const Src& src, int B, int F, void* out, int ldo, cudaStream_t st) 
 }
 
 int argmax_stage1(const Src& src, int B, int V, int vocab_offset, int nchunk, void* cand, const SignalSpec& sig,
-                  cudaStream_t st) {
+                  cudaStream_t st, const SamplerSpec* smp) {
   TPS_CHECK_ARG(B > 0 && V > 0 && nchunk > 0, "argmax_stage1: bad shape");
+  SamplerSpec greedy{nullptr, nullptr, nullptr, nullptr, 1.f};
   return launch_k(argmax_stage1_kernel, dim3(B, nchunk), dim3(kArgmaxThreads), 0, st, true, src, B, V,
-                  vocab_offset, nchunk, reinterpret_cast<ArgmaxCand*>(cand), sig);
+                  vocab_offset, nchunk, reinterpret_cast<ArgmaxCand*>(cand), sig, smp ? *smp : greedy);
 }
 
 int argmax_finalize(const CandList& cands, int nchunk, const WaitSpec& wait, int B, const int* row_slot,

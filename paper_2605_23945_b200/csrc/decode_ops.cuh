@@ -45,6 +45,34 @@ struct DstList {
   int n;
 };
 
+// Stochastic sampling (Gumbel-max with counter-based Philox4x32-10): a sample's sampler
+// state is its key seeds[slot] and the position being sampled, so it migrates with the
+// position (oracle/sampler_ref.py restates the arithmetic). seeds == NULL: greedy.
+struct SamplerSpec {
+  const uint64_t* seeds;
+  const int* row_slot;
+  const int* pos_by_slot;
+  const int* row_pos;
+  float inv_temp;
+};
+
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    k.x += 0x9E3779B9u;
+    k.y += 0xBB67AE85u;
+  }
+  return c;
+}
+
+__device__ __forceinline__ float gumbel_of(uint32_t x) {
+  const float u = ((float)(x >> 8) + 0.5f) * (1.0f / 16777216.0f);
+  return -logf(-logf(u));
+}
+
 struct ArgmaxCand {
   float val;
   int idx;

@@ -140,6 +140,8 @@ class InferExecutor:
         self.fuse_rope = False
         # launch kinds left out of the step program (timing probes only: results are garbage)
         self.skip: frozenset = frozenset()
+        # 0: greedy; > 0: Gumbel-max sampling at this temperature with the slots' Philox keys
+        self.temperature = 0.0
         self.device = torch.device(device)
         self.comm = comm
         self.tp = shard.tp
@@ -323,17 +325,15 @@ class InferExecutor:
         self._last_lm_srcs = (srcs, B)
         nch = argmax_chunks(B)
         if cm is None:
-            nat.check(lib.tps_argmax_stage1(*srcs, B, self.V, self.shard.vocab[0], nch,
-                                            self.local_cand.data_ptr(), None, 0, None, st), "tps_argmax_stage1")
+            self._stage1(srcs, B, nch, self.local_cand.data_ptr(), None, 0, None, rs, pos, st)
             stats.add("argmax_stage1")
             cands = [self.local_cand.data_ptr()]
             wait = None
         else:
             ph = 2 * L
             sigs = [p + ph * 8 for p in cm.peer_ctr]
-            nat.check(lib.tps_argmax_stage1(*srcs, B, self.V, self.shard.vocab[0], nch,
-                                            cm.cand.data_ptr(), self._arr(sigs), len(sigs),
-                                            cm.done.data_ptr() + ph * 4, st), "tps_argmax_stage1")
+            self._stage1(srcs, B, nch, cm.cand.data_ptr(), self._arr(sigs), len(sigs), cm.done.data_ptr() + ph * 4,
+                         rs, pos, st)
             stats.add("argmax_stage1")
             yield
             cands = list(cm.peer_cand)
@@ -345,6 +345,17 @@ class InferExecutor:
         if cm is not None:
             nat.check(lib.tps_epoch_advance(cm.epoch.data_ptr(), st), "tps_epoch_advance")
             stats.add("epoch_advance")
+
+    def _stage1(self, srcs, B, nch, cand, sigs, nsig, done, rs, pos, st):
+        """Per-rank candidates over the vocab slice: greedy argmax, or Gumbel-max sampling."""
+        lib = nat.lib()
+        if self.temperature > 0:
+            nat.check(lib.tps_sample_stage1(*srcs, B, self.V, self.shard.vocab[0], nch, cand, sigs, nsig, done,
+                                            self.slots.seed.data_ptr(), rs, pos, None,
+                                            ctypes.c_float(self.temperature), st), "tps_sample_stage1")
+        else:
+            nat.check(lib.tps_argmax_stage1(*srcs, B, self.V, self.shard.vocab[0], nch, cand, sigs, nsig, done, st),
+                      "tps_argmax_stage1")
 
     def fused_splits(self, fam: str, B: int) -> int:
         """Split-K count of a fused row-parallel projection: the same on every rank of the

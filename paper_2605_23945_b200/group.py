@@ -19,6 +19,7 @@ from .executor import GroupComm, GroupRunner, InferExecutor
 from .kvcache import KVPool, SlotTable, pages_for
 from .models import DecoderGeometry, rank_shard
 from .shards import RankWeights
+from .workload import as_int64
 
 
 @dataclass
@@ -71,7 +72,7 @@ def build_group(geom: DecoderGeometry, tp: int, max_batch: int, num_slots: int, 
 
 
 def admit(ranks: list[RankState], sample_id: int, prompt: list[int], max_ctx: int,
-          slot: int | None = None) -> int:
+          slot: int | None = None, seed: int = 0) -> int:
     """Place a sample on every rank of its group: slot, reserved pages, prompt tokens.
 
     Pages are reserved for max_ctx tokens (prompt + l_max), the reference's
@@ -94,6 +95,7 @@ def admit(ranks: list[RankState], sample_id: int, prompt: list[int], max_ctx: in
         h2d(r.slots.page_table[s, :n_pages], pages)
         r.slots.history[s, :prompt.numel()].copy_(prompt, non_blocking=True)
         r.slots.pos[s] = 0
+        r.slots.seed[s] = as_int64(seed)
         r.executor.prompt_len[s] = prompt.numel()
     return got
 

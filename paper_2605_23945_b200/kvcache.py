@@ -78,6 +78,8 @@ class SlotTable:
         self.history = torch.zeros((num_slots, max_len), dtype=torch.int32, device=self.device)
         self.pos = torch.zeros(num_slots, dtype=torch.int32, device=self.device)
         self.page_table = torch.zeros((num_slots, self.max_pages), dtype=torch.int32, device=self.device)
+        # non-greedy sampler key per slot (uint64 bits; the rest of the sampler state is the position)
+        self.seed = torch.zeros(num_slots, dtype=torch.int64, device=self.device)
         self._free = list(range(num_slots - 1, -1, -1))
         self.pages: dict[int, list[int]] = {}
         self.sample_of: dict[int, int] = {}

@@ -16,6 +16,7 @@ import pytest
 import torch
 
 from oracle.decoder_ref import OracleDecoder
+from oracle.sampler_ref import sample_scores
 from paper_2605_23945_b200.cache_manager import World
 from paper_2605_23945_b200.cluster import ClusterSpec
 from paper_2605_23945_b200.controller import ControllerParams
@@ -25,7 +26,7 @@ from paper_2605_23945_b200.latency import OracleCalibration
 from paper_2605_23945_b200.models import geometry, layer_families
 from paper_2605_23945_b200.shards import full_tensor
 from paper_2605_23945_b200.switchcost import GraphCaptureCalibration, SwitchCalibration
-from paper_2605_23945_b200.workload import LengthDistribution
+from paper_2605_23945_b200.workload import LengthDistribution, sampler_seed
 
 pytestmark = pytest.mark.gpu
 
@@ -47,7 +48,7 @@ def tiny_spec(geom, mode="adaptive", gpus=4, batch=12, l_max=48, prompt=8, initi
                         initial_tp=initial_tp, seed=3, prep_time=0.0, train_time=0.0, mode=mode)
 
 
-def oracle_check(geom, seed, coord, spec):
+def oracle_check(geom, seed, coord, spec, temperature=0.0):
     W = {}
     for fam in ("embed", "ln_f", "lm_head"):
         W[(-1, fam)] = full_tensor(geom, fam, -1, seed, "cuda").float().cpu()
@@ -70,8 +71,10 @@ def oracle_check(geom, seed, coord, spec):
         for t in range(len(toks) - 1):
             lg = orc.step([toks[t]], [t], [0])[0]
             if t >= spec.prompt_len - 1:
+                if temperature > 0:  # the sample's key follows it across switches
+                    lg = torch.from_numpy(sample_scores(lg.numpy(), sampler_seed(spec.seed, i), t + 1, temperature))
                 top2 = lg.topk(2).values
-                if (top2[0] - top2[1]).item() > MARGIN:
+                if (top2[0] - top2[1]).item() > (MARGIN if temperature <= 0 else 2 * 0.05 / temperature):
                     checked += 1
                     agree += int(toks[t + 1] == int(lg.argmax()))
     return checked, agree
@@ -113,6 +116,19 @@ def test_recompute_switch_matches_oracle(name):
     checked, agree = oracle_check(geom, 7, coord, spec)
     assert checked > 50
     assert agree == checked, f"{checked - agree} of {checked} confident tokens disagree with the oracle"
+
+
+def test_stochastic_stage_with_switches_matches_oracle():
+    """Temperature sampling through live switches: each sample's Philox key moves with it,
+    so its draws continue exactly as in the oracle's single-device replay."""
+    geom = geometry("tiny")
+    spec = tiny_spec(geom)
+    coord = GlobalCoordinator(spec, geom, World.virtual(4), seed=7, temperature=0.9)
+    report, _ = coord.run()
+    assert [s for nr in report.node_reports for s in nr["switches"]], "controller never switched"
+    checked, agree = oracle_check(geom, 7, coord, spec, temperature=0.9)
+    assert checked > 50
+    assert agree == checked, f"{checked - agree} of {checked} confident draws disagree with the oracle"
 
 
 def test_static_single_group_matches_adaptive_tokens_before_switch():

@@ -12,9 +12,11 @@ import pytest
 import torch
 
 from oracle.decoder_ref import OracleDecoder
+from oracle.sampler_ref import sample_scores
 from paper_2605_23945_b200.group import admit, build_group, last_logits
 from paper_2605_23945_b200.models import geometry, layer_families
 from paper_2605_23945_b200.shards import full_tensor
+from paper_2605_23945_b200.workload import sampler_seed
 
 pytestmark = pytest.mark.gpu
 
@@ -35,13 +37,16 @@ def oracle_for(geom, seed, tp, max_len):
     return OracleDecoder(geo, W, tp=tp, round_bf16=True, max_len=max_len)
 
 
-def run_parity(name, tp, prompts, gen, use_graph_tail=False):
+def run_parity(name, tp, prompts, gen, use_graph_tail=False, temperature=0.0):
     geom = geometry(name)
     seed = 11
     max_len = 256
     B = len(prompts)
     ranks, runner = build_group(geom, tp, max_batch=max(8, B), num_slots=B + 2, max_len=max_len, seed=seed)
-    slots = [admit(ranks, i, p, max_ctx=len(p) + gen) for i, p in enumerate(prompts)]
+    for r in ranks:
+        r.executor.temperature = temperature
+    keys = [sampler_seed(seed, i) for i in range(B)]
+    slots = [admit(ranks, i, p, max_ctx=len(p) + gen, seed=keys[i]) for i, p in enumerate(prompts)]
     bucket = ranks[0].executor.bucket(B)
     runner.set_rows(bucket, slots)
     Lp = len(prompts[0])
@@ -65,10 +70,16 @@ def run_parity(name, tp, prompts, gen, use_graph_tail=False):
         worst = max(worst, err)
         assert err <= LOGIT_TOL, (t, err)
         if t >= Lp - 1:  # generated token t+1
-            top2 = ref.topk(2, dim=1).values
             for b in range(B):
-                if (top2[b, 0] - top2[b, 1]).item() > MARGIN:
-                    assert hist[b, t + 1].item() == int(ref[b].argmax()), (t, b)
+                if temperature > 0:  # Gumbel-max with the sample's Philox key at position t + 1
+                    sc = torch.from_numpy(sample_scores(ref[b].numpy(), keys[b], t + 1, temperature))
+                else:
+                    sc = ref[b]
+                top2 = sc.topk(2).values
+                # scores carry the logit error / T: require a margin above twice that
+                margin = MARGIN if temperature <= 0 else 2 * LOGIT_TOL / temperature
+                if (top2[0] - top2[1]).item() > margin:
+                    assert hist[b, t + 1].item() == int(sc.argmax()), (t, b)
     for b in range(B):  # prompt untouched
         assert hist[b, :Lp].tolist() == prompts[b]
     return worst
@@ -94,6 +105,14 @@ def test_config3_config4_head_layouts_match_oracle(name, tp):
     # Llama-3 (G=4, 8 KV heads, no bias) up to TP8 without KV replication; Qwen2.5-32B
     # (G=5, 8 KV heads) -- the head partitions of BASELINE configs 3 and 4
     run_parity(name, tp, PROMPTS, gen=8)
+
+
+@pytest.mark.parametrize("name,tp", [("tiny", 1), ("tiny", 2), ("mini-qwen", 4)])
+def test_stochastic_sampling_matches_oracle(name, tp):
+    """Non-greedy decoding: Gumbel-max with per-sample Philox keys, drawn on the vocab-parallel
+    shards, equals the oracle's draw wherever the perturbed scores' top-2 margin exceeds the
+    logit tolerance scaled by 1/T."""
+    run_parity(name, tp, PROMPTS, gen=12, temperature=0.8)
 
 
 def test_graph_replay_matches_eager():
