@@ -1,2 +1,3 @@
 mkdir -p gpurun_out
+timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
 timeout 900 python bench.py > gpurun_out/bench.log 2>&1; tail -c 3500 gpurun_out/bench.log
