@@ -173,22 +173,23 @@ __device__ __forceinline__ bool ll_ok(const ulonglong2& a, const ulonglong2& c, 
          (uint32_t)(c.y >> 32) == want;
 }
 
-// Loads of 8 sources are issued together (one L2 round trip per batch when the data is
+// Loads of NB sources are issued together (one L2 round trip per batch when the data is
 // already there); a source whose tags are not yet current is re-polled on its own.
+template <int NB = 8>
 __device__ __forceinline__ float4 ll_sum4(const uint64_t* base, int n, long long stride, long long off4,
                                           uint32_t want) {
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int i0 = 0; i0 < n; i0 += 8) {
-    ulonglong2 a[8], c[8];
+  for (int i0 = 0; i0 < n; i0 += NB) {
+    ulonglong2 a[NB], c[NB];
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
+    for (int j = 0; j < NB; ++j)
       if (i0 + j < n) {
         const uint64_t* p = base + (long long)(i0 + j) * stride + off4 * 4;
         a[j] = ld_relaxed_sys_v2u64(p);
         c[j] = ld_relaxed_sys_v2u64(p + 2);
       }
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
+    for (int j = 0; j < NB; ++j)
       if (i0 + j < n) {
         if (!ll_ok(a[j], c[j], want)) {
           const uint64_t* p = base + (long long)(i0 + j) * stride + off4 * 4;

@@ -46,7 +46,7 @@ def argmax_chunks(B: int) -> int:
 
 
 FUSE_ROWS = 64     # row-parallel projections push their split partials straight to peers up to this batch
-FUSE_SOURCES = 16  # at most tp x splits partial slots per fused allreduce (one consumer load batch)
+FUSE_SOURCES = 16  # LL slots per parity: tp x splits partials of one fused allreduce (one load batch)
 
 
 class GroupComm:
@@ -359,14 +359,16 @@ class InferExecutor:
 
     def fused_splits(self, fam: str, B: int) -> int:
         """Split-K count of a fused row-parallel projection: the same on every rank of the
-        group (the slots are read as tp x splits partials in one fixed order) and at most
-        FUSE_SOURCES / tp, so the consumer sums every partial in one load batch."""
+        group (the slots are read as tp x splits partials in one fixed order), with at most
+        FUSE_SOURCES partial slots in total (one consumer load batch)."""
         g = self.geom
         if fam == "w_o":
             ks = [rank_shard(g, self.tp, r).n_q * g.head_dim for r in range(self.tp)]
         else:
             ks = [self.F] * self.tp
         s = nat.lib().tps_linear_splits(g.hidden, max(ks), B)
+        # (measured: 32 slots for the long-K down projection -- more CTAs, but a second load
+        # batch in the consumer -- was slower at TP8 B=1..16)
         return max(1, min(FUSE_SOURCES // self.tp, s, min(-(-k // 64) for k in ks)))
 
     def _row_parallel(self, st, stats, phase: int, fam: str, w: torch.Tensor, x: torch.Tensor, B: int,

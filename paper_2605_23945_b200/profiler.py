@@ -236,7 +236,12 @@ def nvlink_adjust(geom, tp: int, batch: int) -> float:
     if tp == 1:
         return 0.0
     from .executor import FUSE_ROWS, FUSE_SOURCES
-    per_row = geom.hidden * 4 * (tp - 1) * (max(1, FUSE_SOURCES // tp) if batch <= FUSE_ROWS else 1)
+    # tail batches: LL pairs (8 B per element) of every split partial (<= FUSE_SOURCES slots
+    # per group); larger batches: the one summed fp32 row per peer (reduce-push)
+    if batch <= FUSE_ROWS:
+        per_row = geom.hidden * 8 * (tp - 1) * max(1, FUSE_SOURCES // tp)
+    else:
+        per_row = geom.hidden * 4 * (tp - 1)
     return 2 * geom.num_layers * (NVLINK_HOP_S + batch * per_row / (NVLINK_GBPS * 1e9))
 
 
