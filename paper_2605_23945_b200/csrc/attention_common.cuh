@@ -5,9 +5,12 @@
 
 namespace tps {
 
+#ifndef ATTN_STAGES
+#define ATTN_STAGES 3
+#endif
 constexpr int kPage = 64;          // tokens per KV page
 constexpr int kAttnThreads = 128;  // 4 warps x 16 tokens of a page
-constexpr int kAttnStages = 3;     // cp.async ring depth (pages)
+constexpr int kAttnStages = ATTN_STAGES;  // cp.async ring depth (pages)
 constexpr int kBalMaxRows = 512;   // rows per launch of the page-balanced schedule
 
 __device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
