@@ -25,6 +25,7 @@ from __future__ import annotations
 
 import argparse
 import dataclasses
+import gc
 import json
 import os
 import statistics
@@ -301,6 +302,7 @@ def main():
             if gpus % tp:
                 continue
             ex = coord = None
+            gc.collect()  # executors / runners / comms form reference cycles
             torch.cuda.empty_cache()
             sspec = dataclasses.replace(spec, mode="static", initial_tp=tp)
             coord = GlobalCoordinator(sspec, geom, world, seed=0, table=table)
@@ -353,6 +355,7 @@ def switch_microbench(args, hbm_peak):
     spec, geom = build_spec(ns, 2)
     spec = dataclasses.replace(spec, initial_tp=1, global_batch=16)
     r = switch_probe(spec, geom, World.virtual(2), 2, 16, 4096, copy_mode=1)
+    gc.collect()
     torch.cuda.empty_cache()
     return {"config": f"c5: {args.model}, virtual TP1/DP2 -> TP2/DP1 on one B200, 16 samples at ctx 4096, "
                       f"TMA bulk copy engine",

@@ -16,6 +16,7 @@ schema that `fit_predictor` turns into the Latency Predictor.
 from __future__ import annotations
 
 import ctypes
+import gc
 import time
 
 import numpy as np
@@ -194,6 +195,7 @@ def switch_probe(spec, geom, world, tp_to: int, n_samples: int, ctx: int, copy_m
                     "host_plan_s": t.host_plan_s, "host_capture_s": t.host_capture_s,
                     "host_build_s": t.host_build_s, "copy_launches": len(be.copy_events)})
         del be
+        gc.collect()  # backends hold reference cycles (runners <-> executors)
         torch.cuda.empty_cache()
     best = min(out, key=lambda d: d["copy_kernel_ms"])
     return best
@@ -315,6 +317,7 @@ def profile_rank(geom, tp: int, token_cap: int, max_ctx: int, batches=None, leng
         steps = -(-b * max(1, l - 1) // R)
         pts.append(ProfilePoint(tp, b, l, d, float(steps * np.interp(l / 2, cs, ts))))
     del runner, r
+    gc.collect()
     torch.cuda.empty_cache()
     return pts
 
