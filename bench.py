@@ -218,7 +218,7 @@ def main():
     torch.cuda.synchronize(dev)
     with ClockSampler(dev.index or 0) as clk:
         for _ in range(args.steps):
-            rep, _ = coord.run()
+            rep, meas = coord.run()
             reports.append(rep)
             times.append(rep.generation_time)
             walls.append(coord.last_wall_s)
@@ -272,6 +272,7 @@ def main():
                    "parallelism": f"tp{spec.initial_tp}->adaptive,dp{gpus // spec.initial_tp}", "l2": "inputs > L2 (15.2 GB weights streamed per step)",
                    "step": "one generation stage (prefill via decode path + decode to last sample)",
                    "predictor": "B200-measured profile table" if table is not None else "analytic b200.cfg"},
+        "phases": stage_phases(rep, meas),
         "tokens_generated": rep.tokens_generated,
         "tokens_per_s": rep.tokens_generated / value,
         "switches": [{"from": s["from_tp"], "to": s["to_tp"], "round": s["round"],
@@ -324,6 +325,15 @@ def main():
                                           f"stage's {sum(hist.values())} rounds and prefill"}
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def stage_phases(rep, meas) -> dict:
+    """Where the (last timed) stage went: prefill, decode rounds, switches (device clock)."""
+    pre = max((g["prefill"] or 0.0) for g in meas["groups"].values()) if meas["groups"] else 0.0
+    sw = [s for nr in rep.node_reports for s in nr["switches"]]
+    t_sw = sum(s["breakdown"]["total"] for s in sw)
+    return {"prefill_s": pre, "switch_s": t_sw, "decode_s": rep.generation_time - pre - t_sw,
+            "switches": len(sw)}
 
 
 def measured_table(model: str):
