@@ -376,8 +376,11 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_cluster_kernel(
   const int g = lane >> 2, c = lane & 3;
   pdl_launch_dependents();  // dependents may launch now: they read our outputs only after their own wait
   const unsigned int trs = trace_begin(kTrAttnSplit);
-  pdl_wait();
-  trace_mark(trs, 2);
+  const bool decode = row_pos == nullptr;
+  if (!decode) pdl_wait();  // prefill rows of this chunk were appended by the previous kernel
+  // decode: positions, page tables and every cached token but the current one were written by
+  // earlier steps, so the first pages stream before the programmatic wait; the current
+  // token's K/V row and q are read after it
   const int slot = row_slot[b];
   const int ctx = slot >= 0 ? (row_pos ? row_pos[b] : pos_by_slot[slot]) + 1 : 0;
   const int npages = (ctx + kPage - 1) / kPage;
@@ -392,7 +395,9 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_cluster_kernel(
   float o[D / 8][4];
 #pragma unroll
   for (int i = 0; i < D / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-  if (p0 < p1) {
+  if (p0 >= p1) {
+    if (decode) pdl_wait();
+  } else {
     const int* pt = page_table + (size_t)slot * max_pages;
     auto load_page = [&](int p, int st) {
       const size_t goff = ((size_t)pt[p] * nkv + kvh) * TILE;
@@ -413,6 +418,7 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_cluster_kernel(
       if (p0 + i < p1) load_page(p0 + i, i);
       cp_async_commit();
     }
+    if (decode) pdl_wait();
     uint32_t qa[D / 16][4];
     load_q_frags<D>(qa, q + ((size_t)b * nq + head0) * D, G);
     for (int it = 0; p0 + it < p1; ++it) {
@@ -424,10 +430,23 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_cluster_kernel(
         cp_async_commit();
       }
       const int st = it % kAttnStages;
+      if (decode && it < kAttnStages - 1 && p0 + it == npages - 1) {
+        // this page was issued before the wait: refresh the current token's K/V row
+        const int r = (ctx - 1) % kPage;
+        const size_t goff = ((size_t)pt[p0 + it] * nkv + kvh) * TILE + (size_t)r * D;
+        for (int i = tid; i < 2 * CPR; i += kAttnThreads) {
+          const bool is_v = i >= CPR;
+          const int cc = i % CPR;
+          const uint4 v = __ldcg(reinterpret_cast<const uint4*>((is_v ? v_cache : k_cache) + goff) + cc);
+          *reinterpret_cast<uint4*>((is_v ? sv : sk) + st * TILE + r * D + ((cc ^ (r & 7)) * 8)) = v;
+        }
+        __syncthreads();
+      }
       attend_page<D>(sk + st * TILE, sv + st * TILE, qa, (p0 + it) * kPage, ctx, scale_log2, m_r, l_r, o);
     }
     cp_async_wait<0>();
   }
+  trace_mark(trs, 2);
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
     l_r[r] += __shfl_xor_sync(0xffffffffu, l_r[r], 1);
@@ -470,19 +489,41 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_cluster_kernel(
     }
   }
   cluster.sync();
-  // merge across the cluster: CTA r finishes output elements r, r + CL, ... of the G x D tile
+  // merge across the cluster. (1) every peer's (max, sum) per head, fetched in parallel
+  // (thread t reads peer t / 16, head t % 16) -> per-(peer, head) rescale factors in smem;
+  // (2) CTA r finishes output elements r, r + CL, ... of the G x D tile with all CL remote
+  // loads of an element issued together (DSMEM latency is paid once, not CL times)
+  __shared__ float s_pm[16 * 16], s_pl[16 * 16], s_f[16 * 16], s_inv[16];
+  for (int t = tid; t < CL * 16; t += kAttnThreads) {
+    const int r = t >> 4, h = t & 15;
+    s_pm[t] = h < G ? *cluster.map_shared_rank(&c_m[h], r) : -INFINITY;
+    s_pl[t] = h < G ? *cluster.map_shared_rank(&c_l[h], r) : 0.f;
+  }
+  __syncthreads();
+  if (tid < 16) {
+    const int h = tid;
+    float M = -INFINITY;
+    for (int r = 0; r < CL; ++r) M = fmaxf(M, s_pm[r * 16 + h]);
+    float L = 0.f;
+    for (int r = 0; r < CL; ++r) {
+      const float mr = s_pm[r * 16 + h];
+      const float f = (mr == -INFINITY || M == -INFINITY) ? 0.f : exp2f(mr - M);
+      s_f[r * 16 + h] = f;
+      L += s_pl[r * 16 + h] * f;
+    }
+    s_inv[h] = L > 0.f ? 1.f / L : 0.f;
+  }
+  __syncthreads();
   for (int i = crank * kAttnThreads + tid; i < G * D; i += CL * kAttnThreads) {
     const int h = i / D, d = i % D;
-    float M = -INFINITY;
-    for (int r = 0; r < CL; ++r) M = fmaxf(M, *cluster.map_shared_rank(&c_m[h], r));
-    float L = 0.f, acc = 0.f;
-    for (int r = 0; r < CL; ++r) {
-      const float mr = *cluster.map_shared_rank(&c_m[h], r);
-      const float f = (mr == -INFINITY) ? 0.f : exp2f(mr - M);
-      L += *cluster.map_shared_rank(&c_l[h], r) * f;
-      acc += *cluster.map_shared_rank(&c_o[h * D + d], r) * f;
-    }
-    out[((size_t)b * nq + head0 + h) * D + d] = f2bf(L > 0.f ? acc / L : 0.f);
+    float v[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = r < CL ? *cluster.map_shared_rank(&c_o[h * D + d], r) : 0.f;
+    float acc = 0.f;
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+      if (r < CL) acc += v[r] * s_f[r * 16 + h];
+    out[((size_t)b * nq + head0 + h) * D + d] = f2bf(acc * s_inv[h]);
   }
   cluster.sync();  // peers may still be reading this CTA's state
   trace_mark(trs, 3);
