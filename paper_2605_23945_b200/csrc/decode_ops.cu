@@ -544,7 +544,8 @@ __global__ void argmax_finalize_kernel(CandList cands, int nchunk, WaitSpec wait
                                        int* __restrict__ pos_by_slot, const int* __restrict__ prompt_len,
                                        int* __restrict__ history, int hist_ld, int* __restrict__ out_tok) {
   const int b = blockIdx.x;
-  pdl_launch_dependents();  // dependents may launch now: they read our outputs only after their own wait
+  // the step's last kernel releases its dependents only after the new positions are written:
+  // the next step's attention streams KV pages before its own wait, from these positions
   const unsigned int trs = trace_begin(kTrArgmax2);
   pdl_wait();
   do_wait(wait);
@@ -571,13 +572,16 @@ __global__ void argmax_finalize_kernel(CandList cands, int nchunk, WaitSpec wait
       pos_by_slot[slot] = pos + 1;
     }
   }
+  __threadfence();
+  pdl_launch_dependents();
   trace_mark(trs, 3);
 }
 
 __global__ void epoch_advance_kernel(uint64_t* epoch) {
-  pdl_launch_dependents();  // dependents may launch now: they read our outputs only after their own wait
-  pdl_wait();
+  pdl_wait();  // (step boundary: dependents launch after the epoch moved, see argmax_finalize)
   *epoch += 1ull;
+  __threadfence();
+  pdl_launch_dependents();
 }
 
 // Plain fp32 sum of a Src into a dense buffer (tests / logits export).
