@@ -149,9 +149,8 @@ int tps_qkv_rope_append(const float* src, int nsrc, int64_t src_stride, const vo
                         void* k_cache, void* v_cache, void* stream);
 
 /* Split policy for tps_paged_attention: -1 = one thread-block cluster per (row, kv head)
- * segment (tail batches, B x nkv <= 8), n = one wave of fixed splits when it fills >= 80 %% of
- * the resident CTA slots (nkv > 1), 0 = page-balanced schedule (B x nkv >= 64 or one
- * local KV head, B <= 512), else the fixed split count for this shape. */
+ * segment (tail batches, B x nkv <= 8); n = one wave of fixed splits when it fills >= 80 %
+ * of the resident CTA slots; 0 = page-balanced schedule (more segments than slots, B <= 512). */
 int tps_attn_splits(int B, int nkv, int max_pages);
 /* fp32 elements of part_o a tps_paged_attention call needs (part_m / part_l: that / D);
  * nsplit = 0 selects the page-balanced schedule. */

@@ -608,10 +608,10 @@ int attn_splits(int B, int nkv, int max_pages) {
   // page-balanced when the (row, kv head) segments give enough parallel work, and for a
   // single local KV head (TP-sharded GQA tail: measured faster than split + combine)
   if (B * nkv <= g_max_cluster) return -1;  // tail: one CTA cluster per (row, kv head)
-  // one wave of fixed splits when it fills >= 80 % of the resident CTA slots (no cross-CTA
-  // merges; measured on the bench stage: -1.4 % vs balanced at B = 16..64); else, and for a
-  // single local KV head or more segments than slots, the page-balanced schedule
-  if (nkv > 1 && B * nkv <= 2 * kNumSMs && g_min_bal == 64) {
+  // one wave of fixed splits when it fills >= 80 % of the resident CTA slots (measured: bench
+  // stage -1.4 % vs balanced at B = 16..64; one local KV head (TP4/TP8 Qwen2.5-7B) B = 12..64
+  // -9..11 % per step); else, with more segments than slots, the page-balanced schedule
+  if (B * nkv <= 2 * kNumSMs && g_min_bal == 64) {
     const int ns = attn_fixed_splits(B, nkv, max_pages);
     if ((long long)B * nkv * ns * 10 >= 8LL * 2 * kNumSMs) return ns;
   }

@@ -39,7 +39,7 @@ def test_library_loads_and_reports_version():
     assert lib.tps_linear_splits(4608, 3584, 64) >= 1
     assert lib.tps_attn_splits(1, 4, 136) == -1       # tail: one CTA cluster per (row, kv head)
     assert lib.tps_attn_splits(96, 4, 136) == 0       # page-balanced schedule
-    assert lib.tps_attn_splits(64, 1, 136) == 0       # one local KV head: page-balanced
+    assert lib.tps_attn_splits(300, 1, 136) == 0      # more segments than CTA slots: page-balanced
     assert 1 <= lib.tps_attn_splits(4, 4, 136) <= 32  # fixed split-KV
 
 
