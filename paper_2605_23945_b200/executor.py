@@ -142,6 +142,8 @@ class InferExecutor:
         self.skip: frozenset = frozenset()
         # 0: greedy; > 0: Gumbel-max sampling at this temperature with the slots' Philox keys
         self.temperature = 0.0
+        # gate/up with the SwiGLU fused (split-K 1) once this many (tile x act) units exist
+        self.fuse_silu_min_units = 120
         self.device = torch.device(device)
         self.comm = comm
         self.tp = shard.tp
@@ -213,7 +215,7 @@ class InferExecutor:
         tiles (x activation tiles) alone fill most of the 148 SMs."""
         bn = 16 if B <= 16 else 32 if B <= 32 else 64 if B <= 64 else 128 if B <= 128 else 256
         units = (2 * self.F // 128) * (-(-B // bn))
-        return units >= 120
+        return units >= self.fuse_silu_min_units
 
     def _attn_splits(self, B: int, fused: bool) -> int:
         """tps_attn_splits policy (-1 = cluster per segment, 0 = page-balanced, n = fixed splits);
