@@ -139,6 +139,12 @@ int tps_add_norm(float* resid, const float* src, int nsrc, int64_t src_stride, c
 int tps_reduce_push(const float* src, int nsrc, int64_t src_stride, float* const* dsts, int ndst, int64_t n,
                     uint64_t* const* sig_ctrs, int nsig, unsigned int* done, void* stream);
 
+/* LL form of tps_reduce_push: the summed [n] fp32 row block goes to every destination as
+ * uint64 {value, tag} pairs (tag = (*epoch) * tag_mult + tag_add); no counters -- the
+ * consumer is tps_add_norm_ll over the tp slots. */
+int tps_reduce_push_ll(const float* src, int nsrc, int64_t src_stride, uint64_t* const* dsts, int ndst, int64_t n,
+                       const uint64_t* epoch, uint32_t tag_mult, uint32_t tag_add, void* stream);
+
 /* QKV: sum split partials [s][B][(nq+2nkv)*D] + bias, rotate-half RoPE (fp32
  * cos/sin tables [pos][D/2]), q -> bf16 [B][nq][D], k/v appended at each
  * row's position into the paged cache [page][nkv][64][D]. */

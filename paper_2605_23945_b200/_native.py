@@ -44,6 +44,7 @@ SIGNATURES = {
     "tps_linear_silu": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _vp, _i64, _vp]),
     "tps_embed": (_i32, [_vp, _vp, _vp, _vp, _i32, _vp, _i32, _i32, _vp, _vp]),
     "tps_add_norm": (_i32, [_vp, _vp, _i32, _i64, _vp, _vp, _f32, _i32, _i32, _vp, _i32, _vp]),
+    "tps_reduce_push_ll": (_i32, [_vp, _i32, _i64, _pp, _i32, _i64, _vp, ctypes.c_uint32, ctypes.c_uint32, _vp]),
     "tps_reduce_push": (_i32, [_vp, _i32, _i64, _pp, _i32, _i64, _pp, _i32, _vp, _vp]),
     "tps_qkv_rope_append": (_i32, [_vp, _i32, _i64, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _i32, _i32, _i32,
                                    _i32, _i32, _vp, _vp, _vp, _vp]),

@@ -51,6 +51,8 @@ int configure_gemm();
 int configure_attention();
 int configure_copy();
 int configure_decode_ops();
+int reduce_push_ll(const Src& src, const DstList& dst, long long n, const uint64_t* epoch, uint32_t mult,
+                   uint32_t add, cudaStream_t st);
 int linear_push_ll(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
                    int64_t ldx, const DstList& dst, int64_t split_stride, int splits, const uint64_t* tag_epoch,
                    uint32_t tag_mult, uint32_t tag_add, cudaStream_t stream);
@@ -182,6 +184,21 @@ int tps_add_norm(float* resid, const float* src, int nsrc, int64_t src_stride, c
   int rc = make_src(src, nsrc, src_stride, &s);
   if (rc) return rc;
   return add_norm(resid, s, make_wait(wait), w, eps, H, B, out, ldo, S(stream));
+}
+
+int tps_reduce_push_ll(const float* src, int nsrc, int64_t src_stride, uint64_t* const* dsts, int ndst, int64_t n,
+                       const uint64_t* epoch, uint32_t tag_mult, uint32_t tag_add, void* stream) {
+  Src s;
+  int rc = make_src(src, nsrc, src_stride, &s);
+  if (rc) return rc;
+  TPS_CHECK_ARG(ndst >= 1 && ndst <= kMaxPeers && dsts, "reduce_push_ll: 1..8 destinations");
+  DstList dl;
+  dl.n = ndst;
+  for (int i = 0; i < ndst; ++i) {
+    TPS_CHECK_ARG((reinterpret_cast<uintptr_t>(dsts[i]) & 31) == 0, "reduce_push_ll: 32B-aligned destinations");
+    dl.p[i] = reinterpret_cast<float*>(dsts[i]);
+  }
+  return reduce_push_ll(s, dl, n, epoch, tag_mult, tag_add, S(stream));
 }
 
 int tps_reduce_push(const float* src, int nsrc, int64_t src_stride, float* const* dsts, int ndst, int64_t n,

@@ -15,6 +15,8 @@
 // row_slot vector. row_slot[b] < 0 marks a padding row of a graph bucket.
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -364,6 +366,30 @@ __global__ void __launch_bounds__(256) reduce_push_kernel(Src src, DstList dst, 
   trace_mark(trs, 3);
 }
 
+// LL form: sum the split partials, store {value, tag} pairs to every destination (no signal:
+// the consumer polls the tags). Used for mid-size tail batches, where pushing every split
+// partial from the projection epilogue would multiply the NVLink bytes by the split count.
+__global__ void __launch_bounds__(256) reduce_push_ll_kernel(Src src, DstList dst, long long n4,
+                                                             const uint64_t* epoch, uint32_t mult, uint32_t add) {
+  pdl_launch_dependents();  // dependents may launch now: they read our outputs only after their own wait
+  const unsigned int trs = trace_begin(kTrReducePush);
+  pdl_wait();
+  trace_mark(trs, 2);
+  const uint64_t tag = (uint64_t)((uint32_t)(*(volatile const uint64_t*)epoch * mult + add)) << 32;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float4 v = src_sum4(src, i);
+    for (int d = 0; d < dst.n; ++d) {
+      uint64_t* o = reinterpret_cast<uint64_t*>(dst.p[d]) + 4 * i;
+      st_relaxed_sys_u64(o, tag | __float_as_uint(v.x));
+      st_relaxed_sys_u64(o + 1, tag | __float_as_uint(v.y));
+      st_relaxed_sys_u64(o + 2, tag | __float_as_uint(v.z));
+      st_relaxed_sys_u64(o + 3, tag | __float_as_uint(v.w));
+    }
+  }
+  trace_mark(trs, 3);
+}
+
 // ---------------------------------------------- QKV bias + RoPE + KV append ---
 // partial layout [split][B][Nqkv] with Nqkv = (nq + 2 nkv) * D, rows ordered
 // [q heads | k heads | v heads] (canonical shard layout). RoPE is the
@@ -658,6 +684,16 @@ int reduce_push(const Src& src, const DstList& dst, long long n, const SignalSpe
   return launch_k(reduce_push_kernel, dim3(kPushBlocks), dim3(256), 0, st, true, src, dst, n / 4, sig);
 }
 
+int reduce_push_ll(const Src& src, const DstList& dst, long long n, const uint64_t* epoch, uint32_t mult,
+                   uint32_t add, cudaStream_t st) {
+  TPS_CHECK_ARG(n % 4 == 0 && src.n >= 1 && dst.n >= 1 && src.stride % 4 == 0 && epoch,
+                "reduce_push_ll: n % 4 == 0, >=1 src/dst, epoch");
+  const long long n4 = n / 4;
+  const int grid = (int)std::min<long long>(4LL * kNumSMs, (n4 + 255) / 256);
+  return launch_k(reduce_push_ll_kernel, dim3(grid > 0 ? grid : 1), dim3(256), 0, st, true, src, dst, n4, epoch,
+                  mult, add);
+}
+
 int qkv_rope_append(const Src& src, const void* bias, const int* row_slot, const int* pos_by_slot,
                     const int* row_pos, const int* page_table, int max_pages, const float* cos_t,
                     const float* sin_t, int B, int nq,
@@ -713,6 +749,7 @@ int configure_decode_ops() {
   TPS_MAX_CARVEOUT(add_norm_cluster_kernel<false>);
   TPS_MAX_CARVEOUT(add_norm_cluster_kernel<true>);
   TPS_MAX_CARVEOUT(reduce_push_kernel);
+  TPS_MAX_CARVEOUT(reduce_push_ll_kernel);
   TPS_MAX_CARVEOUT(qkv_rope_append_kernel);
   TPS_MAX_CARVEOUT(silu_mul_kernel);
   TPS_MAX_CARVEOUT(argmax_stage1_kernel);

@@ -45,7 +45,10 @@ def argmax_chunks(B: int) -> int:
     return max(1, min(64, 296 // max(1, B)))
 
 
-FUSE_ROWS = 64     # row-parallel projections push their split partials straight to peers up to this batch
+FUSE_ROWS = 64     # tail batches (B <= FUSE_ROWS) exchange the TP allreduce as LL {value, tag} pairs
+LL_EPILOGUE_ROWS = 16  # ... from the projection epilogue (every split partial) up to this batch; above it
+                       # a reduce kernel sums the splits first (S x fewer NVLink bytes; the crossover of
+                       # the extra launch vs the modeled NVLink bytes is ~16 rows at TP8)
 FUSE_SOURCES = 16  # LL slots per parity: tp x splits partials of one fused allreduce (one load batch)
 
 
@@ -391,15 +394,23 @@ class InferExecutor:
         g = self.geom
         H = g.hidden
         n, k = w.shape
-        S = self.fused_splits(fam, B)
         par = phase % 2
         # LL: {value, tag} stores polled by the consumer; tag = epoch * n_phases + phase
         # (a loopback timing rank -- profiler.loopback_rank -- fills every rank's slots itself)
-        dsts = [cm.ll_slot(base, par, q if cm.loopback else self.rank, S) for q, base in enumerate(cm.peer_ll)]
-        nat.check(lib.tps_linear_push_ll(w.data_ptr(), n, k, k, x.data_ptr(), B, x.shape[0], x.shape[1],
-                                         self._arr(dsts), len(dsts), FUSE_ROWS * H, S, cm.epoch.data_ptr(),
-                                         cm.n_phases, phase, st), "tps_linear_push_ll")
-        stats.add("linear")
+        if B <= LL_EPILOGUE_ROWS:
+            S = self.fused_splits(fam, B)
+            dsts = [cm.ll_slot(base, par, q if cm.loopback else self.rank, S) for q, base in enumerate(cm.peer_ll)]
+            nat.check(lib.tps_linear_push_ll(w.data_ptr(), n, k, k, x.data_ptr(), B, x.shape[0], x.shape[1],
+                                             self._arr(dsts), len(dsts), FUSE_ROWS * H, S, cm.epoch.data_ptr(),
+                                             cm.n_phases, phase, st), "tps_linear_push_ll")
+            stats.add("linear")
+        else:
+            S = 1  # one summed slot per rank
+            srcs = self._linear(st, stats, w, x, B)
+            dsts = [cm.ll_slot(base, par, q if cm.loopback else self.rank, 1) for q, base in enumerate(cm.peer_ll)]
+            nat.check(lib.tps_reduce_push_ll(*srcs, self._arr(dsts), len(dsts), B * H, cm.epoch.data_ptr(),
+                                             cm.n_phases, phase, st), "tps_reduce_push_ll")
+            stats.add("reduce_push")
         yield
         if "add_norm" in self.skip:
             return

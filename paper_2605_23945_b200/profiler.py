@@ -237,11 +237,13 @@ def nvlink_adjust(geom, tp: int, batch: int) -> float:
     of the 2L allreduces one NVLink hop plus the bytes this rank pushes to its tp-1 peers."""
     if tp == 1:
         return 0.0
-    from .executor import FUSE_ROWS, FUSE_SOURCES
-    # tail batches: LL pairs (8 B per element) of every split partial (<= FUSE_SOURCES slots
-    # per group); larger batches: the one summed fp32 row per peer (reduce-push)
-    if batch <= FUSE_ROWS:
+    from .executor import FUSE_ROWS, FUSE_SOURCES, LL_EPILOGUE_ROWS
+    # B <= 16: LL pairs (8 B per element) of every split partial (<= FUSE_SOURCES slots per
+    # group); B <= 64: LL pairs of the summed row; larger: the summed fp32 row (reduce-push)
+    if batch <= LL_EPILOGUE_ROWS:
         per_row = geom.hidden * 8 * (tp - 1) * max(1, FUSE_SOURCES // tp)
+    elif batch <= FUSE_ROWS:
+        per_row = geom.hidden * 8 * (tp - 1)
     else:
         per_row = geom.hidden * 4 * (tp - 1)
     return 2 * geom.num_layers * (NVLINK_HOP_S + batch * per_row / (NVLINK_GBPS * 1e9))
