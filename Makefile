@@ -1,5 +1,5 @@
 # Builds the sm_100a engine library in-tree (the .so travels to the GPU box with
-# the gpurun snapshot) and the oracle's C helpers.
+# the gpurun snapshot). The oracle (oracle/) is Python/numpy: nothing to compile.
 NVCC ?= /usr/local/cuda/bin/nvcc
 PKG := paper_2605_23945_b200
 CSRC := $(PKG)/csrc
@@ -9,15 +9,11 @@ HDRS := $(CSRC)/common.cuh $(CSRC)/decode_ops.cuh include/tpshift_b200.h
 NVFLAGS := -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
            -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
 
-.PHONY: all clean oracle
-all: $(LIB) oracle
+.PHONY: all clean
+all: $(LIB)
 
 $(LIB): $(SRCS) $(HDRS)
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) 2> build_ptxas.log || (cat build_ptxas.log; false)
 
-oracle:
-	$(MAKE) -C oracle
-
 clean:
 	rm -f $(LIB) build_ptxas.log
-	$(MAKE) -C oracle clean

@@ -291,6 +291,13 @@ def main():
     }
     if e2e:
         line["e2e"] = e2e
+    if table is not None:
+        # the Offline Profiler's prediction of this same stage: the reference engine loop replayed
+        # over the measured table (SURVEY §8(f)2 predictor-error target: <= 8 %)
+        from paper_2605_23945_b200.engine import TableBackend, run as sim_run
+        pred = sim_run(spec, table, TableBackend(spec, table)).generation_time
+        line["predicted"] = {"value": pred, "unit": UNIT, "rel_error": (pred - value) / value,
+                             "source": "reference engine loop over presets/b200_<model>_profile.csv"}
     tr = traffic_record()
     if tr:
         line["roofline"]["traffic"] = tr["dram_bytes"]

@@ -56,9 +56,10 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_kernel(
 
   pdl_launch_dependents();  // dependents may launch now: they read our outputs only after their own wait
   const unsigned int trs = trace_begin(kTrAttnSplit);
-  // plain decode: the first pages stream before the programmatic wait (every cached token but
-  // the current one was written by earlier steps; its row is refreshed after the wait)
-  const bool early = !fused && row_pos == nullptr && early_ok;
+  // decode: the first pages stream before the programmatic wait (every cached token but the
+  // current one was written by earlier steps; its row is refreshed after the wait, or -- fused
+  // form -- patched in from the k/v this kernel finishes)
+  const bool early = row_pos == nullptr && early_ok;
   if (!early) pdl_wait();
   trace_mark(trs, 2);
 
@@ -185,7 +186,7 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_kernel(
         cp_async_commit();
       }
       const int st = it % kAttnStages;
-      if (early && it < kAttnStages - 1 && p0 + it == npages - 1) {
+      if (early && !fused && it < kAttnStages - 1 && p0 + it == npages - 1) {
         // issued before the wait: refresh the current token's K/V row
         const int r = (ctx - 1) % kPage;
         const size_t goff = ((size_t)pt[p0 + it] * nkv + kvh) * TILE + (size_t)r * D;

@@ -139,7 +139,9 @@ class InferExecutor:
         self.prefill_rows = prefill_rows
         rows = max(max_batch, prefill_rows)
         # finishing q/k/v inside the attention kernel saves a launch but every split CTA
-        # recomputes its group's queries; measured slower at B >= 1 on B200 (off by default)
+        # recomputes its group's queries after the wait; measured slower on B200 even with the
+        # KV pages streaming before the wait (TP1 B=64 ctx 2048 4.480 vs 4.462 ms, TP8 B=1
+        # 1.518 vs 1.391): off by default
         self.fuse_rope = False
         # launch kinds left out of the step program (timing probes only: results are garbage)
         self.skip: frozenset = frozenset()
