@@ -145,6 +145,20 @@ int tps_reduce_push(const float* src, int nsrc, int64_t src_stride, float* const
 int tps_reduce_push_ll(const float* src, int nsrc, int64_t src_stride, uint64_t* const* dsts, int ndst, int64_t n,
                        const uint64_t* epoch, uint32_t tag_mult, uint32_t tag_add, void* stream);
 
+/* Split-K count of tps_linear_qkv_rope for an [n x k] QKV weight at batch b; 0 when the
+ * shape does not take the fused form (b > 64, more tiles x splits than SMs, ...). */
+int tps_qkv_fused_splits(int64_t n, int64_t k, int64_t b);
+
+/* QKV projection finished in-kernel: out = W x (split-K over a thread-block cluster, the
+ * partials summed over DSMEM in split order) + bias, RoPE, q -> bf16 [b][nq][D], k/v
+ * appended into the paged cache -- the results of tps_linear + tps_qkv_rope_append in
+ * one launch. n = (nq + 2 nkv) * D. */
+int tps_linear_qkv_rope(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,
+                        int64_t x_rows, int64_t ldx, const void* bias, const int* row_slot,
+                        const int* pos_by_slot, const int* row_pos, const int* page_table, int max_pages,
+                        const float* cos_t, const float* sin_t, int nq, int nkv, int D, int page_size,
+                        void* q_out, void* k_cache, void* v_cache, void* stream);
+
 /* QKV: sum split partials [s][B][(nq+2nkv)*D] + bias, rotate-half RoPE (fp32
  * cos/sin tables [pos][D/2]), q -> bf16 [B][nq][D], k/v appended at each
  * row's position into the paged cache [page][nkv][64][D]. */

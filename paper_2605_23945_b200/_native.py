@@ -15,6 +15,8 @@ from .errors import ConfigError, PlanVerificationError
 
 LIB_NAME = "libtpshift_b200.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+# dev A/B only: TPS_LIB_PATH points at an alternative build of the same library
+LIB_PATH = os.environ.get("TPS_LIB_PATH", LIB_PATH)
 
 TPS_OK = 0
 TPS_EINVAL = -22
@@ -34,6 +36,9 @@ SIGNATURES = {
     "tps_init": (_i32, [_i32, ctypes.POINTER(_i32)]),
     "tps_set_pdl": (None, [_i32]),
     "tps_linear_splits": (_i32, [_i64, _i64, _i64]),
+    "tps_qkv_fused_splits": (_i32, [_i64, _i64, _i64]),
+    "tps_linear_qkv_rope": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _i32,
+                                   _vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
     "tps_linear": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _vp, _i32, _vp]),
     "tps_linear_push": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _pp, _i32, _i64, _i32, _pp, _i32,
                                 _vp, _vp]),

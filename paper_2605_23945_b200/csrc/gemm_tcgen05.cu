@@ -19,6 +19,9 @@
 //     epilogue of unit i overlaps the MMAs of unit i+1.
 // Split partials are reduced, in fixed split order, by the consumer kernels
 // (norm / rope / silu / argmax), which keeps results deterministic.
+#include <cooperative_groups.h>
+#include <stdlib.h>
+
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -38,11 +41,22 @@ struct GemmCfg {
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kStagesRaw = (200 * 1024) / kStageBytes;
-  static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
+#ifndef TPS_GEMM_MAX_STAGES
+#define TPS_GEMM_MAX_STAGES 8
+#endif
+  static constexpr int kStages = kStagesRaw > TPS_GEMM_MAX_STAGES ? TPS_GEMM_MAX_STAGES : kStagesRaw;
   static constexpr int kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
   static constexpr int kBarBytes = 256;
   static constexpr int kEpiBytes = 64 * 17 * 4;  // SwiGLU epilogue exchange buffer
   static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kBarBytes + kEpiBytes;
+  // the in-kernel-finished QKV form keeps a shallower ring so two CTAs fit per SM: the next
+  // launch's clusters become resident (and prefetch) while this one drains
+#ifndef TPS_QKV_STAGES
+#define TPS_QKV_STAGES 4
+#endif
+  static constexpr int kQkvStages = kStages < TPS_QKV_STAGES ? kStages : TPS_QKV_STAGES;
+  static constexpr int kQkvSmemBytes = 1024 + kQkvStages * kStageBytes + kBarBytes + kEpiBytes;
+  static_assert(BN * kBM * 4 <= kQkvStages * kStageBytes, "QKV partial tile must fit the drained ring");
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128 must be 16..256, %16");
   static_assert(kStages >= 3, "need at least 3 stages");
 };
@@ -88,6 +102,86 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 // writes act[b][f] = bf16(silu(gate) * up) directly -- the SwiGLU never round-trips HBM.
 constexpr int kEpiPartial = 0;
 constexpr int kEpiSiluMul = 1;
+// kEpiQkvRope: the QKV projection finished in-kernel. The S split-K CTAs of a weight tile
+// form one thread-block cluster; each parks its fp32 partial tile in its own (drained) smem
+// ring, and after a cluster barrier CTA s sums -- over DSMEM, in split order, like the
+// consumer kernels -- the rotary pairs of its slice of the tile, adds the bias, applies
+// RoPE at each row's position and writes q (bf16) and the new k/v into the paged cache.
+// This replaces tps_qkv_rope_append (one launch + its PDL boundary per layer).
+constexpr int kEpiQkvRope = 2;
+
+
+namespace cg = cooperative_groups;
+
+// Finishing of kEpiQkvRope (all 256 threads of every CTA of the cluster).
+// part: this CTA's [BN][128] fp32 tile partial (row j = token row, column r = weight row).
+template <int BN>
+__device__ __forceinline__ void qkv_finish(const float* part, const QkvEpi& e, int tile, int N, int rows) {
+  __shared__ int s_pos[BN], s_slot[BN], s_page[BN];
+  for (int j = threadIdx.x; j < rows; j += kGemmThreads) {  // row metadata, once per CTA
+    const int slot = e.row_slot[j];
+    const int pos = slot >= 0 ? (e.row_pos ? e.row_pos[j] : e.pos_by_slot[slot]) : 0;
+    s_slot[j] = slot;
+    s_pos[j] = pos;
+    s_page[j] = slot >= 0 ? e.page_table[(size_t)slot * e.max_pages + pos / e.P] : 0;
+  }
+  cg::cluster_group cl = cg::this_cluster();
+  cl.sync();  // every split's partial tile is parked in its CTA's smem (and the metadata is in)
+  const int S = (int)cl.num_blocks();
+  const int rank = (int)cl.block_rank();
+  const int half = e.D / 2;
+  const int li0 = rank * 64 / S, li1 = (rank + 1) * 64 / S;  // 64 rotary pairs per 128-row tile
+  const int nli = li1 - li0;
+  const float* rp[16];
+#pragma unroll
+  for (int s = 0; s < 16; ++s) rp[s] = s < S ? cl.map_shared_rank(part, s) : part;
+  for (int it = threadIdx.x; it < nli * rows; it += kGemmThreads) {
+    const int li = li0 + it % nli, j = it / nli;
+    const int r_lo = (li / half) * e.D + li % half;
+    const int n_lo = tile * kBM + r_lo;
+    if (n_lo >= N) continue;  // (N is a whole number of heads)
+    float v0[16], v1[16];
+#pragma unroll
+    for (int s = 0; s < 16; ++s)
+      if (s < S) {
+        v0[s] = rp[s][j * kBM + r_lo];
+        v1[s] = rp[s][j * kBM + r_lo + half];
+      }
+    float x0 = 0.f, x1 = 0.f;  // split order, from 0: the same sums as the consumer kernels
+#pragma unroll
+    for (int s = 0; s < 16; ++s)
+      if (s < S) {
+        x0 += v0[s];
+        x1 += v1[s];
+      }
+    if (e.bias) {
+      x0 += bf2f(e.bias[n_lo]);
+      x1 += bf2f(e.bias[n_lo + half]);
+    }
+    const int b = j;
+    const int slot = s_slot[b], pos = s_pos[b];
+    const int h = n_lo / e.D, i = n_lo % e.D;
+    if (h < e.nq) {
+      const float cs = e.cos_t[(size_t)pos * half + i], sn = e.sin_t[(size_t)pos * half + i];
+      __nv_bfloat16* q = e.q_out + ((size_t)b * e.nq + h) * e.D;
+      q[i] = f2bf(x0 * cs - x1 * sn);
+      q[i + half] = f2bf(x1 * cs + x0 * sn);
+    } else if (slot >= 0) {
+      const bool is_k = h < e.nq + e.nkv;
+      const int jh = is_k ? h - e.nq : h - e.nq - e.nkv;
+      const int page = s_page[b];
+      const size_t off_c = (((size_t)page * e.nkv + jh) * e.P + (pos % e.P)) * e.D;
+      if (is_k) {
+        const float cs = e.cos_t[(size_t)pos * half + i], sn = e.sin_t[(size_t)pos * half + i];
+        e.k_cache[off_c + i] = f2bf(x0 * cs - x1 * sn);
+        e.k_cache[off_c + i + half] = f2bf(x1 * cs + x0 * sn);
+      } else {
+        e.v_cache[off_c + i] = f2bf(x0);
+        e.v_cache[off_c + i + half] = f2bf(x1);
+      }
+    }
+  }
+}
 
 template <int BN, int EPI>
 __global__ void __launch_bounds__(kGemmThreads, 1)
@@ -95,9 +189,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                        const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ DstList dst,
                        long long split_stride, int N, int B, int num_tiles, int splits, int chunks, int acts,
                        __nv_bfloat16* __restrict__ act_out, int ld_act, const __grid_constant__ SignalSpec sig,
-                       const uint64_t* __restrict__ tag_epoch, uint32_t tag_mult, uint32_t tag_add) {
+                       const uint64_t* __restrict__ tag_epoch, uint32_t tag_mult, uint32_t tag_add,
+                       const __grid_constant__ QkvEpi qkv) {
   using Cfg = GemmCfg<BN>;
-  constexpr int S = Cfg::kStages;
+  constexpr int S = EPI == kEpiQkvRope ? Cfg::kQkvStages : Cfg::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_a = smem;
@@ -278,6 +373,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
           }
         }
+      } else if constexpr (EPI == kEpiQkvRope) {
+        // one unit per CTA: its MMAs (and so every smem read of the ring) are complete
+        float* part = reinterpret_cast<float*>(smem);
+        const int r = q * 32 + lane;
+        for (int j0 = 0; j0 < rows; j0 += 16) {
+          uint32_t v[16];
+          tmem_ld16(tmem_base + (uint32_t)(acc * BN + j0) + ((uint32_t)(q * 32) << 16), v);
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (j0 + j < rows) part[(j0 + j) * kBM + r] = __uint_as_float(v[j]);
+        }
       } else {
         // rows 0..63 of the tile are gate(f), rows 64..127 up(f), f = tile*64 + row
         const int m = (q & 1) * 32 + lane;
@@ -315,6 +421,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if constexpr (EPI == kEpiQkvRope) {
+    pdl_wait();  // (every thread: the finishing reads row metadata and writes q / the cache)
+    qkv_finish<BN>(reinterpret_cast<const float*>(smem), qkv, (int)blockIdx.x / (int)cg::this_cluster().num_blocks(),
+                   N, B);
+    cg::this_cluster().sync();  // keep this smem alive until the cluster has read it
+  }
   if (warp == 2) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                  "n"(Cfg::kTmemCols));
@@ -416,6 +528,7 @@ struct EpiArgs {
   const uint64_t* tag_epoch = nullptr;
   uint32_t tag_mult = 0;
   uint32_t tag_add = 0;
+  QkvEpi qkv{};
 };
 
 template <int BN, int EPI>
@@ -425,9 +538,13 @@ static int launch_gemm(const CUtensorMap& mw, const CUtensorMap& mx, const EpiAr
   const int acts = (b + BN - 1) / BN;
   const int units = tiles * splits * acts;
   const int grid = units < kNumSMs ? units : kNumSMs;
+  if constexpr (EPI == kEpiQkvRope)  // one unit per CTA, the splits of a tile in one cluster
+    return launch_kcs(gemm_swapab_kernel<BN, EPI>, dim3(units), dim3(kGemmThreads), splits, Cfg::kQkvSmemBytes,
+                      stream, true, mw, mx, e.dst, e.split_stride, n, b, tiles, splits, chunks, acts, e.act_out,
+                      e.ld_act, e.sig, e.tag_epoch, e.tag_mult, e.tag_add, e.qkv);
   return launch_k(gemm_swapab_kernel<BN, EPI>, dim3(grid), dim3(kGemmThreads), Cfg::kSmemBytes, stream, true, mw,
                   mx, e.dst, e.split_stride, n, b, tiles, splits, chunks, acts, e.act_out, e.ld_act, e.sig,
-                  e.tag_epoch, e.tag_mult, e.tag_add);
+                  e.tag_epoch, e.tag_mult, e.tag_add, e.qkv);
 }
 
 template <int BN>
@@ -438,6 +555,13 @@ static int configure_one() {
                                     GemmCfg<BN>::kSmemBytes));
   TPS_MAX_CARVEOUT((gemm_swapab_kernel<BN, kEpiPartial>));
   TPS_MAX_CARVEOUT((gemm_swapab_kernel<BN, kEpiSiluMul>));
+  if constexpr (BN <= 64) {
+    TPS_CUDA_TRY(cudaFuncSetAttribute(gemm_swapab_kernel<BN, kEpiQkvRope>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN>::kQkvSmemBytes));
+    TPS_CUDA_TRY(cudaFuncSetAttribute(gemm_swapab_kernel<BN, kEpiQkvRope>,
+                                      cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    TPS_MAX_CARVEOUT((gemm_swapab_kernel<BN, kEpiQkvRope>));
+  }
   return kOk;
 }
 
@@ -449,6 +573,29 @@ int configure_gemm() {
   if (!rc) rc = configure_one<128>();
   if (!rc) rc = configure_one<256>();
   return rc;
+}
+
+// TPS_QKV_CLUSTER=<n>: largest split-K cluster of the in-kernel QKV finishing (default 8,
+// the portable cluster size; 16 is allowed, 0 turns the fused form off)
+static int g_qkv_cluster = [] {
+  const char* v = getenv("TPS_QKV_CLUSTER");
+  return v ? atoi(v) : 8;
+}();
+
+// Split count of the in-kernel-finished QKV projection, 0 when the shape does not take it:
+// b <= 64 (one activation tile), every (tile, split) unit on its own SM (one wave), the
+// splits of a tile within one cluster.
+int qkv_fused_splits(int64_t n, int64_t k, int64_t b) {
+  if (g_qkv_cluster <= 0 || b < 1 || b > 64 || n % kBM) return 0;
+  const int64_t tiles = n / kBM;
+  const int64_t chunks = (k + kBK - 1) / kBK;
+  if (tiles > kNumSMs) return 0;
+  int s = linear_splits(n, k, b);
+  int64_t cap = g_qkv_cluster < 16 ? g_qkv_cluster : 16;
+  if (cap > chunks) cap = chunks;
+  if (cap > kNumSMs / tiles) cap = kNumSMs / tiles;
+  if (s > cap) s = cap;
+  return s >= 1 ? s : 0;
 }
 
 template <int EPI>
@@ -546,6 +693,32 @@ int linear_silu(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x,
   e.ld_act = (int)ld_act;
   e.sig.n = 0;
   return dispatch<kEpiSiluMul>(bn, mw, mx, e, (int)n, (int)b, (int)(n / kBM), 1, (int)chunks, stream);
+}
+
+int linear_qkv_rope(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
+                    int64_t ldx, const QkvEpi& qe, cudaStream_t stream) {
+  const int splits = qkv_fused_splits(n, k, b);
+  TPS_CHECK_ARG(splits >= 1, "linear_qkv_rope: shape not supported (see tps_qkv_fused_splits)");
+  TPS_CHECK_ARG(qe.D % 2 == 0 && kBM % qe.D == 0 && n == (int64_t)(qe.nq + 2 * qe.nkv) * qe.D && qe.P > 0,
+                "linear_qkv_rope: n must be (nq + 2 nkv) * D with D dividing 128");
+  TPS_CHECK_ARG(qe.row_slot && qe.pos_by_slot && qe.page_table && qe.cos_t && qe.sin_t && qe.q_out && qe.k_cache &&
+                    qe.v_cache,
+                "linear_qkv_rope: null pointer");
+  const int64_t chunks = (k + kBK - 1) / kBK;
+  CUtensorMap mw, mx;
+  int bn;
+  int rc = prepare(w, n, k, ldw, x, b, x_rows, ldx, &mw, &mx, &bn);
+  if (rc) return rc;
+  EpiArgs e{};
+  e.dst.n = 0;
+  e.sig.n = 0;
+  e.qkv = qe;
+  const int tiles = (int)(n / kBM);
+  switch (bn) {
+    case 16: return launch_gemm<16, kEpiQkvRope>(mw, mx, e, (int)n, (int)b, tiles, splits, (int)chunks, stream);
+    case 32: return launch_gemm<32, kEpiQkvRope>(mw, mx, e, (int)n, (int)b, tiles, splits, (int)chunks, stream);
+    default: return launch_gemm<64, kEpiQkvRope>(mw, mx, e, (int)n, (int)b, tiles, splits, (int)chunks, stream);
+  }
 }
 
 int trace_register_gemm(uint64_t* p, unsigned int* c, unsigned int n) { return trace_register(p, c, n); }

@@ -143,6 +143,12 @@ class InferExecutor:
         # KV pages streaming before the wait (TP1 B=64 ctx 2048 4.480 vs 4.462 ms, TP8 B=1
         # 1.518 vs 1.391): off by default
         self.fuse_rope = False
+        # decode QKV finished inside the projection kernel (tps_linear_qkv_rope: cluster split-K,
+        # DSMEM partial sums, bias/RoPE/KV append in the epilogue) where the shape takes it.
+        # Bit-identical to tps_linear + tps_qkv_rope_append but measured neutral in the step
+        # (TP1 B=64 ctx 2048 4.475 vs 4.465 ms, TP8 B=1 1.418 vs 1.392: the separate finishing
+        # launch is already hidden under attention's early KV stream): off by default
+        self.qkv_in_gemm = False
         # launch kinds left out of the step program (timing probes only: results are garbage)
         self.skip: frozenset = frozenset()
         # 0: greedy; > 0: Gumbel-max sampling at this temperature with the slots' Philox keys
@@ -273,15 +279,31 @@ class InferExecutor:
         stats.add("add_norm")
         fuse = self.fuse_rope and not prefill
         nsplit = self._attn_splits(B, fuse)
+        w_qkv0 = W[(0, "w_qkv")]
+        # decode: the QKV projection finished in-kernel (cluster split-K + bias/RoPE/KV append)
+        qkv_in_gemm = (self.qkv_in_gemm and not fuse and not prefill and
+                       lib.tps_qkv_fused_splits(w_qkv0.shape[0], w_qkv0.shape[1], B) > 0)
         for l in range(L):
-            srcs = self._linear(st, stats, W[(l, "w_qkv")], self.xn, B)
             kc, vc = self.kv.layer_ptrs(l)
             bias = W.tensor_ptr(l, "b_qkv") if g.qkv_bias else None
             fused = (None, 0, 0, None, None, None)
-            if fuse:
+            if qkv_in_gemm:
+                w = W[(l, "w_qkv")]
+                if "linear" not in self.skip:
+                    nat.check(lib.tps_linear_qkv_rope(w.data_ptr(), w.shape[0], w.shape[1], w.shape[1],
+                                                      self.xn.data_ptr(), B, self.xn.shape[0], self.xn.shape[1],
+                                                      bias, rs, pos, rp, sl.page_table.data_ptr(), sl.max_pages,
+                                                      self.cos.data_ptr(), self.sin.data_ptr(), self.nq, self.nkv,
+                                                      D, PAGE, self.q.data_ptr(), kc, vc, st),
+                              "tps_linear_qkv_rope")
+                    stats.add("linear")
+            elif fuse:
                 # decode: bias + RoPE + KV append are finished inside the attention kernel
+                srcs = self._linear(st, stats, W[(l, "w_qkv")], self.xn, B)
                 fused = (*srcs, bias, self.cos.data_ptr(), self.sin.data_ptr())
-            elif "qkv_rope" not in self.skip:
+            else:
+                srcs = self._linear(st, stats, W[(l, "w_qkv")], self.xn, B)
+            if not qkv_in_gemm and not fuse and "qkv_rope" not in self.skip:
                 # separate bias+RoPE+append launch (always for prefill: many rows of one
                 # sample per launch need every row's K/V appended before attention)
                 nat.check(lib.tps_qkv_rope_append(*srcs, bias, rs, pos, rp,
