@@ -159,6 +159,22 @@ int tps_linear_qkv_rope(const void* w, int64_t n, int64_t k, int64_t ldw, const 
                         const float* cos_t, const float* sin_t, int nq, int nkv, int D, int page_size,
                         void* q_out, void* k_cache, void* v_cache, void* stream);
 
+/* Positions per group of tps_prefill_attention for G query heads per KV head
+ * (min(16, 64 / G); 0 if G > 64). */
+int tps_prefill_group_positions(int G);
+
+/* Chunked-prefill attention by sample group: group y (grid y < max_groups) is the
+ * grp_n[y] rows grp_rows[y * 16 + i] of one sample (same row_slot; grp_n[y] <= 16 and
+ * grp_n[y] * G <= 64; groups numbered densely: the first y with grp_n[y] == 0 ends the
+ * table). One CTA per (group, KV head) streams the
+ * sample's pages once for all its rows; row r attends to tokens 0..row_pos[r] (causal).
+ * out: bf16 [rows][nq][D] for the grouped rows (others untouched). Same result as
+ * tps_paged_attention with row_pos (prefill form) up to fp32 summation order. */
+int tps_prefill_attention(const void* q, const void* k_cache, const void* v_cache, const int* row_slot,
+                          const int* row_pos, const int* grp_rows, const int* grp_n, int max_groups,
+                          const int* page_table, int max_pages, int nq, int nkv, int D, void* out,
+                          void* stream);
+
 /* QKV: sum split partials [s][B][(nq+2nkv)*D] + bias, rotate-half RoPE (fp32
  * cos/sin tables [pos][D/2]), q -> bf16 [B][nq][D], k/v appended at each
  * row's position into the paged cache [page][nkv][64][D]. */

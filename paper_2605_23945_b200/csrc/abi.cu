@@ -50,6 +50,11 @@ int paged_attention(const void*, const void*, const void*, const int*, const int
                     int, int, int, int, int, float*, float*, float*, unsigned int*, void*, const Src&, const void*,
                     const float*, const float*, cudaStream_t);
 int copy_items(const void*, int, int, int, cudaStream_t);
+int prefill_group_positions(int G);
+int paged_prefill_attention(const void* q, const void* k_cache, const void* v_cache, const int* row_slot,
+                            const int* row_pos, const int* grp_rows, const int* grp_n, int max_groups,
+                            const int* page_table, int max_pages, int nq, int nkv, int D, void* out,
+                            cudaStream_t st);
 int configure_gemm();
 int configure_attention();
 int configure_copy();
@@ -66,6 +71,7 @@ int trace_register_decode(uint64_t*, unsigned int*, unsigned int);
 int trace_register_attention(uint64_t*, unsigned int*, unsigned int);
 int trace_register_attention_bal(uint64_t*, unsigned int*, unsigned int);
 int trace_register_gemm(uint64_t*, unsigned int*, unsigned int);
+int trace_register_attention_prefill(uint64_t*, unsigned int*, unsigned int);
 int barrier(uint64_t* const*, int, uint64_t*, uint64_t, cudaStream_t);
 int ipc_get_handle(const void*, void*, int64_t*);
 int ipc_open(const void*, void**);
@@ -199,6 +205,17 @@ int tps_linear_qkv_rope(const void* w, int64_t n, int64_t k, int64_t ldw, const 
   qe.D = D;
   qe.P = page_size;
   return linear_qkv_rope(w, n, k, ldw, x, b, x_rows, ldx, qe, S(stream));
+}
+
+int tps_prefill_group_positions(int G) { return prefill_group_positions(G); }
+
+int tps_prefill_attention(const void* q, const void* k_cache, const void* v_cache, const int* row_slot,
+                          const int* row_pos, const int* grp_rows, const int* grp_n, int max_groups,
+                          const int* page_table, int max_pages, int nq, int nkv, int D, void* out, void* stream) {
+  TPS_CHECK_ARG(q && k_cache && v_cache && row_slot && row_pos && grp_rows && grp_n && page_table && out,
+                "prefill_attention: null pointer");
+  return paged_prefill_attention(q, k_cache, v_cache, row_slot, row_pos, grp_rows, grp_n, max_groups, page_table,
+                                 max_pages, nq, nkv, D, out, S(stream));
 }
 
 int tps_embed(const int* row_slot, const int* pos_by_slot, const int* row_pos, const int* history, int hist_ld,
@@ -361,7 +378,8 @@ int tps_ipc_close(void* base) { return ipc_close(base); }
 int tps_trace_enable(uint64_t* records, unsigned int* counter, unsigned int capacity) {
   TPS_CHECK_ARG((records && counter) || (!records && !counter), "trace: records and counter together");
   if (trace_register_decode(records, counter, capacity) || trace_register_attention(records, counter, capacity) ||
-      trace_register_attention_bal(records, counter, capacity) || trace_register_gemm(records, counter, capacity))
+      trace_register_attention_bal(records, counter, capacity) || trace_register_gemm(records, counter, capacity) ||
+      trace_register_attention_prefill(records, counter, capacity))
     return fail(kCuda, "trace: cudaMemcpyToSymbol failed");
   return kOk;
 }

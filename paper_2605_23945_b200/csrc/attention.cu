@@ -560,9 +560,11 @@ int paged_attention_balanced(const void* q, const void* k_cache, const void* v_c
                              int B, int nq, int nkv, int D, float* part_m, float* part_l, float* part_o,
                              unsigned int* merge_ctr, void* out, cudaStream_t st);
 int configure_attention_balanced();
+int configure_attention_prefill();
 
 int configure_attention() {
   int rc = configure_attention_balanced();
+  if (!rc) rc = configure_attention_prefill();
   if (rc) return rc;
   TPS_CUDA_TRY(cudaFuncSetAttribute(paged_attn_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     attn_smem<128>()));

@@ -41,6 +41,31 @@ def bucket_for(b: int, max_batch: int) -> int:
     return max_batch
 
 
+PREFILL_GROUP_MAX = 16  # positions per group of the grouped prefill attention (tps_prefill_attention)
+
+
+def prefill_groups(row_slot, gp: int) -> tuple[np.ndarray, np.ndarray]:
+    """Group table of a prefill chunk: the rows of each sample (row_slot >= 0) in chunk order,
+    cut into groups of at most `gp` positions -> (rows int32 [R][16] (-1 pad), n int32 [R])."""
+    rs = np.asarray(row_slot, dtype=np.int64)
+    R = len(rs)
+    rows = np.full((R, PREFILL_GROUP_MAX), -1, dtype=np.int32)
+    n = np.zeros(R, dtype=np.int32)
+    open_grp: dict[int, int] = {}
+    ng = 0
+    for i, s in enumerate(rs.tolist()):
+        if s < 0:
+            continue
+        gi = open_grp.get(s)
+        if gi is None or n[gi] >= gp:
+            gi = ng
+            ng += 1
+            open_grp[s] = gi
+        rows[gi, n[gi]] = i
+        n[gi] += 1
+    return rows, n
+
+
 def argmax_chunks(B: int) -> int:
     return max(1, min(64, 296 // max(1, B)))
 
@@ -196,6 +221,14 @@ class InferExecutor:
         self.row_slot = {B: torch.full((B,), -1, dtype=torch.int32, device=dev) for B in sizes}
         self.row_pos = {prefill_rows: torch.zeros(prefill_rows, dtype=torch.int32, device=dev)} \
             if prefill_rows else {}
+        # grouped prefill attention: one CTA per (sample group, KV head) reads the sample's
+        # pages once for all its rows in the chunk (else every row is its own segment)
+        self.group_positions = nat.lib().tps_prefill_group_positions(self.nq // self.nkv) \
+            if self.nq % self.nkv == 0 else 0
+        self.prefill_grouped = self.group_positions > 0
+        if prefill_rows:
+            self.grp_rows = torch.full((prefill_rows, PREFILL_GROUP_MAX), -1, dtype=torch.int32, device=dev)
+            self.grp_n = torch.zeros(prefill_rows, dtype=torch.int32, device=dev)
         self.graphs: dict[int, torch.cuda.CUDAGraph] = {}
         self.launch_stats: dict[int, LaunchStats] = {}
 
@@ -249,6 +282,18 @@ class InferExecutor:
     def _arr(ptrs):
         # host pointer list, consumed (copied into a by-value kernel parameter) by the call
         return nat.ptr_array(ptrs)
+
+    def set_prefill_rows(self, rs: torch.Tensor, rp: torch.Tensor, gp: int = 0) -> None:
+        """Bind a prefill chunk (CPU int32 [prefill_rows] row slots / positions, pinned for an
+        asynchronous copy) and its sample-group table (`gp` positions per group, default this
+        executor's maximum)."""
+        R = self.prefill_rows
+        self.row_slot[R].copy_(rs, non_blocking=True)
+        self.row_pos[R].copy_(rp, non_blocking=True)
+        if self.prefill_grouped:
+            rows, n = prefill_groups(rs.numpy(), gp or self.group_positions)
+            self.grp_rows.copy_(torch.from_numpy(rows).pin_memory(), non_blocking=True)
+            self.grp_n.copy_(torch.from_numpy(n).pin_memory(), non_blocking=True)
 
     # ------------------------------------------------------------ program ---
     def program(self, B: int, st: int, stats: LaunchStats | None = None, prefill: bool = False):
@@ -312,7 +357,13 @@ class InferExecutor:
                                                   self.nkv, D, PAGE, self.q.data_ptr(), kc, vc, st),
                           "tps_qkv_rope_append")
                 stats.add("qkv_rope_append")
-            if "attention" not in self.skip:
+            if "attention" not in self.skip and prefill and self.prefill_grouped:
+                nat.check(lib.tps_prefill_attention(self.q.data_ptr(), kc, vc, rs, rp, self.grp_rows.data_ptr(),
+                                                    self.grp_n.data_ptr(), B, sl.page_table.data_ptr(), sl.max_pages,
+                                                    self.nq, self.nkv, D, self.attn.data_ptr(), st),
+                          "tps_prefill_attention")
+                stats.add("paged_attention")
+            elif "attention" not in self.skip:
                 nat.check(lib.tps_paged_attention(self.q.data_ptr(), kc, vc, rs, pos, rp, sl.page_table.data_ptr(),
                                                   sl.max_pages, B, self.nq, self.nkv, D, nsplit,
                                                   self.att_m.data_ptr(), self.att_l.data_ptr(),
@@ -587,9 +638,9 @@ class GroupRunner:
             rs[:k] = rows_s[k0:k0 + k]
             rp[:k] = rows_p[k0:k0 + k]
             rs, rp = rs.pin_memory(), rp.pin_memory()
+            gp = min(e.group_positions for e in self.ex)
             for e in self.ex:
-                e.row_slot[R].copy_(rs, non_blocking=True)
-                e.row_pos[R].copy_(rp, non_blocking=True)
+                e.set_prefill_rows(rs, rp, gp)
             if self.use_graphs:
                 if key not in self.graphs:
                     self._capture_key(key, lambda st: self._issue_prefill(R, st))

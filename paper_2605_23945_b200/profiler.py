@@ -295,8 +295,7 @@ def profile_rank(geom, tp: int, token_cap: int, max_ctx: int, batches=None, leng
         st.page_table[:nb, :ppl].copy_(pt)
         rs = torch.tensor([i % nb for i in range(R)], dtype=torch.int32)
         rp = torch.tensor([min(ctx, (i // nb) + ctx - (R // nb)) for i in range(R)], dtype=torch.int32)
-        ex.row_slot[R].copy_(rs)
-        ex.row_pos[R].copy_(rp)
+        ex.set_prefill_rows(rs, rp)
         key = ("prefill", R)
         if key not in runner.graphs:
             runner._capture_key(key, lambda s_, rr=runner: rr._issue_prefill(R, s_))

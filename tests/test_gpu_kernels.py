@@ -366,3 +366,50 @@ def test_linear_qkv_rope_in_kernel_finishing(nq, nkv, D, k, b, bias):
         qh = y[i, :nq * D].view(nq, D)
         ref = torch.cat([qh[:, :half] * cos[p] - qh[:, half:] * sin[p], qh[:, half:] * cos[p] + qh[:, :half] * sin[p]], 1)
         assert (qf[i].float() - ref).abs().max().item() <= 2e-2 * (1 + ref.abs().max().item())
+
+
+@pytest.mark.parametrize("D,nq,nkv,nslots,per,ragged", [(128, 28, 4, 8, 8, False), (128, 7, 1, 5, 20, True),
+                                                         (128, 32, 8, 6, 16, True), (64, 4, 4, 9, 3, False),
+                                                         (128, 16, 1, 3, 9, True)])
+def test_grouped_prefill_attention(D, nq, nkv, nslots, per, ragged):
+    """tps_prefill_attention (one CTA per sample group and KV head, per-row causal limits) vs
+    torch fp32, on a position-major chunk with padding rows; groups cut at the executor's
+    positions-per-group limit; rows outside every group stay untouched."""
+    from paper_2605_23945_b200.executor import prefill_groups
+    torch.manual_seed(D + nq + nslots)
+    lib = nat.lib()
+    G = nq // nkv
+    gp = lib.tps_prefill_group_positions(G)
+    assert gp == min(16, 64 // G)
+    base = torch.randint(0, 900, (nslots,)).tolist()
+    n_i = [per - (i % 3 if ragged else 0) for i in range(nslots)]
+    rows_s, rows_p = [], []
+    for j in range(per):
+        for s in range(nslots):
+            if j < n_i[s]:
+                rows_s.append(s)
+                rows_p.append(base[s] + j)
+    R = len(rows_s) + 5
+    rs = torch.tensor(rows_s + [-1] * 5, dtype=torch.int32)
+    rp = torch.tensor(rows_p + [0] * 5, dtype=torch.int32)
+    max_pages = (max(base) + per + 63) // 64 + 1
+    num_pages = nslots * max_pages
+    kc = torch.randn(num_pages, nkv, 64, D, device="cuda").bfloat16()
+    vc = torch.randn(num_pages, nkv, 64, D, device="cuda").bfloat16()
+    perm = torch.randperm(num_pages).view(nslots, max_pages).int()
+    q = torch.randn(R, nq, D, device="cuda").bfloat16()
+    rows, n = prefill_groups(rs.numpy(), gp)
+    assert int(n.sum()) == len(rows_s) and int((n > 0).sum()) >= nslots
+    out = torch.full((R, nq, D), 5.0, device="cuda", dtype=torch.bfloat16)
+    gr, gn = torch.from_numpy(rows).cuda(), torch.from_numpy(n).cuda()
+    rs_d, rp_d, pt_d = rs.cuda(), rp.cuda(), perm.cuda()  # (kept alive across the launch)
+    nat.check(lib.tps_prefill_attention(q.data_ptr(), kc.data_ptr(), vc.data_ptr(), rs_d.data_ptr(),
+                                        rp_d.data_ptr(), gr.data_ptr(), gn.data_ptr(), R,
+                                        pt_d.data_ptr(), max_pages, nq, nkv, D, out.data_ptr(), _stream()))
+    torch.cuda.synchronize()
+    valid = list(range(len(rows_s)))
+    ref = _ref_attention(q.cpu()[valid], kc.cpu(), vc.cpu(), [perm[rows_s[b]].tolist() for b in valid],
+                         [rows_p[b] for b in valid], G)
+    err = (out.float().cpu()[valid] - ref).abs().max().item()
+    assert err < 2e-2, err
+    assert (out[len(rows_s):] == 5.0).all()

@@ -163,3 +163,18 @@ def test_kv_and_history_migration_bit_exact():
                                 n = min(64, ctx[i] - p * 64)
                                 got = mem.view(nb + off, n * D * 2).reshape(n, D * 2)
                                 assert np.array_equal(got, tok[p * 64:p * 64 + n]), (t_old, t_new, i, l, kv, h, p)
+
+
+def test_prefill_group_table():
+    """Host side of the grouped prefill attention: each sample's rows in chunk order, cut at
+    `gp` positions, padding rows in no group, every row in exactly one group."""
+    import numpy as np
+    from paper_2605_23945_b200.executor import prefill_groups
+    rs = np.array([0, 1, 2, 0, 1, 2, 0, 1, -1, 0, 0, 0, 5])
+    rows, n = prefill_groups(rs, 3)
+    assert n.tolist()[:6] == [3, 3, 2, 3, 1, 0]
+    assert rows[0, :3].tolist() == [0, 3, 6] and rows[3, :3].tolist() == [9, 10, 11] and rows[4, 0] == 12
+    got = sorted(int(r) for g in range(len(n)) for r in rows[g, :n[g]])
+    assert got == [i for i in range(len(rs)) if rs[i] >= 0]
+    for g in range(len(n)):
+        assert len({int(rs[r]) for r in rows[g, :n[g]]}) <= 1

@@ -6,7 +6,7 @@ from paper_2605_23945_b200.models import geometry
 from paper_2605_23945_b200.profiler import loopback_rank
 
 KIND = {1: "embed", 2: "add_norm", 3: "reduce_push", 4: "qkv_rope", 5: "silu_mul", 6: "argmax1", 7: "argmax2",
-        8: "epoch", 9: "gemm", 10: "gemm_silu", 11: "attn_split", 12: "attn_combine", 13: "attn_bal"}
+        8: "epoch", 9: "gemm", 10: "gemm_silu", 11: "attn_split", 12: "attn_combine", 13: "attn_bal", 14: "attn_prefill"}
 name = sys.argv[1] if len(sys.argv) > 1 else "qwen2.5-7b"
 ctx = int(sys.argv[2]) if len(sys.argv) > 2 else 256
 R = 512
@@ -18,8 +18,7 @@ ppl = (ctx + 64) // 64 + 1
 r.slots.page_table[:nb, :ppl].copy_(torch.arange(nb * ppl, dtype=torch.int32).view(nb, ppl))
 rs = torch.tensor([i % nb for i in range(R)], dtype=torch.int32)
 rp = torch.tensor([ctx - R // nb + i // nb for i in range(R)], dtype=torch.int32)
-ex.row_slot[R].copy_(rs)
-ex.row_pos[R].copy_(rp)
+ex.set_prefill_rows(rs, rp)
 key = ("prefill", R)
 runner._capture_key(key, lambda s_: runner._issue_prefill(R, s_))
 g = runner.graphs[key]
