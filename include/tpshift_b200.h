@@ -149,6 +149,19 @@ int tps_reduce_push_ll(const float* src, int nsrc, int64_t src_stride, uint64_t*
  * shape does not take the fused form (b > 64, more tiles x splits than SMs, ...). */
 int tps_qkv_fused_splits(int64_t n, int64_t k, int64_t b);
 
+/* Split count of tps_linear_push_ll_cluster for [n x k] at batch b (0: not supported:
+ * b > 64 or more tiles than SMs). */
+int tps_cluster_splits(int64_t n, int64_t k, int64_t b);
+
+/* Row-parallel projection + allreduce push with the split-K reduction inside the kernel:
+ * the split CTAs of a weight tile form one cluster and sum their partials over DSMEM (split
+ * order), then out[i][j] goes to every destination as ONE uint64 {fp32 bits, tag} at
+ * dsts[d] + i * n + j (tag = (*epoch) * tag_mult + tag_add): the tp-source consumer is
+ * tps_add_norm_ll, as after tps_reduce_push_ll. */
+int tps_linear_push_ll_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,
+                               int64_t x_rows, int64_t ldx, uint64_t* const* dsts, int ndst,
+                               const uint64_t* epoch, uint32_t tag_mult, uint32_t tag_add, void* stream);
+
 /* QKV projection finished in-kernel: out = W x (split-K over a thread-block cluster, the
  * partials summed over DSMEM in split order) + bias, RoPE, q -> bf16 [b][nq][D], k/v
  * appended into the paged cache -- the results of tps_linear + tps_qkv_rope_append in

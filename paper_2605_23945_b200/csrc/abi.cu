@@ -30,6 +30,10 @@ int linear_silu(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x,
 int linear(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
            int64_t ldx, float* out, int splits, cudaStream_t stream);
 int qkv_fused_splits(int64_t n, int64_t k, int64_t b);
+int cluster_splits(int64_t n, int64_t k, int64_t b);
+int linear_push_ll_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,
+                           int64_t x_rows, int64_t ldx, const DstList& dst, const uint64_t* tag_epoch,
+                           uint32_t tag_mult, uint32_t tag_add, cudaStream_t stream);
 int linear_qkv_rope(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
                     int64_t ldx, const QkvEpi& qe, cudaStream_t stream);
 int embed(const int*, const int*, const int*, const int*, int, const void*, int, int, float*, cudaStream_t);
@@ -181,6 +185,18 @@ int tps_linear_silu(const void* w, int64_t n, int64_t k, int64_t ldw, const void
 }
 
 int tps_qkv_fused_splits(int64_t n, int64_t k, int64_t b) { return qkv_fused_splits(n, k, b); }
+
+int tps_cluster_splits(int64_t n, int64_t k, int64_t b) { return cluster_splits(n, k, b); }
+
+int tps_linear_push_ll_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,
+                               int64_t x_rows, int64_t ldx, uint64_t* const* dsts, int ndst, const uint64_t* epoch,
+                               uint32_t tag_mult, uint32_t tag_add, void* stream) {
+  TPS_CHECK_ARG(ndst >= 1 && ndst <= kMaxPeers && dsts, "linear_push_ll_cluster: 1..8 destinations");
+  DstList dl;
+  dl.n = ndst;
+  for (int i = 0; i < ndst; ++i) dl.p[i] = reinterpret_cast<float*>(dsts[i]);
+  return linear_push_ll_cluster(w, n, k, ldw, x, b, x_rows, ldx, dl, epoch, tag_mult, tag_add, S(stream));
+}
 
 int tps_linear_qkv_rope(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
                         int64_t ldx, const void* bias, const int* row_slot, const int* pos_by_slot,

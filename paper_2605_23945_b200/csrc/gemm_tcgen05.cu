@@ -109,12 +109,48 @@ constexpr int kEpiSiluMul = 1;
 // RoPE at each row's position and writes q (bf16) and the new k/v into the paged cache.
 // This replaces tps_qkv_rope_append (one launch + its PDL boundary per layer).
 constexpr int kEpiQkvRope = 2;
+// kEpiClusterLL: row-parallel projection + TP allreduce push. The split-K CTAs of a tile
+// (one cluster) sum their partials over DSMEM in split order and push ONE LL {value, tag}
+// pair per element to every peer (tps_linear_push_ll pushes every split partial: S x the
+// NVLink bytes and tp x S sources for the consumer; tps_reduce_push_ll needs a launch).
+constexpr int kEpiClusterLL = 3;
+constexpr bool cluster_epi(int epi) { return epi == kEpiQkvRope || epi == kEpiClusterLL; }
 
 
 namespace cg = cooperative_groups;
 
 // Finishing of kEpiQkvRope (all 256 threads of every CTA of the cluster).
 // part: this CTA's [BN][128] fp32 tile partial (row j = token row, column r = weight row).
+// Finishing of kEpiClusterLL: CTA s of S sums columns [s*128/S, (s+1)*128/S) of the tile.
+template <int BN>
+__device__ __forceinline__ void cluster_ll_finish(const float* part, const DstList& dst, uint64_t tag, int tile,
+                                                  int N, int rows) {
+  cg::cluster_group cl = cg::this_cluster();
+  cl.sync();  // every split's partial tile is parked in its CTA's smem
+  const int S = (int)cl.num_blocks();
+  const int rank = (int)cl.block_rank();
+  const int r0 = rank * kBM / S, r1 = (rank + 1) * kBM / S;
+  const int nr = r1 - r0;
+  const float* rp[16];
+#pragma unroll
+  for (int s = 0; s < 16; ++s) rp[s] = s < S ? cl.map_shared_rank(part, s) : part;
+  for (int it = threadIdx.x; it < nr * rows; it += kGemmThreads) {
+    const int r = r0 + it % nr, j = it / nr;
+    const int n = tile * kBM + r;
+    if (n >= N) continue;
+    float v[16];
+#pragma unroll
+    for (int s = 0; s < 16; ++s)
+      if (s < S) v[s] = rp[s][j * kBM + r];
+    float x = 0.f;  // split order, from 0 (as tps_reduce_push_ll)
+#pragma unroll
+    for (int s = 0; s < 16; ++s)
+      if (s < S) x += v[s];
+    for (int d = 0; d < dst.n; ++d)
+      st_relaxed_sys_u64(reinterpret_cast<uint64_t*>(dst.p[d]) + (size_t)j * N + n, tag | __float_as_uint(x));
+  }
+}
+
 template <int BN>
 __device__ __forceinline__ void qkv_finish(const float* part, const QkvEpi& e, int tile, int N, int rows) {
   __shared__ int s_pos[BN], s_slot[BN], s_page[BN];
@@ -192,7 +228,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                        const uint64_t* __restrict__ tag_epoch, uint32_t tag_mult, uint32_t tag_add,
                        const __grid_constant__ QkvEpi qkv) {
   using Cfg = GemmCfg<BN>;
-  constexpr int S = EPI == kEpiQkvRope ? Cfg::kQkvStages : Cfg::kStages;
+  constexpr int S = cluster_epi(EPI) ? Cfg::kQkvStages : Cfg::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_a = smem;
@@ -373,7 +409,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
           }
         }
-      } else if constexpr (EPI == kEpiQkvRope) {
+      } else if constexpr (cluster_epi(EPI)) {
         // one unit per CTA: its MMAs (and so every smem read of the ring) are complete
         float* part = reinterpret_cast<float*>(smem);
         const int r = q * 32 + lane;
@@ -426,6 +462,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     qkv_finish<BN>(reinterpret_cast<const float*>(smem), qkv, (int)blockIdx.x / (int)cg::this_cluster().num_blocks(),
                    N, B);
     cg::this_cluster().sync();  // keep this smem alive until the cluster has read it
+  }
+  if constexpr (EPI == kEpiClusterLL) {
+    pdl_wait();  // (every thread: the pushes overwrite LL slots the predecessor chain consumed)
+    const uint64_t tag = (uint64_t)((uint32_t)(*(volatile const uint64_t*)tag_epoch * tag_mult + tag_add)) << 32;
+    cluster_ll_finish<BN>(reinterpret_cast<const float*>(smem), dst, tag,
+                          (int)blockIdx.x / (int)cg::this_cluster().num_blocks(), N, B);
+    cg::this_cluster().sync();
   }
   if (warp == 2) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
@@ -538,7 +581,7 @@ static int launch_gemm(const CUtensorMap& mw, const CUtensorMap& mx, const EpiAr
   const int acts = (b + BN - 1) / BN;
   const int units = tiles * splits * acts;
   const int grid = units < kNumSMs ? units : kNumSMs;
-  if constexpr (EPI == kEpiQkvRope)  // one unit per CTA, the splits of a tile in one cluster
+  if constexpr (cluster_epi(EPI))  // one unit per CTA, the splits of a tile in one cluster
     return launch_kcs(gemm_swapab_kernel<BN, EPI>, dim3(units), dim3(kGemmThreads), splits, Cfg::kQkvSmemBytes,
                       stream, true, mw, mx, e.dst, e.split_stride, n, b, tiles, splits, chunks, acts, e.act_out,
                       e.ld_act, e.sig, e.tag_epoch, e.tag_mult, e.tag_add, e.qkv);
@@ -561,6 +604,11 @@ static int configure_one() {
     TPS_CUDA_TRY(cudaFuncSetAttribute(gemm_swapab_kernel<BN, kEpiQkvRope>,
                                       cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     TPS_MAX_CARVEOUT((gemm_swapab_kernel<BN, kEpiQkvRope>));
+    TPS_CUDA_TRY(cudaFuncSetAttribute(gemm_swapab_kernel<BN, kEpiClusterLL>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN>::kQkvSmemBytes));
+    TPS_CUDA_TRY(cudaFuncSetAttribute(gemm_swapab_kernel<BN, kEpiClusterLL>,
+                                      cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    TPS_MAX_CARVEOUT((gemm_swapab_kernel<BN, kEpiClusterLL>));
   }
   return kOk;
 }
@@ -585,9 +633,9 @@ static int g_qkv_cluster = [] {
 // Split count of the in-kernel-finished QKV projection, 0 when the shape does not take it:
 // b <= 64 (one activation tile), every (tile, split) unit on its own SM (one wave), the
 // splits of a tile within one cluster.
-int qkv_fused_splits(int64_t n, int64_t k, int64_t b) {
-  if (g_qkv_cluster <= 0 || b < 1 || b > 64 || n % kBM) return 0;
-  const int64_t tiles = n / kBM;
+int cluster_splits(int64_t n, int64_t k, int64_t b) {
+  if (g_qkv_cluster <= 0 || b < 1 || b > 64) return 0;
+  const int64_t tiles = (n + kBM - 1) / kBM;
   const int64_t chunks = (k + kBK - 1) / kBK;
   if (tiles > kNumSMs) return 0;
   int s = linear_splits(n, k, b);
@@ -597,6 +645,8 @@ int qkv_fused_splits(int64_t n, int64_t k, int64_t b) {
   if (s > cap) s = cap;
   return s >= 1 ? s : 0;
 }
+
+int qkv_fused_splits(int64_t n, int64_t k, int64_t b) { return n % kBM ? 0 : cluster_splits(n, k, b); }
 
 template <int EPI>
 static int dispatch(int bn, const CUtensorMap& mw, const CUtensorMap& mx, const EpiArgs& e, int n, int b, int tiles,
@@ -718,6 +768,31 @@ int linear_qkv_rope(const void* w, int64_t n, int64_t k, int64_t ldw, const void
     case 16: return launch_gemm<16, kEpiQkvRope>(mw, mx, e, (int)n, (int)b, tiles, splits, (int)chunks, stream);
     case 32: return launch_gemm<32, kEpiQkvRope>(mw, mx, e, (int)n, (int)b, tiles, splits, (int)chunks, stream);
     default: return launch_gemm<64, kEpiQkvRope>(mw, mx, e, (int)n, (int)b, tiles, splits, (int)chunks, stream);
+  }
+}
+
+// Row-parallel projection with the split-K reduction inside a cluster and one LL pair per
+// element pushed to every destination at i * n + j (tag = (*tag_epoch) * tag_mult + tag_add).
+int linear_push_ll_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,
+                           int64_t x_rows, int64_t ldx, const DstList& dst, const uint64_t* tag_epoch,
+                           uint32_t tag_mult, uint32_t tag_add, cudaStream_t stream) {
+  const int splits = cluster_splits(n, k, b);
+  TPS_CHECK_ARG(splits >= 1, "linear_push_ll_cluster: shape not supported (see tps_cluster_splits)");
+  TPS_CHECK_ARG(dst.n >= 1 && dst.n <= kMaxPeers && tag_epoch, "linear_push_ll_cluster: 1..8 destinations, epoch");
+  for (int d = 0; d < dst.n; ++d)
+    TPS_CHECK_ARG((reinterpret_cast<uintptr_t>(dst.p[d]) & 7) == 0, "linear_push_ll_cluster: 8B-aligned slots");
+  const int64_t chunks = (k + kBK - 1) / kBK;
+  CUtensorMap mw, mx;
+  int bn;
+  int rc = prepare(w, n, k, ldw, x, b, x_rows, ldx, &mw, &mx, &bn);
+  if (rc) return rc;
+  EpiArgs e{dst, 0, nullptr, 0, SignalSpec{}, tag_epoch, tag_mult, tag_add};
+  e.sig.n = 0;
+  const int tiles = (int)((n + kBM - 1) / kBM);
+  switch (bn) {
+    case 16: return launch_gemm<16, kEpiClusterLL>(mw, mx, e, (int)n, (int)b, tiles, splits, (int)chunks, stream);
+    case 32: return launch_gemm<32, kEpiClusterLL>(mw, mx, e, (int)n, (int)b, tiles, splits, (int)chunks, stream);
+    default: return launch_gemm<64, kEpiClusterLL>(mw, mx, e, (int)n, (int)b, tiles, splits, (int)chunks, stream);
   }
 }
 

@@ -21,6 +21,7 @@ once into a CUDA graph and replayed for every round of a block.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -74,6 +75,9 @@ FUSE_ROWS = 64     # tail batches (B <= FUSE_ROWS) exchange the TP allreduce as 
 LL_EPILOGUE_ROWS = 16  # ... from the projection epilogue (every split partial) up to this batch; above it
                        # a reduce kernel sums the splits first (S x fewer NVLink bytes; the crossover of
                        # the extra launch vs the modeled NVLink bytes is ~16 rows at TP8)
+# B <= LL_CLUSTER_ROWS: the projection's split-K CTAs reduce over DSMEM inside the kernel and
+# push one LL pair per element (tps_linear_push_ll_cluster; supersedes both forms above)
+LL_CLUSTER_ROWS = int(os.environ.get("TPS_LL_CLUSTER_ROWS", "64"))
 FUSE_SOURCES = 16  # LL slots per parity: tp x splits partials of one fused allreduce (one load batch)
 
 
@@ -472,7 +476,14 @@ class InferExecutor:
         par = phase % 2
         # LL: {value, tag} stores polled by the consumer; tag = epoch * n_phases + phase
         # (a loopback timing rank -- profiler.loopback_rank -- fills every rank's slots itself)
-        if B <= LL_EPILOGUE_ROWS:
+        if B <= LL_CLUSTER_ROWS and lib.tps_cluster_splits(n, k, B) > 0:
+            S = 1  # one reduced slot per rank
+            dsts = [cm.ll_slot(base, par, q if cm.loopback else self.rank, 1) for q, base in enumerate(cm.peer_ll)]
+            nat.check(lib.tps_linear_push_ll_cluster(w.data_ptr(), n, k, k, x.data_ptr(), B, x.shape[0], x.shape[1],
+                                                     self._arr(dsts), len(dsts), cm.epoch.data_ptr(), cm.n_phases,
+                                                     phase, st), "tps_linear_push_ll_cluster")
+            stats.add("linear")
+        elif B <= LL_EPILOGUE_ROWS:
             S = self.fused_splits(fam, B)
             dsts = [cm.ll_slot(base, par, q if cm.loopback else self.rank, S) for q, base in enumerate(cm.peer_ll)]
             nat.check(lib.tps_linear_push_ll(w.data_ptr(), n, k, k, x.data_ptr(), B, x.shape[0], x.shape[1],

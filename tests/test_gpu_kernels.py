@@ -413,3 +413,35 @@ def test_grouped_prefill_attention(D, nq, nkv, nslots, per, ragged):
     err = (out.float().cpu()[valid] - ref).abs().max().item()
     assert err < 2e-2, err
     assert (out[len(rows_s):] == 5.0).all()
+
+
+@pytest.mark.parametrize("n,k,b,ndst", [(3584, 2368, 1, 8), (3584, 512, 16, 8), (256, 128, 7, 2), (3584, 4736, 64, 4),
+                                        (4096, 1792, 33, 8)])
+def test_linear_push_ll_cluster(n, k, b, ndst):
+    """tps_linear_push_ll_cluster: the split partials summed over DSMEM in split order equal
+    tps_linear (same split count) + an in-order sum, bit for bit, in every destination as
+    {value, tag}; rows >= b untouched."""
+    lib = nat.lib()
+    S = lib.tps_cluster_splits(n, k, b)
+    assert S >= 1
+    torch.manual_seed(n + k + b)
+    w = (torch.randn(n, k, device="cuda") * 0.05).bfloat16()
+    x = torch.randn(b, k, device="cuda").bfloat16()
+    ws = torch.zeros(S, b, n, device="cuda")
+    nat.check(lib.tps_linear(w.data_ptr(), n, k, k, x.data_ptr(), b, b, k, ws.data_ptr(), S, _stream()))
+    ref = torch.zeros(b, n, device="cuda")
+    for s in range(S):
+        ref += ws[s]
+    epoch = torch.tensor([5], dtype=torch.int64, device="cuda")
+    slots = [torch.full((b + 2, n), -1, dtype=torch.int64, device="cuda") for _ in range(ndst)]
+    nat.check(lib.tps_linear_push_ll_cluster(w.data_ptr(), n, k, k, x.data_ptr(), b, b, k,
+                                             nat.ptr_array([t.data_ptr() for t in slots]), ndst, epoch.data_ptr(),
+                                             3, 1, _stream()))
+    torch.cuda.synchronize()
+    for t in slots:
+        u = t[:b].cpu()
+        tags = (u >> 32) & 0xFFFFFFFF
+        assert (tags == 5 * 3 + 1).all()
+        vals = (u & 0xFFFFFFFF).to(torch.int32).view(torch.float32)
+        assert torch.equal(vals, ref.cpu())
+        assert (t[b:] == -1).all()
