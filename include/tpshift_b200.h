@@ -153,6 +153,11 @@ int tps_qkv_fused_splits(int64_t n, int64_t k, int64_t b);
  * b > 64 or more tiles than SMs). */
 int tps_cluster_splits(int64_t n, int64_t k, int64_t b);
 
+/* out[i][j] = (W x_i)_j as ONE fp32 [b][n] result: the split-K CTAs of a tile (one cluster)
+ * reduce their partials over DSMEM in split order (tps_linear's partials summed in-kernel). */
+int tps_linear_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,
+                       int64_t x_rows, int64_t ldx, float* out, void* stream);
+
 /* Row-parallel projection + allreduce push with the split-K reduction inside the kernel:
  * the split CTAs of a weight tile form one cluster and sum their partials over DSMEM (split
  * order), then out[i][j] goes to every destination as ONE uint64 {fp32 bits, tag} at

@@ -31,6 +31,8 @@ int linear(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int6
            int64_t ldx, float* out, int splits, cudaStream_t stream);
 int qkv_fused_splits(int64_t n, int64_t k, int64_t b);
 int cluster_splits(int64_t n, int64_t k, int64_t b);
+int linear_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
+                   int64_t ldx, float* out, cudaStream_t stream);
 int linear_push_ll_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,
                            int64_t x_rows, int64_t ldx, const DstList& dst, const uint64_t* tag_epoch,
                            uint32_t tag_mult, uint32_t tag_add, cudaStream_t stream);
@@ -187,6 +189,11 @@ int tps_linear_silu(const void* w, int64_t n, int64_t k, int64_t ldw, const void
 int tps_qkv_fused_splits(int64_t n, int64_t k, int64_t b) { return qkv_fused_splits(n, k, b); }
 
 int tps_cluster_splits(int64_t n, int64_t k, int64_t b) { return cluster_splits(n, k, b); }
+
+int tps_linear_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
+                       int64_t ldx, float* out, void* stream) {
+  return linear_cluster(w, n, k, ldw, x, b, x_rows, ldx, out, S(stream));
+}
 
 int tps_linear_push_ll_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,
                                int64_t x_rows, int64_t ldx, uint64_t* const* dsts, int ndst, const uint64_t* epoch,

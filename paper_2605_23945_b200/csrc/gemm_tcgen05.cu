@@ -146,8 +146,11 @@ __device__ __forceinline__ void cluster_ll_finish(const float* part, const DstLi
 #pragma unroll
     for (int s = 0; s < 16; ++s)
       if (s < S) x += v[s];
-    for (int d = 0; d < dst.n; ++d)
-      st_relaxed_sys_u64(reinterpret_cast<uint64_t*>(dst.p[d]) + (size_t)j * N + n, tag | __float_as_uint(x));
+    if (tag)
+      for (int d = 0; d < dst.n; ++d)
+        st_relaxed_sys_u64(reinterpret_cast<uint64_t*>(dst.p[d]) + (size_t)j * N + n, tag | __float_as_uint(x));
+    else
+      dst.p[0][(size_t)j * N + n] = x;  // local fp32 result (tps_linear_cluster)
   }
 }
 
@@ -465,7 +468,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
   if constexpr (EPI == kEpiClusterLL) {
     pdl_wait();  // (every thread: the pushes overwrite LL slots the predecessor chain consumed)
-    const uint64_t tag = (uint64_t)((uint32_t)(*(volatile const uint64_t*)tag_epoch * tag_mult + tag_add)) << 32;
+    const uint64_t tag =
+        tag_epoch ? (uint64_t)((uint32_t)(*(volatile const uint64_t*)tag_epoch * tag_mult + tag_add)) << 32 : 0ull;
     cluster_ll_finish<BN>(reinterpret_cast<const float*>(smem), dst, tag,
                           (int)blockIdx.x / (int)cg::this_cluster().num_blocks(), N, B);
     cg::this_cluster().sync();
@@ -787,6 +791,29 @@ int linear_push_ll_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, con
   int rc = prepare(w, n, k, ldw, x, b, x_rows, ldx, &mw, &mx, &bn);
   if (rc) return rc;
   EpiArgs e{dst, 0, nullptr, 0, SignalSpec{}, tag_epoch, tag_mult, tag_add};
+  e.sig.n = 0;
+  const int tiles = (int)((n + kBM - 1) / kBM);
+  switch (bn) {
+    case 16: return launch_gemm<16, kEpiClusterLL>(mw, mx, e, (int)n, (int)b, tiles, splits, (int)chunks, stream);
+    case 32: return launch_gemm<32, kEpiClusterLL>(mw, mx, e, (int)n, (int)b, tiles, splits, (int)chunks, stream);
+    default: return launch_gemm<64, kEpiClusterLL>(mw, mx, e, (int)n, (int)b, tiles, splits, (int)chunks, stream);
+  }
+}
+
+// fp32 result [b][n] (the split-K partials reduced over DSMEM inside the kernel, split order):
+// the same sums a consumer of tps_linear's partials forms, without the partial traffic.
+int linear_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
+                   int64_t ldx, float* out, cudaStream_t stream) {
+  const int splits = cluster_splits(n, k, b);
+  TPS_CHECK_ARG(splits >= 1 && out, "linear_cluster: shape not supported (see tps_cluster_splits)");
+  const int64_t chunks = (k + kBK - 1) / kBK;
+  CUtensorMap mw, mx;
+  int bn;
+  int rc = prepare(w, n, k, ldw, x, b, x_rows, ldx, &mw, &mx, &bn);
+  if (rc) return rc;
+  EpiArgs e{};
+  e.dst.n = 1;
+  e.dst.p[0] = out;
   e.sig.n = 0;
   const int tiles = (int)((n + kBM - 1) / kBM);
   switch (bn) {

@@ -178,6 +178,10 @@ class InferExecutor:
         # (TP1 B=64 ctx 2048 4.475 vs 4.465 ms, TP8 B=1 1.418 vs 1.392: the separate finishing
         # launch is already hidden under attention's early KV stream): off by default
         self.qkv_in_gemm = False
+        # every split-K projection at B <= 64 with its partials reduced in-kernel (tps_linear_cluster;
+        # measured slower for column-parallel / TP1 projections: TP1 B=64 4.465 -> 4.838 ms, the
+        # 4-stage ring of the cluster form costs more than the partial traffic it saves): off
+        self.cluster_linear = os.environ.get("TPS_CLUSTER_LINEAR", "0") == "1"
         # launch kinds left out of the step program (timing probes only: results are garbage)
         self.skip: frozenset = frozenset()
         # 0: greedy; > 0: Gumbel-max sampling at this temperature with the slots' Philox keys
@@ -274,6 +278,12 @@ class InferExecutor:
     def _linear(self, st, stats, w: torch.Tensor, x: torch.Tensor, B: int) -> tuple[int, int, int]:
         """Projection into the split-K workspace; returns the strided source (base, n, stride)."""
         n, k = w.shape
+        if self.cluster_linear and "linear" not in self.skip and nat.lib().tps_cluster_splits(n, k, B) > 0:
+            # split-K reduced inside the kernel: consumers read one fp32 result
+            nat.check(nat.lib().tps_linear_cluster(w.data_ptr(), n, k, k, x.data_ptr(), B, x.shape[0], x.shape[1],
+                                                   self.ws.data_ptr(), st), "tps_linear_cluster")
+            stats.add("linear")
+            return (self.ws.data_ptr(), 1, B * n)
         s = self._splits(n, k, B)
         if "linear" in self.skip:
             return (self.ws.data_ptr(), s, B * n)

@@ -445,3 +445,8 @@ def test_linear_push_ll_cluster(n, k, b, ndst):
         vals = (u & 0xFFFFFFFF).to(torch.int32).view(torch.float32)
         assert torch.equal(vals, ref.cpu())
         assert (t[b:] == -1).all()
+    # the local fp32 form (tps_linear_cluster): the same in-order sums
+    out = torch.full((b + 2, n), 7.0, device="cuda")
+    nat.check(lib.tps_linear_cluster(w.data_ptr(), n, k, k, x.data_ptr(), b, b, k, out.data_ptr(), _stream()))
+    torch.cuda.synchronize()
+    assert torch.equal(out[:b], ref) and (out[b:] == 7.0).all()
