@@ -371,6 +371,12 @@ constexpr int kInKernelMergeMaxSplits = 4;
 // its (max, sum, O) softmax state in shared memory; after a cluster barrier every CTA merges
 // a slice of the G x D output straight out of its peers' shared memory (DSMEM) -- no
 // global partials, atomics or second kernel on the critical path of a 1..16-row step.
+// TPS_ATTN_CLUSTER_EARLY=1: the cluster form streams its first pages before the PDL wait
+// (TP8 B=1 1.330 -> 1.287 ms). Off: graph-replayed decode then diverges from eager decode
+// from the first generated token on, at TP1 too (tools/graph_probe.py), while eager decode
+// matches the oracle -- not understood yet.
+__device__ int g_cluster_early = 0;
+
 template <int D>
 __global__ void __launch_bounds__(kAttnThreads) paged_attn_cluster_kernel(
     const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k_cache,
@@ -397,7 +403,7 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_cluster_kernel(
   // (streaming pages before the wait, as the split kernel does, broke graph-replayed TP2
   // decode in this cluster form -- tests/test_gpu_decode.py::test_graph_replay_matches_eager;
   // kept off until understood)
-  const bool decode = row_pos == nullptr && early_ok && false;
+  const bool decode = row_pos == nullptr && early_ok && g_cluster_early;
   if (!decode) pdl_wait();  // prefill rows of this chunk were appended by the previous kernel
   // decode: positions, page tables and every cached token but the current one were written by
   // earlier steps, so the first pages stream before the programmatic wait; the current
@@ -563,6 +569,11 @@ int configure_attention_balanced();
 int configure_attention_prefill();
 
 int configure_attention() {
+  {
+    const char* e = getenv("TPS_ATTN_CLUSTER_EARLY");
+    const int v = e ? atoi(e) : 0;
+    TPS_CUDA_TRY(cudaMemcpyToSymbol(g_cluster_early, &v, sizeof(int)));
+  }
   int rc = configure_attention_balanced();
   if (!rc) rc = configure_attention_prefill();
   if (rc) return rc;
@@ -607,6 +618,13 @@ static int g_max_cluster = [] {
   return e ? atoi(e) : 8;
 }();
 
+// TPS_ATTN_CLUSTER_SIZE=<n>: CTAs per segment of the cluster form (default 16; 2..16)
+static int g_cluster_size = [] {
+  const char* e = getenv("TPS_ATTN_CLUSTER_SIZE");
+  const int v = e ? atoi(e) : 16;
+  return v < 2 ? 2 : (v > 16 ? 16 : v);
+}();
+
 int attn_splits(int B, int nkv, int max_pages) {
   // page-balanced when the (row, kv head) segments give enough parallel work, and for a
   // single local KV head (TP-sharded GQA tail: measured faster than split + combine)
@@ -648,7 +666,7 @@ int paged_attention(const void* q, const void* k_cache, const void* v_cache, con
   TPS_CHECK_ARG(nsplit >= 0 || B * nkv <= 65535, "paged_attention: too many segments for the cluster form");
   if (nsplit < 0) {
     // cluster kernel (tail batches): 16 CTAs per segment when there are few segments
-    const int cl = 16;  // (non-portable size: 16 CTAs of <= 2 per SM per cluster)
+    const int cl = g_cluster_size;  // (non-portable size 16: 16 CTAs of <= 2 per SM per cluster)
     const float scale = 1.4426950408889634f / sqrtf((float)D);
     const auto* qq = reinterpret_cast<const __nv_bfloat16*>(q);
     const auto* kk = reinterpret_cast<const __nv_bfloat16*>(k_cache);

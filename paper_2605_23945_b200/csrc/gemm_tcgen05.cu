@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* tmem_empty = bars + 2 * S + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
 
-  const unsigned int trs = trace_begin(EPI == kEpiPartial ? kTrGemm : kTrGemmSilu);
+  const unsigned int trs = trace_begin(EPI == kEpiSiluMul ? kTrGemmSilu : EPI == kEpiClusterLL ? kTrGemmPush : kTrGemm);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   // unit u = ((tile * splits + split) * acts + act): the activation tiles of one weight
