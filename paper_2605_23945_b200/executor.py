@@ -78,6 +78,10 @@ LL_EPILOGUE_ROWS = 16  # ... from the projection epilogue (every split partial) 
 # B <= LL_CLUSTER_ROWS: the projection's split-K CTAs reduce over DSMEM inside the kernel and
 # push one LL pair per element (tps_linear_push_ll_cluster; supersedes both forms above)
 LL_CLUSTER_ROWS = int(os.environ.get("TPS_LL_CLUSTER_ROWS", "64"))
+# ... at TP >= 4 (TP2 shards are large enough that the one-wave cluster split -- 4-stage ring,
+# S <= 148 / tiles -- streams slower than the 8-stage per-partial form: Qwen2.5-32B fixed TP2
+# stage 63.4 -> 65.5 s predicted; Qwen2.5-7B TP2 B <= 32 +2-3 % in loopback)
+LL_CLUSTER_MIN_TP = 4
 FUSE_SOURCES = 16  # LL slots per parity: tp x splits partials of one fused allreduce (one load batch)
 
 
@@ -486,7 +490,7 @@ class InferExecutor:
         par = phase % 2
         # LL: {value, tag} stores polled by the consumer; tag = epoch * n_phases + phase
         # (a loopback timing rank -- profiler.loopback_rank -- fills every rank's slots itself)
-        if B <= LL_CLUSTER_ROWS and lib.tps_cluster_splits(n, k, B) > 0:
+        if B <= LL_CLUSTER_ROWS and cm.tp >= LL_CLUSTER_MIN_TP and lib.tps_cluster_splits(n, k, B) > 0:
             S = 1  # one reduced slot per rank
             dsts = [cm.ll_slot(base, par, q if cm.loopback else self.rank, 1) for q, base in enumerate(cm.peer_ll)]
             nat.check(lib.tps_linear_push_ll_cluster(w.data_ptr(), n, k, k, x.data_ptr(), B, x.shape[0], x.shape[1],

@@ -237,11 +237,11 @@ def nvlink_adjust(geom, tp: int, batch: int) -> float:
     of the 2L allreduces one NVLink hop plus the bytes this rank pushes to its tp-1 peers."""
     if tp == 1:
         return 0.0
-    from .executor import FUSE_ROWS, FUSE_SOURCES, LL_CLUSTER_ROWS, LL_EPILOGUE_ROWS
+    from .executor import FUSE_ROWS, FUSE_SOURCES, LL_CLUSTER_MIN_TP, LL_CLUSTER_ROWS, LL_EPILOGUE_ROWS
     # B <= 64: LL pairs (8 B per element) of the summed row (cluster-reduced epilogue or
     # reduce-push); else B <= 16: of every split partial (<= FUSE_SOURCES slots per group);
     # larger: the summed fp32 row (reduce-push)
-    if batch <= min(LL_CLUSTER_ROWS, FUSE_ROWS):
+    if batch <= min(LL_CLUSTER_ROWS, FUSE_ROWS) and tp >= LL_CLUSTER_MIN_TP:
         per_row = geom.hidden * 8 * (tp - 1)
     elif batch <= LL_EPILOGUE_ROWS:
         per_row = geom.hidden * 8 * (tp - 1) * max(1, FUSE_SOURCES // tp)
