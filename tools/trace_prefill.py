@@ -1,4 +1,6 @@
-"""Dev probe: in-chain timeline of one chunked-prefill step (512 rows) on one rank."""
+"""Dev probe: in-chain timeline of one chunked-prefill step (512 rows) on one rank.
+
+python tools/trace_prefill.py <model> <ctx> [tp]  (tp > 1: loopback rank, tools/solo_step.py)"""
 import collections, sys, torch
 sys.path.insert(0, ".")
 from paper_2605_23945_b200 import _native as nat
@@ -9,10 +11,11 @@ KIND = {1: "embed", 2: "add_norm", 3: "reduce_push", 4: "qkv_rope", 5: "silu_mul
         8: "epoch", 9: "gemm", 10: "gemm_silu", 11: "attn_split", 12: "attn_combine", 13: "attn_bal", 14: "attn_prefill", 15: "gemm_push"}
 name = sys.argv[1] if len(sys.argv) > 1 else "qwen2.5-7b"
 ctx = int(sys.argv[2]) if len(sys.argv) > 2 else 256
+tp = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 R = 512
 geom = geometry(name)
 nb = 64
-r, runner = loopback_rank(geom, 1, nb, nb, ctx + 256, nb * ((ctx + 256) // 64 + 2), prefill_rows=R)
+r, runner = loopback_rank(geom, tp, nb, nb, ctx + 256, nb * ((ctx + 256) // 64 + 2), prefill_rows=R)
 ex = r.executor
 ppl = (ctx + 64) // 64 + 1
 r.slots.page_table[:nb, :ppl].copy_(torch.arange(nb * ppl, dtype=torch.int32).view(nb, ppl))
