@@ -373,8 +373,10 @@ constexpr int kInKernelMergeMaxSplits = 4;
 // global partials, atomics or second kernel on the critical path of a 1..16-row step.
 // TPS_ATTN_CLUSTER_EARLY=1: the cluster form streams its first pages before the PDL wait
 // (TP8 B=1 1.330 -> 1.287 ms). Off: graph-replayed decode then diverges from eager decode
-// from the first generated token on, at TP1 too (tools/graph_probe.py), while eager decode
-// matches the oracle -- not understood yet.
+// from the first generated token on, at TP1 too and with a device sync between replays
+// (tools/graph_probe.py), while eager decode matches the oracle. Re-issuing the early pages
+// after the wait makes graph replay exact, so some early-streamed data other than the
+// refreshed current row is stale; adding a post-wait printf also hides it -- not understood yet.
 __device__ int g_cluster_early = 0;
 
 template <int D>

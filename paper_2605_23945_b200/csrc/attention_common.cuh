@@ -133,10 +133,12 @@ __device__ __forceinline__ void load_q_frags(uint32_t (&qa)[D / 16][4], const __
 #pragma unroll
   for (int ks = 0; ks < D / 16; ++ks) {
     const int d0 = ks * 16 + 2 * c;
-    qa[ks][0] = (g < G) ? *reinterpret_cast<const uint32_t*>(q0 + g * D + d0) : 0u;
-    qa[ks][1] = (g + 8 < G) ? *reinterpret_cast<const uint32_t*>(q0 + (g + 8) * D + d0) : 0u;
-    qa[ks][2] = (g < G) ? *reinterpret_cast<const uint32_t*>(q0 + g * D + d0 + 8) : 0u;
-    qa[ks][3] = (g + 8 < G) ? *reinterpret_cast<const uint32_t*>(q0 + (g + 8) * D + d0 + 8) : 0u;
+    // q is written by the predecessor kernel, which may still have been running when this grid
+    // started (PDL): coherent L2 loads, never the non-coherent read-only path
+    qa[ks][0] = (g < G) ? __ldcg(reinterpret_cast<const unsigned int*>(q0 + g * D + d0)) : 0u;
+    qa[ks][1] = (g + 8 < G) ? __ldcg(reinterpret_cast<const unsigned int*>(q0 + (g + 8) * D + d0)) : 0u;
+    qa[ks][2] = (g < G) ? __ldcg(reinterpret_cast<const unsigned int*>(q0 + g * D + d0 + 8)) : 0u;
+    qa[ks][3] = (g + 8 < G) ? __ldcg(reinterpret_cast<const unsigned int*>(q0 + (g + 8) * D + d0 + 8)) : 0u;
   }
 }
 

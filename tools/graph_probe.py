@@ -13,7 +13,12 @@ for name, tp, nsteps in [("tiny", 1, 20), ("tiny", 2, 20), ("mini-qwen", 1, 20),
         runner.step(2, 1)
         if graphs:
             runner.capture(2)
-        runner.step(2, nsteps)
+        if len(sys.argv) > 1 and sys.argv[1] == "sync":
+            for _ in range(nsteps):
+                runner.step(2, 1)
+                torch.cuda.synchronize()
+        else:
+            runner.step(2, nsteps)
         torch.cuda.synchronize()
         outs.append(ranks[0].slots.history[slots].cpu())
     d = (outs[0] != outs[1]).nonzero()
