@@ -172,3 +172,26 @@ def test_protocol_mix_ll_counter_prefill_tp2():
         ep = int(cm.epoch.item())
         L = geom.num_layers
         assert cm.ctr[:2 * L].tolist() == [(ep - 1) * 2] * (2 * L)
+
+
+@pytest.mark.parametrize("tp,B", [(1, 16), (1, 64), (2, 40)])
+def test_graph_replay_matches_eager_wide(tp, B):
+    """Graph replay == eager decode where attention runs the fixed-split and page-balanced
+    forms, which stream KV pages before the programmatic-dependency wait."""
+    geom = geometry("mini-qwen")
+    gen = torch.Generator().manual_seed(B)
+    prompts = torch.randint(0, geom.vocab, (B, 8), generator=gen).tolist()
+    outs = []
+    for graphs in (False, True):
+        ranks, runner = build_group(geom, tp, max_batch=64, num_slots=B + 2, max_len=128, seed=3,
+                                    use_graphs=graphs)
+        slots = [admit(ranks, i, p, max_ctx=len(p) + 26) for i, p in enumerate(prompts)]
+        bk = ranks[0].executor.bucket(B)
+        runner.set_rows(bk, slots)
+        runner.step(bk, 1)
+        if graphs:
+            runner.capture(bk)
+        runner.step(bk, 24)
+        torch.cuda.synchronize()
+        outs.append(ranks[0].slots.history[slots].cpu())
+    assert torch.equal(outs[0], outs[1])
