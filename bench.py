@@ -269,7 +269,7 @@ def main():
                                f"{args.seed}), start TP{spec.initial_tp}/DP{gpus // spec.initial_tp}, Algorithm 1 over tp_list "
                                f"{list(spec.controller.tp_list)}",
                    "model": args.model, "global_batch": spec.global_batch, "seq_len": args.prompt_len + args.l_max,
-                   "parallelism": f"tp{spec.initial_tp}->adaptive,dp{gpus // spec.initial_tp}", "l2": "inputs > L2 (15.2 GB weights streamed per step)",
+                   "parallelism": f"tp{spec.initial_tp}->adaptive,dp{gpus // spec.initial_tp}", "l2": "inputs > L2 (14.1 GB of weight shards streamed per step)",
                    "step": "one generation stage (prefill via decode path + decode to last sample)",
                    "predictor": "B200-measured profile table" if table is not None else "analytic b200.cfg"},
         "phases": stage_phases(rep, meas),
@@ -298,6 +298,8 @@ def main():
         pred = sim_run(spec, table, TableBackend(spec, table)).generation_time
         line["predicted"] = {"value": pred, "unit": UNIT, "rel_error": (pred - value) / value,
                              "source": "reference engine loop over presets/b200_<model>_profile.csv"}
+    if gpus == 1 and spec.initial_tp == 1 and not line["switches"]:
+        line["stage_roofline"] = stage_roofline(spec, geom, line["phases"]["decode_s"], peak)
     tr = traffic_record()
     if tr:
         line["roofline"]["traffic"] = tr["dram_bytes"]
@@ -332,6 +334,23 @@ def main():
                                           f"stage's {sum(hist.values())} rounds and prefill"}
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def stage_roofline(spec, geom, decode_s: float, peak_gbps: float) -> dict:
+    """HBM floor of the stage's decode rounds on one GPU at TP1: every round streams all
+    weight shards (linears + LM head) and every active sample's K/V (SURVEY §8(d) units)."""
+    from paper_2605_23945_b200.workload import sample_response_lengths
+    lens = np.asarray(sample_response_lengths(spec.distribution, spec.global_batch, spec.seed))
+    lens = np.minimum(lens, spec.l_max)
+    w = geom.num_layers * geom.layer_param_bytes + geom.vocab * geom.hidden * geom.bytes_per_elem
+    kvpt = geom.kv_bytes_per_token
+    rounds = int(lens.max())
+    r = np.arange(rounds)
+    active = (lens[None, :] > r[:, None]).sum(1)
+    total = float(rounds * w + (kvpt * (spec.prompt_len + r) * active).sum())
+    floor = total / (peak_gbps * 1e9)
+    return {"decode_floor_s": floor, "decode_s": decode_s, "frac": floor / decode_s, "bytes": total,
+            "rounds": rounds, "note": "weights + live K/V per round at the measured copy peak"}
 
 
 def stage_phases(rep, meas) -> dict:
