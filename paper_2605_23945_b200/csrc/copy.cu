@@ -11,7 +11,7 @@
 // into rows / <=64 KB pieces). Two engines:
 //   mode 0: LSU copy, 4 x 16 B loads in flight per thread, persistent grid;
 //   mode 1: TMA-staged copy, cp.async.bulk global->smem->global through a
-//           4-deep ring of 32 KB buffers per CTA (no register round trip).
+//           2-deep ring of 48 KB buffers per CTA, 2 CTAs per SM (no register round trip).
 #include "common.cuh"
 
 namespace tps {
@@ -46,14 +46,31 @@ __global__ void __launch_bounds__(kCopyThreads) copy_items_lsu_kernel(const Copy
   }
 }
 
-constexpr int kBulkBuf = 32 * 1024;
-constexpr int kBulkDepth = 4;
+constexpr int kBulkMaxDepth = 8;
+// ring geometry (TPS_COPY_BUF_KB x TPS_COPY_DEPTH per CTA, TPS_COPY_CTAS_PER_SM CTAs per SM).
+// Swept on the config-5 switch microbench (Qwen2.5-7B TP1 -> TP2, 16 samples at 4K, 20.1 GB of
+// items): 32 KB x 4 x 2 (one CTA resident per SM) 2465 GB/s; 32 x 2 x 3 2848-2881; 16 x 2 x 4
+// 2862; 48 x 2 x 2 2968 (91 % of the read+write copy peak) -- two 96 KB CTAs per SM.
+static int g_bulk_buf = [] {
+  const char* v = getenv("TPS_COPY_BUF_KB");
+  return (v ? atoi(v) : 48) * 1024;
+}();
+static int g_bulk_depth = [] {
+  const char* v = getenv("TPS_COPY_DEPTH");
+  const int d = v ? atoi(v) : 2;
+  return d < 2 ? 2 : (d > kBulkMaxDepth ? kBulkMaxDepth : d);
+}();
+static int g_bulk_ctas = [] {
+  const char* v = getenv("TPS_COPY_CTAS_PER_SM");
+  return v ? atoi(v) : 2;
+}();
 
-// One elected thread per CTA drives a kBulkDepth-deep ring: loads of chunks
+// One elected thread per CTA drives a depth-deep ring: loads of chunks
 // k+1..k+depth-1 are in flight while chunk k is being stored.
-__global__ void __launch_bounds__(32) copy_items_tma_kernel(const CopyItem* __restrict__ items, int n) {
+__global__ void __launch_bounds__(32) copy_items_tma_kernel(const CopyItem* __restrict__ items, int n,
+                                                            int kBulkBuf, int kBulkDepth) {
   extern __shared__ __align__(128) uint8_t sbuf[];
-  __shared__ __align__(8) uint64_t bars[kBulkDepth];
+  __shared__ __align__(8) uint64_t bars[kBulkMaxDepth];
   if (threadIdx.x != 0) return;
   for (int i = 0; i < kBulkDepth; ++i) mbar_init(&bars[i], 1);
   fence_barrier_init();
@@ -75,8 +92,8 @@ __global__ void __launch_bounds__(32) copy_items_tma_kernel(const CopyItem* __re
     }
     return false;
   };
-  uint8_t* dsts[kBulkDepth];
-  uint32_t lens[kBulkDepth];
+  uint8_t* dsts[kBulkMaxDepth];
+  uint32_t lens[kBulkMaxDepth];
   uint32_t phases = 0;
   int head = 0, tail = 0;
   const uint8_t* s;
@@ -112,20 +129,21 @@ __global__ void __launch_bounds__(32) copy_items_tma_kernel(const CopyItem* __re
 
 int configure_copy() {
   TPS_CUDA_TRY(cudaFuncSetAttribute(copy_items_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    kBulkBuf * kBulkDepth));
+                                    g_bulk_buf * g_bulk_depth));
   return kOk;
 }
 
 int copy_items(const void* items, int n, int mode, int grid, cudaStream_t st) {
   TPS_CHECK_ARG(n >= 0, "copy_items: n >= 0");
   if (n == 0) return kOk;
-  if (grid <= 0) grid = 2 * kNumSMs;
+  if (grid <= 0) grid = (mode == 1 ? g_bulk_ctas : 2) * kNumSMs;
   if (grid > n) grid = n;
   if (mode == 0) {
     copy_items_lsu_kernel<<<grid, kCopyThreads, 0, st>>>(reinterpret_cast<const CopyItem*>(items), n);
   } else if (mode == 1) {
-    const int smem = kBulkBuf * kBulkDepth;
-    copy_items_tma_kernel<<<grid, 32, smem, st>>>(reinterpret_cast<const CopyItem*>(items), n);
+    const int smem = g_bulk_buf * g_bulk_depth;
+    copy_items_tma_kernel<<<grid, 32, smem, st>>>(reinterpret_cast<const CopyItem*>(items), n, g_bulk_buf,
+                                                  g_bulk_depth);
   } else {
     return fail(kInvalid, "copy_items: mode must be 0 (LSU) or 1 (TMA bulk)");
   }
