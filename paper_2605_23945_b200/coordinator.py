@@ -79,7 +79,7 @@ class B200Backend:
     exact_pool_cost = False
 
     def __init__(self, spec: ScenarioSpec, geom: DecoderGeometry, world: World, seed: int = 0,
-                 use_graphs: bool = True, copy_mode: int = 0, prompts: np.ndarray | None = None,
+                 use_graphs: bool = True, copy_mode: int = 1, prompts: np.ndarray | None = None,
                  host_io: bool = False, state_method: str | None = None, temperature: float = 0.0):
         self.spec, self.geom, self.world = spec, geom, world
         self.temperature = temperature  # 0: greedy; > 0: Gumbel-max with per-sample Philox keys
@@ -424,16 +424,22 @@ class B200Backend:
     def _copy(self, items: np.ndarray, st) -> None:
         if len(items) == 0:
             return
-        host = torch.from_numpy(np.ascontiguousarray(items, dtype=np.int64)).pin_memory()
-        dev = host.to(st.device, non_blocking=True)
+        items = np.ascontiguousarray(items, dtype=np.int64)
+        parts = [(items, self.copy_mode)]
+        if self.copy_mode == 1:
+            # the bulk-copy engine needs 16-B aligned addresses and sizes; the rest go through LSU
+            ok = ((items[:, 0] | items[:, 1] | items[:, 2]) & 15) == 0
+            parts = [(p, m) for p, m in ((items[ok], 1), (items[~ok], 0)) if len(p)]
         if self.copy_events is not None:
             self.copy_events.append((_event(st), int(items[:, 2].sum())))
-        nat.check(nat.lib().tps_copy_items(dev.data_ptr(), len(items), self.copy_mode, 0, st.cuda_stream),
-                  "tps_copy_items")
+        for part, mode in parts:
+            host = torch.from_numpy(np.ascontiguousarray(part)).pin_memory()
+            dev = host.to(st.device, non_blocking=True)
+            nat.check(nat.lib().tps_copy_items(dev.data_ptr(), len(part), mode, 0, st.cuda_stream), "tps_copy_items")
+            self._keep.append(dev)
         if self.copy_events is not None:
             self.copy_events[-1] += (_event(st),)
-        self.kernels_launched += 1
-        self._keep.append(dev)
+        self.kernels_launched += len(parts)
 
     def _device_barrier(self) -> None:
         """Node-wide device barrier (a virtual world is already ordered by its single stream)."""
@@ -546,7 +552,7 @@ class GlobalCoordinator:
     """Run one generation stage on B200 and report it in the reference's SimReport schema."""
 
     def __init__(self, spec: ScenarioSpec, geom: DecoderGeometry, world: World | None = None, seed: int = 0,
-                 table=None, use_graphs: bool = True, copy_mode: int = 0, host_io: bool = False,
+                 table=None, use_graphs: bool = True, copy_mode: int = 1, host_io: bool = False,
                  state_method: str | None = None, temperature: float = 0.0):
         self.spec = spec
         self.geom = geom

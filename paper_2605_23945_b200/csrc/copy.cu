@@ -79,6 +79,13 @@ __global__ void __launch_bounds__(32) copy_items_tma_kernel(const CopyItem* __re
   auto next = [&](const uint8_t*& s, uint8_t*& d, uint32_t& len) -> bool {
     while (git < n) {
       const CopyItem ci = items[git];
+      if (((reinterpret_cast<uintptr_t>(ci.src) | reinterpret_cast<uintptr_t>(ci.dst) | ci.bytes) & 15u) != 0) {
+        // not bulk-copyable (the host routes such items to the LSU engine): plain bytes
+        for (uint64_t j = goff; j < ci.bytes; ++j) ci.dst[j] = ci.src[j];
+        git += gridDim.x;
+        goff = 0;
+        continue;
+      }
       if (goff < ci.bytes) {
         const uint64_t rem = ci.bytes - goff;
         len = (uint32_t)(rem < (uint64_t)kBulkBuf ? rem : (uint64_t)kBulkBuf);
