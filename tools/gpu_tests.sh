@@ -1,1 +1,1 @@
-timeout 900 python -m pytest tests/test_gpu_reshard_fullsize.py tests/test_gpu_kernels.py -x -q -k "reshard or copy" > gpurun_out/pytest_gpu.log 2>&1; grep -E "FAILED|passed|failed" gpurun_out/pytest_gpu.log | head -5
+timeout 300 python tools/switch_bench.py --modes 0,1 2>&1 | grep -o '"copy_gbps": [0-9.]*\|"copy_launches": [0-9]*' | tr '\n' ' '; echo
