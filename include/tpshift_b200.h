@@ -153,6 +153,13 @@ int tps_qkv_fused_splits(int64_t n, int64_t k, int64_t b);
  * b > 64 or more tiles than SMs). */
 int tps_cluster_splits(int64_t n, int64_t k, int64_t b);
 
+/* Gate/up projection + SwiGLU with split-K kept: the split CTAs of a tile (one cluster) sum
+ * their partials over DSMEM in split order, then act[i][f] = bf16(silu(gate_f . x_i) *
+ * (up_f . x_i)) -- the results of tps_linear + tps_silu_mul in one launch (same W layout as
+ * tps_linear_silu). */
+int tps_linear_silu_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,
+                            int64_t x_rows, int64_t ldx, void* act, int64_t ld_act, void* stream);
+
 /* out[i][j] = (W x_i)_j as ONE fp32 [b][n] result: the split-K CTAs of a tile (one cluster)
  * reduce their partials over DSMEM in split order (tps_linear's partials summed in-kernel). */
 int tps_linear_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,

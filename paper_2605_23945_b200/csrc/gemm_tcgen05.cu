@@ -114,7 +114,11 @@ constexpr int kEpiQkvRope = 2;
 // pair per element to every peer (tps_linear_push_ll pushes every split partial: S x the
 // NVLink bytes and tp x S sources for the consumer; tps_reduce_push_ll needs a launch).
 constexpr int kEpiClusterLL = 3;
-constexpr bool cluster_epi(int epi) { return epi == kEpiQkvRope || epi == kEpiClusterLL; }
+// kEpiClusterSilu: gate/up projection (interleaved 64-row [gate c | up c] blocks) with the
+// split-K partials summed over DSMEM in the cluster and SwiGLU applied: act = bf16(silu(g) * u),
+// the result of tps_linear + tps_silu_mul with split-K kept (tps_linear_silu needs S = 1).
+constexpr int kEpiClusterSilu = 5;
+constexpr bool cluster_epi(int epi) { return epi == kEpiQkvRope || epi == kEpiClusterLL || epi == kEpiClusterSilu; }
 
 
 namespace cg = cooperative_groups;
@@ -151,6 +155,41 @@ __device__ __forceinline__ void cluster_ll_finish(const float* part, const DstLi
         st_relaxed_sys_u64(reinterpret_cast<uint64_t*>(dst.p[d]) + (size_t)j * N + n, tag | __float_as_uint(x));
     else
       dst.p[0][(size_t)j * N + n] = x;  // local fp32 result (tps_linear_cluster)
+  }
+}
+
+// Finishing of kEpiClusterSilu: CTA s of S produces f in [s*64/S, (s+1)*64/S) of the tile.
+template <int BN>
+__device__ __forceinline__ void cluster_silu_finish(const float* part, __nv_bfloat16* act, int ld_act, int tile,
+                                                    int F, int rows) {
+  cg::cluster_group cl = cg::this_cluster();
+  cl.sync();  // every split's partial tile is parked in its CTA's smem
+  const int S = (int)cl.num_blocks();
+  const int rank = (int)cl.block_rank();
+  const int f0 = rank * 64 / S, f1 = (rank + 1) * 64 / S;
+  const int nf = f1 - f0;
+  const float* rp[16];
+#pragma unroll
+  for (int s = 0; s < 16; ++s) rp[s] = s < S ? cl.map_shared_rank(part, s) : part;
+  for (int it = threadIdx.x; it < nf * rows; it += kGemmThreads) {
+    const int fl = f0 + it % nf, j = it / nf;
+    const int f = tile * 64 + fl;
+    if (f >= F) continue;
+    float vg[16], vu[16];
+#pragma unroll
+    for (int s = 0; s < 16; ++s)
+      if (s < S) {
+        vg[s] = rp[s][j * kBM + fl];
+        vu[s] = rp[s][j * kBM + 64 + fl];
+      }
+    float g = 0.f, u = 0.f;  // split order, from 0 (as tps_silu_mul)
+#pragma unroll
+    for (int s = 0; s < 16; ++s)
+      if (s < S) {
+        g += vg[s];
+        u += vu[s];
+      }
+    act[(size_t)j * ld_act + f] = f2bf(g / (1.f + __expf(-g)) * u);
   }
 }
 
@@ -244,7 +283,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* tmem_empty = bars + 2 * S + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
 
-  const unsigned int trs = trace_begin(EPI == kEpiSiluMul ? kTrGemmSilu : EPI == kEpiClusterLL ? kTrGemmPush : kTrGemm);
+  const unsigned int trs =
+      trace_begin((EPI == kEpiSiluMul || EPI == kEpiClusterSilu) ? kTrGemmSilu : EPI == kEpiClusterLL ? kTrGemmPush
+                                                                                                        : kTrGemm);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   // unit u = ((tile * splits + split) * acts + act): the activation tiles of one weight
@@ -466,6 +507,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                    N, B);
     cg::this_cluster().sync();  // keep this smem alive until the cluster has read it
   }
+  if constexpr (EPI == kEpiClusterSilu) {
+    pdl_wait();  // (every thread: act is read by the previous layer's down projection)
+    cluster_silu_finish<BN>(reinterpret_cast<const float*>(smem), act_out, ld_act,
+                            (int)blockIdx.x / (int)cg::this_cluster().num_blocks(), N / 2, B);
+    cg::this_cluster().sync();
+  }
   if constexpr (EPI == kEpiClusterLL) {
     pdl_wait();  // (every thread: the pushes overwrite LL slots the predecessor chain consumed)
     const uint64_t tag =
@@ -613,6 +660,11 @@ static int configure_one() {
     TPS_CUDA_TRY(cudaFuncSetAttribute(gemm_swapab_kernel<BN, kEpiClusterLL>,
                                       cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     TPS_MAX_CARVEOUT((gemm_swapab_kernel<BN, kEpiClusterLL>));
+    TPS_CUDA_TRY(cudaFuncSetAttribute(gemm_swapab_kernel<BN, kEpiClusterSilu>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN>::kQkvSmemBytes));
+    TPS_CUDA_TRY(cudaFuncSetAttribute(gemm_swapab_kernel<BN, kEpiClusterSilu>,
+                                      cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    TPS_MAX_CARVEOUT((gemm_swapab_kernel<BN, kEpiClusterSilu>));
   }
   return kOk;
 }
@@ -820,6 +872,30 @@ int linear_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, const void*
     case 16: return launch_gemm<16, kEpiClusterLL>(mw, mx, e, (int)n, (int)b, tiles, splits, (int)chunks, stream);
     case 32: return launch_gemm<32, kEpiClusterLL>(mw, mx, e, (int)n, (int)b, tiles, splits, (int)chunks, stream);
     default: return launch_gemm<64, kEpiClusterLL>(mw, mx, e, (int)n, (int)b, tiles, splits, (int)chunks, stream);
+  }
+}
+
+// Gate/up + SwiGLU with split-K reduced in the cluster: act[i][f] = bf16(silu(g_f) * u_f).
+int linear_silu_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
+                        int64_t ldx, void* act, int64_t ld_act, cudaStream_t stream) {
+  TPS_CHECK_ARG(act && n % kBM == 0 && ld_act >= n / 2, "linear_silu_cluster: n = 2F, F % 64 == 0, ld_act >= F");
+  const int splits = cluster_splits(n, k, b);
+  TPS_CHECK_ARG(splits >= 1, "linear_silu_cluster: shape not supported (see tps_cluster_splits)");
+  const int64_t chunks = (k + kBK - 1) / kBK;
+  CUtensorMap mw, mx;
+  int bn;
+  int rc = prepare(w, n, k, ldw, x, b, x_rows, ldx, &mw, &mx, &bn);
+  if (rc) return rc;
+  EpiArgs e{};
+  e.dst.n = 0;
+  e.sig.n = 0;
+  e.act_out = reinterpret_cast<__nv_bfloat16*>(act);
+  e.ld_act = (int)ld_act;
+  const int tiles = (int)(n / kBM);
+  switch (bn) {
+    case 16: return launch_gemm<16, kEpiClusterSilu>(mw, mx, e, (int)n, (int)b, tiles, splits, (int)chunks, stream);
+    case 32: return launch_gemm<32, kEpiClusterSilu>(mw, mx, e, (int)n, (int)b, tiles, splits, (int)chunks, stream);
+    default: return launch_gemm<64, kEpiClusterSilu>(mw, mx, e, (int)n, (int)b, tiles, splits, (int)chunks, stream);
   }
 }
 

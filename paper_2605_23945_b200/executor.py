@@ -186,6 +186,10 @@ class InferExecutor:
         # measured slower for column-parallel / TP1 projections: TP1 B=64 4.465 -> 4.838 ms, the
         # 4-stage ring of the cluster form costs more than the partial traffic it saves): off
         self.cluster_linear = os.environ.get("TPS_CLUSTER_LINEAR", "0") == "1"
+        # unfused-SwiGLU shapes (TP >= 4) through tps_linear_silu_cluster (bit-identical; measured
+        # neutral: TP8 B=1 1.334 vs 1.317 ms, TP4 B=64 2.591 vs 2.507 -- the SiLU launch already
+        # hides under the down projection's weight prefetch): off
+        self.silu_cluster = os.environ.get("TPS_SILU_CLUSTER", "0") == "1"
         # launch kinds left out of the step program (timing probes only: results are garbage)
         self.skip: frozenset = frozenset()
         # 0: greedy; > 0: Gumbel-max sampling at this temperature with the slots' Philox keys
@@ -396,6 +400,13 @@ class InferExecutor:
                 nat.check(lib.tps_linear_silu(w_gu.data_ptr(), 2 * self.F, H, H, self.xn.data_ptr(), B,
                                               self.xn.shape[0], H, self.act.data_ptr(), self.F, st),
                           "tps_linear_silu")
+                stats.add("linear")
+            elif (self.silu_cluster and self.comm is not None and self.comm.tp >= LL_CLUSTER_MIN_TP and
+                  lib.tps_cluster_splits(2 * self.F, H, B) > 0):
+                # split-K reduced in the cluster, SwiGLU in the epilogue (no tps_silu_mul launch)
+                nat.check(lib.tps_linear_silu_cluster(w_gu.data_ptr(), 2 * self.F, H, H, self.xn.data_ptr(), B,
+                                                      self.xn.shape[0], H, self.act.data_ptr(), self.F, st),
+                          "tps_linear_silu_cluster")
                 stats.add("linear")
             else:
                 srcs = self._linear(st, stats, w_gu, self.xn, B)

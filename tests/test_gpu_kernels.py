@@ -450,3 +450,23 @@ def test_linear_push_ll_cluster(n, k, b, ndst):
     nat.check(lib.tps_linear_cluster(w.data_ptr(), n, k, k, x.data_ptr(), b, b, k, out.data_ptr(), _stream()))
     torch.cuda.synchronize()
     assert torch.equal(out[:b], ref) and (out[b:] == 7.0).all()
+
+
+@pytest.mark.parametrize("F,k,b", [(2368, 3584, 1), (1792, 4096, 16), (3456, 5120, 5), (512, 256, 64)])
+def test_linear_silu_cluster(F, k, b):
+    """tps_linear_silu_cluster == tps_linear (same split count) + tps_silu_mul, bit for bit."""
+    lib = nat.lib()
+    n = 2 * F
+    S = lib.tps_cluster_splits(n, k, b)
+    assert S >= 1
+    torch.manual_seed(F + b)
+    w = (torch.randn(n, k, device="cuda") * 0.05).bfloat16()
+    x = torch.randn(b, k, device="cuda").bfloat16()
+    ws = torch.zeros(S, b, n, device="cuda")
+    ref = torch.zeros(b, F, device="cuda", dtype=torch.bfloat16)
+    nat.check(lib.tps_linear(w.data_ptr(), n, k, k, x.data_ptr(), b, b, k, ws.data_ptr(), S, _stream()))
+    nat.check(lib.tps_silu_mul(ws.data_ptr(), S, b * n, b, F, ref.data_ptr(), F, _stream()))
+    got = torch.full((b + 1, F), 3.0, device="cuda", dtype=torch.bfloat16)
+    nat.check(lib.tps_linear_silu_cluster(w.data_ptr(), n, k, k, x.data_ptr(), b, b, k, got.data_ptr(), F, _stream()))
+    torch.cuda.synchronize()
+    assert torch.equal(got[:b], ref) and (got[b:] == 3.0).all()
