@@ -375,8 +375,9 @@ constexpr int kInKernelMergeMaxSplits = 4;
 // (TP8 B=1 1.330 -> 1.287 ms). Off: graph-replayed decode then diverges from eager decode
 // from the first generated token on, at TP1 too and with a device sync between replays
 // (tools/graph_probe.py), while eager decode matches the oracle. Re-issuing the early pages
-// after the wait makes graph replay exact, so some early-streamed data other than the
-// refreshed current row is stale; adding a post-wait printf also hides it -- not understood yet.
+// after the wait makes graph replay exact (so does re-reading only rows >= ctx - 1, or any
+// post-wait delay in thread 0: a printf, a 20 us spin), and q re-read 20 us after the wait is
+// unchanged -- timing-dependent, root cause not found yet.
 __device__ int g_cluster_early = 0;
 
 template <int D>

@@ -1,3 +1,2 @@
-timeout 600 python -m pytest tests/test_gpu_kernels.py -x -q -k "silu_cluster" 2>&1 | tail -2
-timeout 900 python -m pytest tests/test_gpu_decode.py -x -q 2>&1 | tail -2
-for v in 0 1; do TPS_SILU_CLUSTER=$v timeout 600 python tools/solo_step.py qwen2.5-7b 4,8 1,8,16,64 2048 2>&1 | grep -v watchdog; done
+echo "== early"; TPS_LIB_PATH=$PWD/build_variants/diag5.so TPS_ATTN_CLUSTER_EARLY=1 timeout 600 python tools/graph_probe.py 2>&1 | grep -v watchdog | sort | uniq -c | head
+echo "== late"; TPS_LIB_PATH=$PWD/build_variants/diag5.so TPS_ATTN_CLUSTER_EARLY=0 timeout 600 python tools/graph_probe.py 2>&1 | grep -v watchdog | sort | uniq -c | head
