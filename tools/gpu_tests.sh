@@ -1,2 +1,3 @@
-echo "== early"; TPS_LIB_PATH=$PWD/build_variants/diag5.so TPS_ATTN_CLUSTER_EARLY=1 timeout 600 python tools/graph_probe.py 2>&1 | grep -v watchdog | sort | uniq -c | head
-echo "== late"; TPS_LIB_PATH=$PWD/build_variants/diag5.so TPS_ATTN_CLUSTER_EARLY=0 timeout 600 python tools/graph_probe.py 2>&1 | grep -v watchdog | sort | uniq -c | head
+mkdir -p gpurun_out
+timeout 1200 python tools/profile_b200.py --model llama3-8b --budget 900 --out gpurun_out/b200_llama3-8b.csv > gpurun_out/profile_llama.log 2>&1
+tail -1 gpurun_out/profile_llama.log
