@@ -126,6 +126,7 @@ class B200Backend:
         # life of the backend like the communicator pool: a later switch to the same degree,
         # or the next stage, reuses the buffers and graphs instead of allocating and capturing
         self._layouts: dict[int, dict] = {}
+        self._witems: dict = {}  # weight copy items per (transition, rank, arena pointers)
         self._build_layout(self.layout, weights_seed=seed)
         self._layouts[self.layout.tp] = {"ranks": self.ranks, "runners": self.runners,
                                          "cap": {g: self.max_batch for g in self.local_groups()}}
@@ -360,7 +361,12 @@ class B200Backend:
             rs, st = self.ranks[r], self.stream(r)
             t0 = time.perf_counter()
             wp = cached_weight_pulls(self.geom, old, new, r)  # verified once when first planned
-            w_items = to_items(wp, {k: v["w"] for k, v in ptrs.items()}, rs.weights.arena.data_ptr())
+            w_src = {k: v["w"] for k, v in ptrs.items()}
+            # layouts (and so arena pointers) are cached: the items of a repeated transition too
+            ikey = (old, new, r, rs.weights.arena.data_ptr(), tuple(sorted(w_src.items())))
+            w_items = self._witems.get(ikey)
+            if w_items is None:
+                w_items = self._witems[ikey] = to_items(wp, w_src, rs.weights.arena.data_ptr())
             nv, loc = nvlink_bytes(wp, r)
             stats["nv"] += nv
             stats["loc"] += loc
