@@ -160,6 +160,13 @@ int tps_cluster_splits(int64_t n, int64_t k, int64_t b);
 int tps_linear_silu_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,
                             int64_t x_rows, int64_t ldx, void* act, int64_t ld_act, void* stream);
 
+/* LM head with greedy argmax stage 1 in the epilogue (split-K 1): logits [b][n] fp32 and, per
+ * row i and 128-column tile t, cand[i * ceil(n/128) + t] = {max logit, smallest vocab index on
+ * ties} (index = vocab0 + column) -- the candidates tps_argmax_finalize merges with
+ * nchunk = ceil(n / 128); the same token tps_argmax_stage1 + finalize would pick. */
+int tps_linear_argmax(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,
+                      int64_t x_rows, int64_t ldx, float* logits, void* cand, int vocab0, void* stream);
+
 /* out[i][j] = (W x_i)_j as ONE fp32 [b][n] result: the split-K CTAs of a tile (one cluster)
  * reduce their partials over DSMEM in split order (tps_linear's partials summed in-kernel). */
 int tps_linear_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,

@@ -38,6 +38,7 @@ SIGNATURES = {
     "tps_linear_splits": (_i32, [_i64, _i64, _i64]),
     "tps_qkv_fused_splits": (_i32, [_i64, _i64, _i64]),
     "tps_cluster_splits": (_i32, [_i64, _i64, _i64]),
+    "tps_linear_argmax": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _vp, _vp, _i32, _vp]),
     "tps_linear_silu_cluster": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _vp, _i64, _vp]),
     "tps_linear_cluster": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _vp, _vp]),
     "tps_linear_push_ll_cluster": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _pp, _i32, _vp,

@@ -31,6 +31,8 @@ int linear(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int6
            int64_t ldx, float* out, int splits, cudaStream_t stream);
 int qkv_fused_splits(int64_t n, int64_t k, int64_t b);
 int cluster_splits(int64_t n, int64_t k, int64_t b);
+int linear_argmax(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
+                  int64_t ldx, float* logits, void* cand, int vocab0, cudaStream_t stream);
 int linear_silu_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
                         int64_t ldx, void* act, int64_t ld_act, cudaStream_t stream);
 int linear_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
@@ -191,6 +193,11 @@ int tps_linear_silu(const void* w, int64_t n, int64_t k, int64_t ldw, const void
 int tps_qkv_fused_splits(int64_t n, int64_t k, int64_t b) { return qkv_fused_splits(n, k, b); }
 
 int tps_cluster_splits(int64_t n, int64_t k, int64_t b) { return cluster_splits(n, k, b); }
+
+int tps_linear_argmax(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
+                      int64_t ldx, float* logits, void* cand, int vocab0, void* stream) {
+  return linear_argmax(w, n, k, ldw, x, b, x_rows, ldx, logits, cand, vocab0, S(stream));
+}
 
 int tps_linear_silu_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,
                             int64_t x_rows, int64_t ldx, void* act, int64_t ld_act, void* stream) {

@@ -118,6 +118,16 @@ constexpr int kEpiClusterLL = 3;
 // split-K partials summed over DSMEM in the cluster and SwiGLU applied: act = bf16(silu(g) * u),
 // the result of tps_linear + tps_silu_mul with split-K kept (tps_linear_silu needs S = 1).
 constexpr int kEpiClusterSilu = 5;
+// kEpiArgmax: LM head (splits == 1): the fp32 logits as kEpiPartial, plus the greedy candidate
+// {max logit, smallest index on ties} of every (row, 128-column tile) -- argmax stage 1 done
+// in the epilogue, so no kernel re-reads the logits (tps_argmax_finalize merges the tiles).
+constexpr int kEpiArgmax = 6;
+
+struct ArgEpi {
+  ArgmaxCand* cand;  // [rows][ntiles]
+  int ntiles;
+  int vocab0;        // global index of column 0
+};
 constexpr bool cluster_epi(int epi) { return epi == kEpiQkvRope || epi == kEpiClusterLL || epi == kEpiClusterSilu; }
 
 
@@ -268,7 +278,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                        long long split_stride, int N, int B, int num_tiles, int splits, int chunks, int acts,
                        __nv_bfloat16* __restrict__ act_out, int ld_act, const __grid_constant__ SignalSpec sig,
                        const uint64_t* __restrict__ tag_epoch, uint32_t tag_mult, uint32_t tag_add,
-                       const __grid_constant__ QkvEpi qkv) {
+                       const __grid_constant__ QkvEpi qkv, const __grid_constant__ ArgEpi arg) {
   using Cfg = GemmCfg<BN>;
   constexpr int S = cluster_epi(EPI) ? Cfg::kQkvStages : Cfg::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -423,7 +433,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int n = tile * kBM + q * 32 + lane;
       const int b0 = act * BN;
       const int rows = min(BN, B - b0);
-      if constexpr (EPI == kEpiPartial) {
+      if constexpr (EPI == kEpiPartial || EPI == kEpiArgmax) {
         // fp32 partial of (split, rows b0.., column n) into every destination: the local
         // split-K workspace, or -- the fused TP allreduce -- this rank's slots in each
         // peer's receive area (NVLink P2P stores), split-major with split_stride. The
@@ -451,6 +461,36 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                   if (j0 + j < rows) o[(size_t)(j0 + j) * N] = __uint_as_float(r[j]);
               }
             }
+          }
+          if constexpr (EPI == kEpiArgmax) {
+            // per row: warp max over its 32 columns (smallest index on ties), then the 4 warps
+            ArgmaxCand* xb = reinterpret_cast<ArgmaxCand*>(up_buf);  // [4][16]
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              float v = (n < N) ? __uint_as_float(r[j]) : -INFINITY;
+              int ix = arg.vocab0 + n;
+#pragma unroll
+              for (int o2 = 16; o2 > 0; o2 >>= 1) {
+                const float v2 = __shfl_xor_sync(0xffffffffu, v, o2);
+                const int i2 = __shfl_xor_sync(0xffffffffu, ix, o2);
+                if (v2 > v || (v2 == v && i2 < ix)) {
+                  v = v2;
+                  ix = i2;
+                }
+              }
+              if (lane == 0) xb[q * 16 + j] = ArgmaxCand{v, ix};
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (q == 0 && lane < 16 && j0 + lane < rows) {
+              ArgmaxCand best = xb[lane];
+#pragma unroll
+              for (int w = 1; w < 4; ++w) {
+                const ArgmaxCand c = xb[w * 16 + lane];
+                if (c.val > best.val || (c.val == best.val && c.idx < best.idx)) best = c;
+              }
+              arg.cand[(size_t)(b0 + j0 + lane) * arg.ntiles + tile] = best;
+            }
+            asm volatile("bar.sync 2, 128;" ::: "memory");
           }
         }
       } else if constexpr (cluster_epi(EPI)) {
@@ -623,6 +663,7 @@ struct EpiArgs {
   uint32_t tag_mult = 0;
   uint32_t tag_add = 0;
   QkvEpi qkv{};
+  ArgEpi arg{};
 };
 
 template <int BN, int EPI>
@@ -635,10 +676,10 @@ static int launch_gemm(const CUtensorMap& mw, const CUtensorMap& mx, const EpiAr
   if constexpr (cluster_epi(EPI))  // one unit per CTA, the splits of a tile in one cluster
     return launch_kcs(gemm_swapab_kernel<BN, EPI>, dim3(units), dim3(kGemmThreads), splits, Cfg::kQkvSmemBytes,
                       stream, true, mw, mx, e.dst, e.split_stride, n, b, tiles, splits, chunks, acts, e.act_out,
-                      e.ld_act, e.sig, e.tag_epoch, e.tag_mult, e.tag_add, e.qkv);
+                      e.ld_act, e.sig, e.tag_epoch, e.tag_mult, e.tag_add, e.qkv, e.arg);
   return launch_k(gemm_swapab_kernel<BN, EPI>, dim3(grid), dim3(kGemmThreads), Cfg::kSmemBytes, stream, true, mw,
                   mx, e.dst, e.split_stride, n, b, tiles, splits, chunks, acts, e.act_out, e.ld_act, e.sig,
-                  e.tag_epoch, e.tag_mult, e.tag_add, e.qkv);
+                  e.tag_epoch, e.tag_mult, e.tag_add, e.qkv, e.arg);
 }
 
 template <int BN>
@@ -647,6 +688,9 @@ static int configure_one() {
                                     GemmCfg<BN>::kSmemBytes));
   TPS_CUDA_TRY(cudaFuncSetAttribute(gemm_swapab_kernel<BN, kEpiSiluMul>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     GemmCfg<BN>::kSmemBytes));
+  TPS_CUDA_TRY(cudaFuncSetAttribute(gemm_swapab_kernel<BN, kEpiArgmax>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    GemmCfg<BN>::kSmemBytes));
+  TPS_MAX_CARVEOUT((gemm_swapab_kernel<BN, kEpiArgmax>));
   TPS_MAX_CARVEOUT((gemm_swapab_kernel<BN, kEpiPartial>));
   TPS_MAX_CARVEOUT((gemm_swapab_kernel<BN, kEpiSiluMul>));
   if constexpr (BN <= 64) {
@@ -897,6 +941,26 @@ int linear_silu_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, const 
     case 32: return launch_gemm<32, kEpiClusterSilu>(mw, mx, e, (int)n, (int)b, tiles, splits, (int)chunks, stream);
     default: return launch_gemm<64, kEpiClusterSilu>(mw, mx, e, (int)n, (int)b, tiles, splits, (int)chunks, stream);
   }
+}
+
+// LM head with the greedy argmax stage in the epilogue: logits [b][n] fp32 (splits = 1) and
+// cand[i][t] = {max, smallest index on ties} over columns [128 t, 128 t + 128) (+ vocab0).
+int linear_argmax(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
+                  int64_t ldx, float* logits, void* cand, int vocab0, cudaStream_t stream) {
+  TPS_CHECK_ARG(logits && cand, "linear_argmax: null output");
+  const int64_t chunks = (k + kBK - 1) / kBK;
+  CUtensorMap mw, mx;
+  int bn;
+  int rc = prepare(w, n, k, ldw, x, b, x_rows, ldx, &mw, &mx, &bn);
+  if (rc) return rc;
+  EpiArgs e{};
+  e.dst.n = 1;
+  e.dst.p[0] = logits;
+  e.split_stride = b * n;
+  e.sig.n = 0;
+  const int tiles = (int)((n + kBM - 1) / kBM);
+  e.arg = ArgEpi{reinterpret_cast<ArgmaxCand*>(cand), tiles, vocab0};
+  return dispatch<kEpiArgmax>(bn, mw, mx, e, (int)n, (int)b, tiles, 1, (int)chunks, stream);
 }
 
 int trace_register_gemm(uint64_t* p, unsigned int* c, unsigned int n) { return trace_register(p, c, n); }

@@ -233,6 +233,10 @@ class InferExecutor:
         self.att_l = torch.zeros_like(self.att_m)
         self.att_ctr = torch.zeros(rows * self.nkv, dtype=torch.int32, device=dev)
         self.local_cand = torch.zeros((max_batch, 64, 2), dtype=torch.int32, device=dev)
+        # TP1 greedy: the LM head's epilogue emits one candidate per (row, 128-column tile)
+        self.lm_argmax = os.environ.get("TPS_LM_ARGMAX", "1") == "1"
+        self.lm_tiles = -(-self.w[(-1, "lm_head")].shape[0] // 128)
+        self.lm_cand = torch.zeros((max_batch, self.lm_tiles, 2), dtype=torch.int32, device=dev)
         self.out_tok = torch.zeros(max_batch, dtype=torch.int32, device=dev)
         self.row_slot = {B: torch.full((B,), -1, dtype=torch.int32, device=dev) for B in sizes}
         self.row_pos = {prefill_rows: torch.zeros(prefill_rows, dtype=torch.int32, device=dev)} \
@@ -429,6 +433,18 @@ class InferExecutor:
                 nat.check(lib.tps_epoch_advance(cm.epoch.data_ptr(), st), "tps_epoch_advance")
                 stats.add("reduce_push")
                 stats.add("epoch_advance")
+            return
+        if cm is None and self.temperature <= 0 and self.lm_argmax and "linear" not in self.skip:
+            w = W[(-1, "lm_head")]
+            nat.check(lib.tps_linear_argmax(w.data_ptr(), w.shape[0], w.shape[1], w.shape[1], self.xn.data_ptr(), B,
+                                            self.xn.shape[0], self.xn.shape[1], self.ws.data_ptr(),
+                                            self.lm_cand.data_ptr(), self.shard.vocab[0], st), "tps_linear_argmax")
+            stats.add("linear")
+            self._last_lm_srcs = ((self.ws.data_ptr(), 1, B * w.shape[0]), B)
+            nat.check(lib.tps_argmax_finalize(self._arr([self.lm_cand.data_ptr()]), 1, self.lm_tiles, None, B, rs,
+                                              pos, self.prompt_len.data_ptr(), hist, sl.max_len,
+                                              self.out_tok.data_ptr(), st), "tps_argmax_finalize")
+            stats.add("argmax_finalize")
             return
         srcs = self._linear(st, stats, W[(-1, "lm_head")], self.xn, B)
         self._last_lm_srcs = (srcs, B)

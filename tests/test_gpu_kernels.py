@@ -470,3 +470,34 @@ def test_linear_silu_cluster(F, k, b):
     nat.check(lib.tps_linear_silu_cluster(w.data_ptr(), n, k, k, x.data_ptr(), b, b, k, got.data_ptr(), F, _stream()))
     torch.cuda.synchronize()
     assert torch.equal(got[:b], ref) and (got[b:] == 3.0).all()
+
+
+@pytest.mark.parametrize("V,k,b", [(4096, 256, 2), (152064, 3584, 64), (151936, 3584, 1), (19008, 3584, 17)])
+def test_linear_argmax_epilogue(V, k, b):
+    """tps_linear_argmax: logits equal tps_linear's (split-K 1) bit for bit, and the per-tile
+    candidates merged by tps_argmax_finalize pick the row's max logit with the smallest index
+    on ties -- the token of tps_argmax_stage1 + finalize."""
+    lib = nat.lib()
+    torch.manual_seed(V + b)
+    w = (torch.randn(V, k, device="cuda") * 0.05).bfloat16()
+    x = torch.randn(b, k, device="cuda").bfloat16()
+    x[0] = 0  # a row of exact ties (all logits 0): the smallest index must win
+    ref = torch.zeros(1, b, V, device="cuda")
+    nat.check(lib.tps_linear(w.data_ptr(), V, k, k, x.data_ptr(), b, b, k, ref.data_ptr(), 1, _stream()))
+    tiles = -(-V // 128)
+    logits = torch.full((b, V), float("nan"), device="cuda")
+    cand = torch.zeros(b, tiles, 2, dtype=torch.int32, device="cuda")
+    vocab0 = 1000
+    nat.check(lib.tps_linear_argmax(w.data_ptr(), V, k, k, x.data_ptr(), b, b, k, logits.data_ptr(),
+                                    cand.data_ptr(), vocab0, _stream()))
+    torch.cuda.synchronize()
+    assert torch.equal(logits, ref[0])
+    vals = cand[..., 0].view(torch.float32).cpu()
+    idxs = cand[..., 1].cpu()
+    lg = ref[0].cpu()
+    for i in range(b):
+        t = int(vals[i].argmax())
+        m = lg[i].max()
+        assert vals[i, t] == m
+        first = int((lg[i] == m).nonzero()[0])
+        assert int(idxs[i][vals[i] == m].min()) == vocab0 + first
