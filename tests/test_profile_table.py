@@ -50,3 +50,19 @@ def test_reference_loop_replays_the_table():
         want = sum(min(t, s.l_max) for t in sample_response_lengths(s.distribution, s.global_batch, s.seed))
         assert rep.tokens_generated == want
         assert rep.generation_time > 0
+
+
+def test_bench_stage_roofline_units():
+    """bench.stage_roofline: the decode HBM floor of config 2's stage (SURVEY §8(d) units:
+    all weight shards + every live sample's K/V per round) at the measured copy peak."""
+    import argparse
+    import bench
+    ns = argparse.Namespace(model="qwen2.5-7b", per_gpu_batch=64, l_max=8192, prompt_len=512, seed=4, tp_list="",
+                            initial_tp=1)
+    spec, geom = bench.build_spec(ns, 1)
+    r = bench.stage_roofline(spec, geom, decode_s=12.0, peak_gbps=6547.2)
+    w = geom.num_layers * geom.layer_param_bytes + geom.vocab * geom.hidden * 2
+    assert abs(w - 14.14e9) < 0.01e9                     # SURVEY §8(a) a1: 14.14 GB at TP1
+    assert r["rounds"] == 3104 and r["bytes"] > r["rounds"] * w
+    assert abs(r["decode_floor_s"] - r["bytes"] / 6547.2e9) < 1e-9
+    assert 0.6 < r["frac"] < 0.8
