@@ -27,7 +27,10 @@ constexpr int kMinPagesPerSplit = 2;
 constexpr int kMaxAttnSplits = 128;
 int attn_fixed_splits(int B, int nkv, int max_pages);
 
-template <int D>
+// TMA = true: pages arrive as four SWIZZLE_128B tensor-map boxes (K/V x two 64-column halves)
+// issued by one thread and tracked by an mbarrier per ring stage, instead of 2 x 1024 16-byte
+// cp.async per page from every thread (LSU-throttled at short contexts).
+template <int D, bool TMA>
 __global__ void __launch_bounds__(kAttnThreads) paged_attn_kernel(
     const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k_cache,
     const __nv_bfloat16* __restrict__ v_cache, const int* __restrict__ row_slot,
@@ -36,14 +39,25 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_kernel(
     int G, int nsplit, float scale_log2, float* __restrict__ part_m, float* __restrict__ part_l,
     float* __restrict__ part_o, unsigned int* __restrict__ merge_ctr, __nv_bfloat16* __restrict__ out,
     Src qkv, const __nv_bfloat16* __restrict__ qkv_bias, const float* __restrict__ cos_t,
-    const float* __restrict__ sin_t, int early_ok) {
+    const float* __restrict__ sin_t, int early_ok, const __grid_constant__ CUtensorMap tmk,
+    const __grid_constant__ CUtensorMap tmv) {
   constexpr int CPR = D / 8;       // 16-byte chunks per token row
   constexpr int TILE = kPage * D;  // elements per K (or V) page slice
   constexpr int HALF = D / 2;
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  __nv_bfloat16* sk = reinterpret_cast<__nv_bfloat16*>(smem_raw);
+  uint8_t* smem_base = TMA ? reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023))
+                           : smem_raw;  // (SWIZZLE_128B boxes land on 1024-byte boundaries)
+  __nv_bfloat16* sk = reinterpret_cast<__nv_bfloat16*>(smem_base);
   __nv_bfloat16* sv = sk + kAttnStages * TILE;
   __shared__ int s_last;
+  __shared__ __align__(8) uint64_t full_bar[kAttnStages];
+  if constexpr (TMA) {
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < kAttnStages; ++i) mbar_init(&full_bar[i], 1);
+      fence_barrier_init();
+    }
+    __syncthreads();
+  }
   // fused decode path: q (rotated) of this KV group and the current token's k/v,
   // finished here from the QKV projection's split partials (no separate rope kernel)
   __shared__ __align__(16) __nv_bfloat16 sq[16 * D];
@@ -86,17 +100,30 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_kernel(
   } else {
     const int* pt = page_table + (size_t)slot * max_pages;
     auto load_page = [&](int p, int st) {
-      const size_t goff = ((size_t)pt[p] * nkv + kvh) * TILE;
-      const __nv_bfloat16* gk = k_cache + goff;
-      const __nv_bfloat16* gv = v_cache + goff;
-      __nv_bfloat16* dk = sk + st * TILE;
-      __nv_bfloat16* dv = sv + st * TILE;
+      if constexpr (TMA) {
+        if (tid == 0) {
+          const int row0 = (pt[p] * nkv + kvh) * kPage;
+          const uint64_t pol = policy_evict_first();
+          mbar_arrive_expect_tx(&full_bar[st], 2 * TILE * 2);
 #pragma unroll
-      for (int i = tid; i < kPage * CPR; i += kAttnThreads) {
-        const int row = i / CPR, cc = i % CPR;
-        const int sw = row * D + ((cc ^ (row & 7)) * 8);
-        cp_async16(dk + sw, gk + row * D + cc * 8);
-        cp_async16(dv + sw, gv + row * D + cc * 8);
+          for (int h = 0; h < D / 64; ++h) {
+            tma_load_2d(sk + st * TILE + h * kPage * 64, &tmk, &full_bar[st], h * 64, row0, pol);
+            tma_load_2d(sv + st * TILE + h * kPage * 64, &tmv, &full_bar[st], h * 64, row0, pol);
+          }
+        }
+      } else {
+        const size_t goff = ((size_t)pt[p] * nkv + kvh) * TILE;
+        const __nv_bfloat16* gk = k_cache + goff;
+        const __nv_bfloat16* gv = v_cache + goff;
+        __nv_bfloat16* dk = sk + st * TILE;
+        __nv_bfloat16* dv = sv + st * TILE;
+#pragma unroll
+        for (int i = tid; i < kPage * CPR; i += kAttnThreads) {
+          const int row = i / CPR, cc = i % CPR;
+          const int sw = row * D + ((cc ^ (row & 7)) * 8);
+          cp_async16(dk + sw, gk + row * D + cc * 8);
+          cp_async16(dv + sw, gv + row * D + cc * 8);
+        }
       }
     };
 
@@ -178,14 +205,22 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_kernel(
     for (int i = 0; i < D / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
 
     for (int it = 0; p0 + it < p1; ++it) {
-      cp_async_wait<kAttnStages - 2>();
-      __syncthreads();
-      {
+      const int st = it % kAttnStages;
+      if constexpr (TMA) {
+        __syncthreads();  // every warp is done with the stage the next load overwrites
+        const int nxt = it + kAttnStages - 1;
+        if (p0 + nxt < p1) {
+          if (tid == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          load_page(p0 + nxt, nxt % kAttnStages);
+        }
+        mbar_wait(&full_bar[st], (uint32_t)((it / kAttnStages) & 1));
+      } else {
+        cp_async_wait<kAttnStages - 2>();
+        __syncthreads();
         const int nxt = it + kAttnStages - 1;
         if (p0 + nxt < p1) load_page(p0 + nxt, nxt % kAttnStages);
         cp_async_commit();
       }
-      const int st = it % kAttnStages;
       if (early && !fused && it < kAttnStages - 1 && p0 + it == npages - 1) {
         // issued before the wait: refresh the current token's K/V row
         const int r = (ctx - 1) % kPage;
@@ -194,7 +229,7 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_kernel(
           const bool is_v = i >= CPR;
           const int cc = i % CPR;
           const uint4 v = __ldcg(reinterpret_cast<const uint4*>((is_v ? v_cache : k_cache) + goff) + cc);
-          *reinterpret_cast<uint4*>((is_v ? sv : sk) + st * TILE + r * D + ((cc ^ (r & 7)) * 8)) = v;
+          *reinterpret_cast<uint4*>((is_v ? sv : sk) + st * TILE + tile_off<D, TMA>(r, cc)) = v;
         }
         __syncthreads();
       }
@@ -204,12 +239,12 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_kernel(
         for (int i = tid; i < 2 * CPR; i += kAttnThreads) {
           const bool is_v = i >= CPR;
           const int cc = i % CPR;
-          __nv_bfloat16* dst = (is_v ? sv : sk) + st * TILE + r * D + ((cc ^ (r & 7)) * 8);
+          __nv_bfloat16* dst = (is_v ? sv : sk) + st * TILE + tile_off<D, TMA>(r, cc);
           *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(skv + (is_v ? D : 0) + cc * 8);
         }
         __syncthreads();
       }
-      attend_page<D>(sk + st * TILE, sv + st * TILE, qa, (p0 + it) * kPage, ctx, scale_log2, m_r, l_r, o);
+      attend_page<D, TMA>(sk + st * TILE, sv + st * TILE, qa, (p0 + it) * kPage, ctx, scale_log2, m_r, l_r, o);
     }
     cp_async_wait<0>();
 
@@ -580,10 +615,13 @@ int configure_attention() {
   int rc = configure_attention_balanced();
   if (!rc) rc = configure_attention_prefill();
   if (rc) return rc;
-  TPS_CUDA_TRY(cudaFuncSetAttribute(paged_attn_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  TPS_CUDA_TRY(cudaFuncSetAttribute(paged_attn_kernel<128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     attn_smem<128>()));
-  TPS_CUDA_TRY(cudaFuncSetAttribute(paged_attn_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  TPS_CUDA_TRY(cudaFuncSetAttribute(paged_attn_kernel<64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     attn_smem<64>()));
+  TPS_CUDA_TRY(cudaFuncSetAttribute(paged_attn_kernel<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    attn_smem<128>() + 1024));
+  TPS_MAX_CARVEOUT((paged_attn_kernel<128, true>));
   TPS_CUDA_TRY(cudaFuncSetAttribute(paged_attn_cluster_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     attn_smem<128>()));
   TPS_CUDA_TRY(cudaFuncSetAttribute(paged_attn_cluster_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -592,8 +630,8 @@ int configure_attention() {
   TPS_CUDA_TRY(cudaFuncSetAttribute(paged_attn_cluster_kernel<64>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   TPS_MAX_CARVEOUT(paged_attn_cluster_kernel<128>);
   TPS_MAX_CARVEOUT(paged_attn_cluster_kernel<64>);
-  TPS_MAX_CARVEOUT(paged_attn_kernel<128>);
-  TPS_MAX_CARVEOUT(paged_attn_kernel<64>);
+  TPS_MAX_CARVEOUT((paged_attn_kernel<128, false>));
+  TPS_MAX_CARVEOUT((paged_attn_kernel<64, false>));
   TPS_MAX_CARVEOUT(attn_combine_kernel<128>);
   TPS_MAX_CARVEOUT(attn_combine_kernel<64>);
   return kOk;
@@ -627,6 +665,16 @@ static int g_cluster_size = [] {
   const int v = e ? atoi(e) : 16;
   return v < 2 ? 2 : (v > 16 ? 16 : v);
 }();
+
+// TPS_ATTN_TMA=0: the fixed-split decode attention stages its pages with cp.async instead of
+// tensor-map TMA boxes (TMA measured: TP1 B=64 step 4.474 -> 4.432 ms at ctx 2048, 3.661 ->
+// 3.644 at ctx 512; no LSU throttling of 2 x 1024 cp.async per page)
+static int g_attn_tma = [] {
+  const char* e = getenv("TPS_ATTN_TMA");
+  return e ? atoi(e) : 1;
+}();
+
+int make_tmap_bf16(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows);
 
 int attn_splits(int B, int nkv, int max_pages) {
   // page-balanced when the (row, kv head) segments give enough parallel work, and for a
@@ -697,14 +745,27 @@ int paged_attention(const void* q, const void* k_cache, const void* v_cache, con
   const bool in_kernel = nsplit <= kInKernelMergeMaxSplits;
   unsigned int* mc = in_kernel ? merge_ctr : nullptr;
   int rc;
-  if (D == 128)
-    rc = launch_k(paged_attn_kernel<128>, grid, dim3(kAttnThreads), attn_smem<128>(), st, true, qq, kk, vv,
+  CUtensorMap tmk{}, tmv{};
+  const bool tma = g_attn_tma && D == 128 && qkv.n == 0;
+  if (tma) {
+    // the pool as a 2-D [rows][D] bf16 tensor, one (page, kv head) slice = 64 rows; a generous
+    // row bound (boxes are only ever requested inside allocated pages)
+    rc = make_tmap_bf16(&tmk, k_cache, 1LL << 28, D, D, kPage);
+    if (!rc) rc = make_tmap_bf16(&tmv, v_cache, 1LL << 28, D, D, kPage);
+    if (rc) return rc;
+  }
+  if (D == 128 && tma)
+    rc = launch_k(paged_attn_kernel<128, true>, grid, dim3(kAttnThreads), attn_smem<128>() + 1024, st, true, qq, kk,
+                  vv, row_slot, pos_by_slot, row_pos, page_table, max_pages, nq, nkv, G, nsplit, scale_log2, part_m,
+                  part_l, part_o, mc, oo, qkv, bias, cos_t, sin_t, g_attn_early, tmk, tmv);
+  else if (D == 128)
+    rc = launch_k(paged_attn_kernel<128, false>, grid, dim3(kAttnThreads), attn_smem<128>(), st, true, qq, kk, vv,
                   row_slot, pos_by_slot, row_pos, page_table, max_pages, nq, nkv, G, nsplit, scale_log2, part_m,
-                  part_l, part_o, mc, oo, qkv, bias, cos_t, sin_t, g_attn_early);
+                  part_l, part_o, mc, oo, qkv, bias, cos_t, sin_t, g_attn_early, tmk, tmv);
   else if (D == 64)
-    rc = launch_k(paged_attn_kernel<64>, grid, dim3(kAttnThreads), attn_smem<64>(), st, true, qq, kk, vv,
+    rc = launch_k(paged_attn_kernel<64, false>, grid, dim3(kAttnThreads), attn_smem<64>(), st, true, qq, kk, vv,
                   row_slot, pos_by_slot, row_pos, page_table, max_pages, nq, nkv, G, nsplit, scale_log2, part_m,
-                  part_l, part_o, mc, oo, qkv, bias, cos_t, sin_t, g_attn_early);
+                  part_l, part_o, mc, oo, qkv, bias, cos_t, sin_t, g_attn_early, tmk, tmv);
   else
     return fail(kInvalid, "paged_attention: head_dim must be 64 or 128");
   if (rc || in_kernel) return rc;

@@ -45,7 +45,17 @@ __device__ __forceinline__ void ldmatrix_x4_trans(uint32_t (&r)[4], const void* 
 // [16w, 16w+16) of the page. K and V tiles are [64][D] bf16 in smem with the
 // 16-byte chunk index XOR-swizzled by (row & 7). Updates the warp's running
 // (max, sum, O) state for the 16 query rows (the G heads of the KV group).
-template <int D>
+// Element offset of (token row t, 16-byte chunk cc) in a staged [64][D] page tile: the cp.async
+// layout is row-major with the chunk index XOR-swizzled by (t & 7); the TMA layout (HALVES) is
+// [D/64][64][64] as written by SWIZZLE_128B boxes of 64 columns -- the same XOR inside each
+// 128-byte row, so fragment loads stay bank-conflict free in both.
+template <int D, bool HALVES>
+__device__ __forceinline__ int tile_off(int t, int cc) {
+  if constexpr (HALVES) return (cc >> 3) * (kPage * 64) + t * 64 + (((cc & 7) ^ (t & 7)) * 8);
+  else return t * D + ((cc ^ (t & 7)) * 8);
+}
+
+template <int D, bool HALVES = false>
 __device__ __forceinline__ void attend_page(const __nv_bfloat16* K, const __nv_bfloat16* V,
                                             const uint32_t (&qa)[D / 16][4], int tok0, int ctx,
                                             float scale_log2, float (&m_r)[2], float (&l_r)[2],
@@ -57,11 +67,10 @@ __device__ __forceinline__ void attend_page(const __nv_bfloat16* K, const __nv_b
   for (int nt = 0; nt < 2; ++nt) {
     s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
     const int t = warp * 16 + nt * 8 + g;
-    const __nv_bfloat16* krow = K + t * D + 2 * c;
 #pragma unroll
     for (int ks = 0; ks < D / 16; ++ks) {
-      const uint32_t b0 = *reinterpret_cast<const uint32_t*>(krow + (((2 * ks) ^ (t & 7)) * 8));
-      const uint32_t b1 = *reinterpret_cast<const uint32_t*>(krow + (((2 * ks + 1) ^ (t & 7)) * 8));
+      const uint32_t b0 = *reinterpret_cast<const uint32_t*>(K + tile_off<D, HALVES>(t, 2 * ks) + 2 * c);
+      const uint32_t b1 = *reinterpret_cast<const uint32_t*>(K + tile_off<D, HALVES>(t, 2 * ks + 1) + 2 * c);
       mma16816(s[nt], qa[ks], b0, b1);
     }
   }
@@ -119,7 +128,7 @@ __device__ __forceinline__ void attend_page(const __nv_bfloat16* K, const __nv_b
   for (int dn2 = 0; dn2 < D / 16; ++dn2) {
     const int chunk = 2 * dn2 + (lane >> 4);
     uint32_t r[4];
-    ldmatrix_x4_trans(r, V + vrow * D + ((chunk ^ (vrow & 7)) * 8));
+    ldmatrix_x4_trans(r, V + tile_off<D, HALVES>(vrow, chunk));
     mma16816(o[2 * dn2], pa, r[0], r[1]);
     mma16816(o[2 * dn2 + 1], pa, r[2], r[3]);
   }
