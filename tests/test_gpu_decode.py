@@ -130,9 +130,9 @@ def test_qkv_finished_in_gemm_matches_oracle(name, tp):
     run_parity(name, tp, PROMPTS, gen=10, qkv_in_gemm=True)
 
 
-@pytest.mark.parametrize("fuse_rope", [False, True])
-def test_graph_replay_matches_eager(fuse_rope):
-    geom = geometry("tiny")
+@pytest.mark.parametrize("name,fuse_rope", [("tiny", False), ("tiny", True), ("mini-qwen", False)])
+def test_graph_replay_matches_eager(name, fuse_rope):
+    geom = geometry(name)
     outs = []
     for graphs in (False, True):
         ranks, runner = build_group(geom, 2, max_batch=8, num_slots=4, max_len=128, seed=3,
