@@ -37,18 +37,20 @@ static constexpr int bal_smem() {
          + kBalTab * 4;                       // unit table
 }
 
-template <int D>
+template <int D, bool TMA>
 __global__ void __launch_bounds__(kAttnThreads) paged_attn_balanced_kernel(
     const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k_cache,
     const __nv_bfloat16* __restrict__ v_cache, const int* __restrict__ row_slot,
     const int* __restrict__ pos_by_slot, const int* __restrict__ row_pos, const int* __restrict__ page_table,
     int max_pages, int B, int nq, int nkv, int G, float scale_log2, float* __restrict__ part_m,
     float* __restrict__ part_l, float* __restrict__ part_o, unsigned int* __restrict__ merge_ctr,
-    __nv_bfloat16* __restrict__ out) {
+    __nv_bfloat16* __restrict__ out, const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv) {
   constexpr int CPR = D / 8;
   constexpr int TILE = kPage * D;
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  __nv_bfloat16* sk = reinterpret_cast<__nv_bfloat16*>(smem_raw);
+  uint8_t* smem_base = TMA ? reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023))
+                           : smem_raw;  // (SWIZZLE_128B boxes land on 1024-byte boundaries)
+  __nv_bfloat16* sk = reinterpret_cast<__nv_bfloat16*>(smem_base);
   __nv_bfloat16* sv = sk + kAttnStages * TILE;
   float* scr = reinterpret_cast<float*>(sv + kAttnStages * TILE);  // [4 warps][16][32]
   float* wm = scr + kBalScratch;                                    // [4][16]
@@ -58,6 +60,14 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_balanced_kernel(
   int* utab = pre + kBalMaxRows + 1;                                // [kBalTab] page * nkv + head
   __shared__ int s_wsum[4], s_wmax[4];
   __shared__ int s_last, s_cf, s_cl;
+  __shared__ __align__(8) uint64_t full_bar[kAttnStages];
+  if constexpr (TMA) {
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < kAttnStages; ++i) mbar_init(&full_bar[i], 1);
+      fence_barrier_init();
+    }
+    __syncthreads();
+  }
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, c4 = lane & 3;
@@ -140,6 +150,19 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_balanced_kernel(
     }
   };
   auto load_unit = [&](int j, int st) {
+    if constexpr (TMA) {
+      if (tid == 0) {
+        const int row0 = utab[j & (kBalTab - 1)] * kPage;
+        const uint64_t pol = policy_evict_first();
+        mbar_arrive_expect_tx(&full_bar[st], 2 * TILE * 2);
+#pragma unroll
+        for (int hh = 0; hh < D / 64; ++hh) {
+          tma_load_2d(sk + st * TILE + hh * kPage * 64, &tmk, &full_bar[st], hh * 64, row0, pol);
+          tma_load_2d(sv + st * TILE + hh * kPage * 64, &tmv, &full_bar[st], hh * 64, row0, pol);
+        }
+      }
+      return;
+    }
     const size_t goff = (size_t)utab[j & (kBalTab - 1)] * TILE;
     const __nv_bfloat16* gk = k_cache + goff;
     const __nv_bfloat16* gv = v_cache + goff;
@@ -186,9 +209,21 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_balanced_kernel(
   float o[D / 8][4];
   int piece_first = 0;  // first iteration of the current piece
   for (int it = 0; it < n_units; ++it) {
-    cp_async_wait<kAttnStages - 2>();
-    __syncthreads();
-    {
+    if constexpr (TMA) {
+      __syncthreads();  // every warp is done with the stage the next load overwrites
+      const int nxt = it + kAttnStages - 1;
+      if ((nxt & 127) == 0 && nxt >= 128) {
+        fill(nxt + 128);  // slots of units [nxt-128, nxt) are free
+        __syncthreads();
+      }
+      if (nxt < n_units) {
+        if (tid == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        load_unit(nxt, nxt % kAttnStages);
+      }
+      mbar_wait(&full_bar[it % kAttnStages], (uint32_t)((it / kAttnStages) & 1));
+    } else {
+      cp_async_wait<kAttnStages - 2>();
+      __syncthreads();
       const int nxt = it + kAttnStages - 1;
       if ((nxt & 127) == 0 && nxt >= 128) fill(nxt + 128);  // slots of units [nxt-128, nxt) are free
       if (nxt < n_units) load_unit(nxt, nxt % kAttnStages);
@@ -212,11 +247,11 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_balanced_kernel(
         const bool is_v = i >= CPR;
         const int cc = i % CPR;
         const uint4 v = __ldcg(reinterpret_cast<const uint4*>((is_v ? v_cache : k_cache) + goff) + cc);
-        *reinterpret_cast<uint4*>((is_v ? sv : sk) + st * TILE + r * D + ((cc ^ (r & 7)) * 8)) = v;
+        *reinterpret_cast<uint4*>((is_v ? sv : sk) + st * TILE + tile_off<D, TMA>(r, cc)) = v;
       }
       __syncthreads();
     }
-    attend_page<D>(sk + st * TILE, sv + st * TILE, qa, p * kPage, ctx, scale_log2, m_r, l_r, o);
+    attend_page<D, TMA>(sk + st * TILE, sv + st * TILE, qa, p * kPage, ctx, scale_log2, m_r, l_r, o);
 
     const bool seg_end = p == nb - 1;
     if (seg_end || it == n_units - 1) {
@@ -376,22 +411,37 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_balanced_kernel(
 
 static int g_bal_grid[2] = {0, 0};  // resident CTA capacity for D = 64, 128
 
+// TPS_ATTN_TMA_BAL=0: the page-balanced form stages its pages with cp.async instead of TMA boxes
+static int g_bal_tma = [] {
+  const char* e = getenv("TPS_ATTN_TMA_BAL");
+  return e ? atoi(e) : 1;
+}();
+
+int make_tmap_bf16(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows);
+
 int configure_attention_balanced() {
   int dev = 0, sms = 0;
   TPS_CUDA_TRY(cudaGetDevice(&dev));
   TPS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  TPS_CUDA_TRY(cudaFuncSetAttribute(paged_attn_balanced_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    bal_smem<128>()));
-  TPS_CUDA_TRY(cudaFuncSetAttribute(paged_attn_balanced_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    bal_smem<64>()));
-  TPS_MAX_CARVEOUT(paged_attn_balanced_kernel<128>);
-  TPS_MAX_CARVEOUT(paged_attn_balanced_kernel<64>);
+  TPS_CUDA_TRY(cudaFuncSetAttribute(paged_attn_balanced_kernel<128, false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, bal_smem<128>()));
+  TPS_CUDA_TRY(cudaFuncSetAttribute(paged_attn_balanced_kernel<128, true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, bal_smem<128>() + 1024));
+  TPS_CUDA_TRY(cudaFuncSetAttribute(paged_attn_balanced_kernel<64, false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, bal_smem<64>()));
+  TPS_MAX_CARVEOUT((paged_attn_balanced_kernel<128, false>));
+  TPS_MAX_CARVEOUT((paged_attn_balanced_kernel<128, true>));
+  TPS_MAX_CARVEOUT((paged_attn_balanced_kernel<64, false>));
   int occ = 0;
-  TPS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, paged_attn_balanced_kernel<64>, kAttnThreads,
-                                                             bal_smem<64>()));
+  TPS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, paged_attn_balanced_kernel<64, false>,
+                                                             kAttnThreads, bal_smem<64>()));
   g_bal_grid[0] = occ * sms;
-  TPS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, paged_attn_balanced_kernel<128>, kAttnThreads,
-                                                             bal_smem<128>()));
+  int occ_t = 0;
+  TPS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, paged_attn_balanced_kernel<128, false>,
+                                                             kAttnThreads, bal_smem<128>()));
+  TPS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_t, paged_attn_balanced_kernel<128, true>,
+                                                             kAttnThreads, bal_smem<128>() + 1024));
+  if (occ_t < occ) g_bal_tma = 0;  // (the TMA form only where it keeps the residency)
   g_bal_grid[1] = occ * sms;
   if (g_bal_grid[0] <= 0 || g_bal_grid[1] <= 0) return fail(kCuda, "balanced attention: zero occupancy");
   return kOk;
@@ -417,14 +467,23 @@ int paged_attention_balanced(const void* q, const void* k_cache, const void* v_c
   const auto* vv = reinterpret_cast<const __nv_bfloat16*>(v_cache);
   auto* oo = reinterpret_cast<__nv_bfloat16*>(out);
   const dim3 grid(attn_balanced_grid(D));
+  CUtensorMap tmk{}, tmv{};
+  if (D == 128 && g_bal_tma) {
+    int rc = make_tmap_bf16(&tmk, k_cache, 1LL << 28, D, D, kPage);
+    if (!rc) rc = make_tmap_bf16(&tmv, v_cache, 1LL << 28, D, D, kPage);
+    if (rc) return rc;
+    return launch_k(paged_attn_balanced_kernel<128, true>, grid, dim3(kAttnThreads), bal_smem<128>() + 1024, st, true,
+                    qq, kk, vv, row_slot, pos_by_slot, row_pos, page_table, max_pages, B, nq, nkv, G, scale_log2,
+                    part_m, part_l, part_o, merge_ctr, oo, tmk, tmv);
+  }
   if (D == 128)
-    return launch_k(paged_attn_balanced_kernel<128>, grid, dim3(kAttnThreads), bal_smem<128>(), st, true, qq, kk,
-                    vv, row_slot, pos_by_slot, row_pos, page_table, max_pages, B, nq, nkv, G, scale_log2, part_m,
-                    part_l, part_o, merge_ctr, oo);
+    return launch_k(paged_attn_balanced_kernel<128, false>, grid, dim3(kAttnThreads), bal_smem<128>(), st, true, qq,
+                    kk, vv, row_slot, pos_by_slot, row_pos, page_table, max_pages, B, nq, nkv, G, scale_log2, part_m,
+                    part_l, part_o, merge_ctr, oo, tmk, tmv);
   if (D == 64)
-    return launch_k(paged_attn_balanced_kernel<64>, grid, dim3(kAttnThreads), bal_smem<64>(), st, true, qq, kk, vv,
-                    row_slot, pos_by_slot, row_pos, page_table, max_pages, B, nq, nkv, G, scale_log2, part_m,
-                    part_l, part_o, merge_ctr, oo);
+    return launch_k(paged_attn_balanced_kernel<64, false>, grid, dim3(kAttnThreads), bal_smem<64>(), st, true, qq, kk,
+                    vv, row_slot, pos_by_slot, row_pos, page_table, max_pages, B, nq, nkv, G, scale_log2, part_m,
+                    part_l, part_o, merge_ctr, oo, tmk, tmv);
   return fail(kInvalid, "paged_attention: head_dim must be 64 or 128");
 }
 
