@@ -578,6 +578,7 @@ __global__ void argmax_finalize_kernel(CandList cands, int nchunk, WaitSpec wait
   trace_mark(trs, 2);
   float best = -INFINITY;
   int bidx = 0x7fffffff;
+#pragma unroll 4
   for (int k = threadIdx.x; k < cands.n * nchunk; k += blockDim.x) {
     const ArgmaxCand c = cands.p[k / nchunk][(size_t)b * nchunk + (k % nchunk)];
     cand_merge(best, bidx, c.val, c.idx);
@@ -587,6 +588,18 @@ __global__ void argmax_finalize_kernel(CandList cands, int nchunk, WaitSpec wait
     const float v2 = __shfl_xor_sync(0xffffffffu, best, o);
     const int i2 = __shfl_xor_sync(0xffffffffu, bidx, o);
     cand_merge(best, bidx, v2, i2);
+  }
+  if (blockDim.x > 32) {  // (many candidates per row: the LM-head epilogue's per-tile ones)
+    __shared__ float s_v[32];
+    __shared__ int s_i[32];
+    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+      s_v[w] = best;
+      s_i[w] = bidx;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int k = 1; k < nw; ++k) cand_merge(best, bidx, s_v[k], s_i[k]);
   }
   if (threadIdx.x == 0) {
     if (out_tok) out_tok[b] = bidx;
@@ -727,7 +740,8 @@ int argmax_finalize(const CandList& cands, int nchunk, const WaitSpec& wait, int
                     int* pos_by_slot, const int* prompt_len, int* history, int hist_ld, int* out_tok,
                     cudaStream_t st) {
   TPS_CHECK_ARG(B > 0 && cands.n >= 1 && cands.n <= kMaxPeers, "argmax_finalize: bad args");
-  return launch_k(argmax_finalize_kernel, dim3(B), dim3(32), 0, st, true, cands, nchunk, wait, row_slot,
+  const int threads = cands.n * nchunk > 256 ? 256 : 32;
+  return launch_k(argmax_finalize_kernel, dim3(B), dim3(threads), 0, st, true, cands, nchunk, wait, row_slot,
                   pos_by_slot, prompt_len, history, hist_ld, out_tok);
 }
 
