@@ -5,7 +5,7 @@ PKG := paper_2605_23945_b200
 CSRC := $(PKG)/csrc
 LIB := $(PKG)/libtpshift_b200.so
 SRCS := $(CSRC)/abi.cu $(CSRC)/gemm_tcgen05.cu $(CSRC)/decode_ops.cu $(CSRC)/attention.cu $(CSRC)/attention_balanced.cu $(CSRC)/attention_prefill.cu $(CSRC)/copy.cu
-HDRS := $(CSRC)/common.cuh $(CSRC)/decode_ops.cuh include/tpshift_b200.h
+HDRS := $(CSRC)/common.cuh $(CSRC)/decode_ops.cuh $(CSRC)/attention_common.cuh include/tpshift_b200.h
 NVFLAGS := -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
            -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
 

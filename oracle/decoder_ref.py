@@ -116,6 +116,13 @@ class OracleDecoder:
         f0, f1 = p["ffn"]
         v0, v1 = p["vocab"]
         out = {}
+        if self.tp == 1:  # the single rank owns every tensor whole: views, no copies
+            for l in range(self.L):
+                for fam in ("w_qkv", "w_o", "w_gu", "w_d"):
+                    out[(l, fam)] = self.W[(l, fam)]
+                out[(l, "b_qkv")] = self.W.get((l, "b_qkv"))
+            out.update(lm_head=self.W[(-1, "lm_head")], nq=nq, nkv=nkv, F=g["ffn"])
+            return out
         for l in range(self.L):
             wqkv = self.W[(l, "w_qkv")]
             rows = list(range(q0 * D, q1 * D)) + list(range((nq + k0) * D, (nq + k1) * D)) + \
@@ -142,6 +149,86 @@ class OracleDecoder:
             self.cache[key] = (torch.zeros(self.max_len, nkv, self.D), torch.zeros(self.max_len, nkv, self.D))
         return self.cache[key]
 
+    def seed_context(self, sample: int, k_full: torch.Tensor, v_full: torch.Tensor) -> None:
+        """Install a synthetic context for positions [0, P): k_full / v_full [L, P, n_kv, D]
+        (post-RoPE K and V of every KV head, bf16-representable) -- the state a prefill of P
+        tokens would leave; each simulated rank keeps its own KV heads."""
+        P = k_full.shape[1]
+        for l in range(self.L):
+            for r, p in enumerate(self.parts):
+                k0, k1 = p["kv"]
+                kc, vc = self._kv(sample, l, r)
+                kc[:P] = k_full[l, :, k0:k1]
+                vc[:P] = v_full[l, :, k0:k1]
+
+    @torch.no_grad()
+    def prefill(self, tokens, sample: int, start: int = 0) -> torch.Tensor:
+        """Positions start .. start+T-1 of one sample in one pass (causal attention over
+        the cached context plus the chunk), the same rounding points as step(); returns
+        the fp32 logits of the last position [V]. Equivalent to T calls of step()."""
+        g, D = self.geo, self.D
+        T = len(tokens)
+        pos = torch.arange(start, start + T)
+        x = self.W[(-1, "embed")][torch.tensor(tokens)].clone()
+        cos, sin = self.cos[pos][:, None, :], self.sin[pos][:, None, :]
+        scale = 1.0 / math.sqrt(D)
+        S = start + T
+        causal = torch.arange(S)[None, :] > pos[:, None]  # [T, S] True = masked
+        for l in range(self.L):
+            xn = self._r(rms_norm(x, self.W[(l, "ln1")], self.eps))
+            partials = []
+            for r, sh in enumerate(self.shards):
+                nq, nkv = sh["nq"], sh["nkv"]
+                qkv = xn @ sh[(l, "w_qkv")].T
+                if sh[(l, "b_qkv")] is not None:
+                    qkv = qkv + sh[(l, "b_qkv")]
+                q = self._r(rope(qkv[:, :nq * D].view(T, nq, D), cos, sin))
+                k = self._r(rope(qkv[:, nq * D:(nq + nkv) * D].view(T, nkv, D), cos, sin))
+                v = self._r(qkv[:, (nq + nkv) * D:].reshape(T, nkv, D))
+                kc, vc = self._kv(sample, l, r)
+                kc[start:S] = k
+                vc[start:S] = v
+                G = nq // nkv
+                kk = kc[:S].repeat_interleave(G, dim=1)  # [S, nq, D]
+                vv = vc[:S].repeat_interleave(G, dim=1)
+                s = torch.einsum("thd,shd->hts", q, kk) * scale
+                s = s.masked_fill(causal[None], float("-inf"))
+                o = torch.einsum("hts,shd->thd", torch.softmax(s, dim=-1), vv)
+                partials.append(self._r(o).reshape(T, nq * D) @ sh[(l, "w_o")].T)
+            for p_ in partials:
+                x = x + p_
+            xn = self._r(rms_norm(x, self.W[(l, "ln2")], self.eps))
+            partials = []
+            for sh in self.shards:
+                gu = xn @ sh[(l, "w_gu")].T
+                F = sh["F"]
+                act = self._r(torch.nn.functional.silu(gu[:, :F]) * gu[:, F:])
+                partials.append(act @ sh[(l, "w_d")].T)
+            for p_ in partials:
+                x = x + p_
+        xn = self._r(rms_norm(x[-1:], self.W[(-1, "ln_f")], self.eps))
+        return torch.cat([xn @ sh["lm_head"].T for sh in self.shards], dim=1)[0]
+
+    def _attend(self, q, k, v, positions, samples, l, r):
+        """Decode attention of B rows against their cached contexts (rows' own K/V appended
+        first). One batched masked SDPA over the padded contexts (vectorised over rows)."""
+        B, nq, D = q.shape
+        nkv = k.shape[1]
+        G = nq // nkv
+        for i in range(B):
+            kc, vc = self._kv(samples[i], l, r)
+            kc[positions[i]] = k[i]
+            vc[positions[i]] = v[i]
+        S = max(positions) + 1
+        K = torch.stack([self._kv(s, l, r)[0][:S] for s in samples])  # [B, S, nkv, D]
+        V = torch.stack([self._kv(s, l, r)[1][:S] for s in samples])
+        qg = q.view(B, nkv, G, D)
+        s = torch.einsum("bkgd,bskd->bkgs", qg, K) / math.sqrt(D)
+        mask = torch.arange(S)[None, :] > torch.tensor(positions)[:, None]  # [B, S]
+        s = s.masked_fill(mask[:, None, None, :], float("-inf"))
+        o = torch.einsum("bkgs,bskd->bkgd", torch.softmax(s, dim=-1), V)
+        return o.reshape(B, nq, D)
+
     @torch.no_grad()
     def step(self, tokens, positions, samples) -> torch.Tensor:
         """One decode round: row i processes token tokens[i] at position positions[i]
@@ -152,7 +239,6 @@ class OracleDecoder:
         pos = torch.tensor(positions)
         x = self.W[(-1, "embed")][torch.tensor(tokens)].clone()
         cos, sin = self.cos[pos][:, None, :], self.sin[pos][:, None, :]
-        scale = 1.0 / math.sqrt(D)
         for l in range(self.L):
             xn = self._r(rms_norm(x, self.W[(l, "ln1")], self.eps))
             partials = []
@@ -167,19 +253,7 @@ class OracleDecoder:
                 q = self._r(rope(q, cos, sin))
                 k = self._r(rope(k, cos, sin))
                 v = self._r(v)
-                G = nq // nkv
-                o = torch.empty(B, nq, D)
-                for i in range(B):
-                    kc, vc = self._kv(samples[i], l, r)
-                    p = positions[i]
-                    kc[p] = k[i]
-                    vc[p] = v[i]
-                    kk = kc[:p + 1].repeat_interleave(G, dim=1)  # [T, nq, D]
-                    vv = vc[:p + 1].repeat_interleave(G, dim=1)
-                    s = torch.einsum("hd,thd->ht", q[i], kk) * scale
-                    pr = torch.softmax(s, dim=-1)
-                    o[i] = torch.einsum("ht,thd->hd", pr, vv)
-                o = self._r(o).reshape(B, nq * D)
+                o = self._r(self._attend(q, k, v, positions, samples, l, r)).reshape(B, nq * D)
                 partials.append(o @ sh[(l, "w_o")].T)
             for p_ in partials:
                 x = x + p_

@@ -305,9 +305,12 @@ class B200Backend:
                 r.kv.release(r.slots.pages.get(slot, []))
                 r.slots.release(slot)
 
+    def planned_state_method(self, decision, naive_mode: bool) -> str:
+        return self.state_method or decision.breakdown.state_method
+
     def realize_switch(self, node: NodeState, decision, statuses, merged, naive_mode: bool):
         quote = decision.breakdown
-        method = self.state_method or quote.state_method
+        method = self.planned_state_method(decision, naive_mode)
         self._execute_switch(decision.target.tp, merged, recompute=method == RECOMPUTE)
         # host-side placeholder with the realised method; the reported clocks come from
         # the recorded events (RecordedBackend)
@@ -540,6 +543,9 @@ class RecordedBackend:
         ends = np.asarray(self.groups[key]["rounds"][i:i + n], dtype=float)
         self.cursor[key] = i + n
         return np.diff(np.concatenate([[group.clock], ends]))
+
+    def planned_state_method(self, decision, naive_mode) -> str:
+        return self.switch_meas[self.nswitch]["method"]
 
     def realize_switch(self, node, decision, statuses, merged, naive_mode):
         m = self.switch_meas[self.nswitch]

@@ -178,8 +178,9 @@ def cached_weight_pulls(geom: DecoderGeometry, old: Layout, new: Layout, dst_ran
     key = (geom.name, geom.num_layers, geom.hidden, old, new, dst_rank)
     if key not in _WEIGHT_PLANS:
         wp = plan_weight_pulls(geom, old, new, dst_rank)
-        total = arena_layout(geom, rank_shard(geom, new.tp, new.tp_rank(dst_rank))).total_bytes
-        check(verify_cover(wp, total, allow_gaps=True), "weight pull plan")
+        lay = arena_layout(geom, rank_shard(geom, new.tp, new.tp_rank(dst_rank)))
+        check(verify_cover(wp, lay.total_bytes, allow_gaps=True), "weight pull plan")
+        check(verify_entries(wp, lay), "weight pull plan")
         _WEIGHT_PLANS[key] = wp
     return _WEIGHT_PLANS[key]
 
@@ -292,6 +293,27 @@ def verify_cover(pieces: Pieces, total_bytes: int, allow_gaps: bool = False) -> 
         covered = int(n.sum())
         if covered != total_bytes:
             issues.append(f"covers {covered} of {total_bytes} bytes")
+    return issues
+
+
+def verify_entries(pieces: Pieces, layout) -> list[str]:
+    """Every tensor of an arena layout is covered exactly: no piece crosses a tensor's payload
+    bounds (or lands in the 256-B alignment padding) and each tensor's payload bytes are all
+    written. With verify_cover's no-overlap check this is exactly-once coverage of every
+    payload byte, which allow_gaps alone (padding is never written) cannot show."""
+    _, _, do, nb = pieces.arrays()
+    ents = sorted((off, 2 * int(np.prod(shape))) for off, shape in layout.entries.values())
+    starts = np.array([e[0] for e in ents], dtype=np.int64)
+    sizes = np.array([e[1] for e in ents], dtype=np.int64)
+    idx = np.searchsorted(starts, do, side="right") - 1
+    issues = []
+    if np.any(idx < 0) or np.any(do + nb > starts[np.maximum(idx, 0)] + sizes[np.maximum(idx, 0)]):
+        issues.append("piece outside a tensor payload")
+        return issues
+    got = np.bincount(idx, weights=nb.astype(np.float64), minlength=len(ents)).astype(np.int64)
+    missing = int(np.count_nonzero(got != sizes))
+    if missing:
+        issues.append(f"{missing} tensors not covered exactly")
     return issues
 
 

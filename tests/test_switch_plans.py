@@ -178,3 +178,24 @@ def test_prefill_group_table():
     assert got == [i for i in range(len(rs)) if rs[i] >= 0]
     for g in range(len(n)):
         assert len({int(rs[r]) for r in rows[g, :n[g]]}) <= 1
+
+
+def test_weight_plan_entry_coverage_check():
+    """verify_entries accepts every real weight plan and rejects a plan missing one piece or
+    writing into alignment padding (the runtime check cached_weight_pulls applies)."""
+    from paper_2605_23945_b200.switch_executor import Pieces, cached_weight_pulls, verify_entries
+    geom = geometry("mini-qwen")
+    old, new = Layout(1, 4), Layout(4, 4)
+    for r in range(4):
+        wp = cached_weight_pulls(geom, old, new, r)
+        lay = arena_layout(geom, rank_shard(geom, 4, r))
+        assert verify_entries(wp, lay) == []
+        sr, so, do, nb = wp.arrays()
+        cut = Pieces()
+        cut.add(sr[1:], so[1:], do[1:], nb[1:])
+        assert verify_entries(cut, lay)
+        off, shape = lay.entries[(-1, "ln_f")]
+        pad = Pieces()
+        pad.add(sr, so, do, nb)
+        pad.add(np.array([0]), np.array([0]), np.array([off + 2 * int(np.prod(shape))]), np.array([2]))
+        assert verify_entries(pad, lay)
