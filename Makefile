@@ -1,19 +1,31 @@
-# Builds the sm_100a engine library in-tree (the .so travels to the GPU box with
-# the gpurun snapshot). The oracle (oracle/) is Python/numpy: nothing to compile.
+# Builds the sm_100a engine library in-tree (the .so travels to the GPU box with the gpurun
+# snapshot). One object per translation unit (make -j builds them in parallel; -MMD tracks
+# header dependencies). The oracle (oracle/) is Python/numpy: nothing to compile.
 NVCC ?= /usr/local/cuda/bin/nvcc
 PKG := paper_2605_23945_b200
 CSRC := $(PKG)/csrc
 LIB := $(PKG)/libtpshift_b200.so
-SRCS := $(CSRC)/abi.cu $(CSRC)/gemm_tcgen05.cu $(CSRC)/decode_ops.cu $(CSRC)/attention.cu $(CSRC)/attention_balanced.cu $(CSRC)/attention_prefill.cu $(CSRC)/copy.cu
-HDRS := $(CSRC)/common.cuh $(CSRC)/decode_ops.cuh $(CSRC)/attention_common.cuh include/tpshift_b200.h
+OBJDIR := build/obj
+SRCS := abi gemm_tcgen05 decode_ops attention attention_balanced attention_prefill copy persist
+OBJS := $(SRCS:%=$(OBJDIR)/%.o)
 NVFLAGS := -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
            -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
 
 .PHONY: all clean
 all: $(LIB)
 
-$(LIB): $(SRCS) $(HDRS)
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) 2> build_ptxas.log || (cat build_ptxas.log; false)
+$(OBJDIR)/%.o: $(CSRC)/%.cu Makefile
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -MMD -MP -c -o $@ $< 2> $(OBJDIR)/$*.ptxas.log || (cat $(OBJDIR)/$*.ptxas.log; false)
+
+$(LIB): $(OBJS)
+	$(NVCC) -gencode arch=compute_100a,code=sm_100a -shared -o $@ $(OBJS)
+	cat $(OBJDIR)/*.ptxas.log > build_ptxas.log
+
+-include $(OBJS:.o=.d)
 
 clean:
-	rm -f $(LIB) build_ptxas.log
+	rm -rf $(LIB) build_ptxas.log $(OBJDIR)
+
+
+

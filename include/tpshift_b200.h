@@ -300,6 +300,82 @@ int tps_ipc_close(void* base);
  * at records[4 * atomicAdd(counter, 1)] (up to `capacity` records). NULL, NULL disables. */
 int tps_trace_enable(uint64_t* records, unsigned int* counter, unsigned int capacity);
 
+
+/* ------------------------------------------------ persistent decode step --- *
+ * One launch per decode step for tail batches (B <= 16, head_dim 128): the whole step
+ * (embedding, every layer's QKV / RoPE + paged KV append / attention / O + TP allreduce /
+ * RMSNorm / gate-up + SiLU / down + TP allreduce, LM head, greedy argmax) in one cooperative
+ * grid of one CTA per SM per rank. Replaces, for the post-switch tail, the same
+ * oracle_decode_latency step (tpshift/latency.py:111-133) the per-kernel entry points above
+ * implement; the TP allreduce uses the LL slots of tps_linear_push_ll (S = 1 layout) and the
+ * phase counters stay at epoch * tp, so a layout may alternate between the two forms. */
+typedef struct tps_persist_geom {
+  int num_layers;
+  int hidden;
+  int head_dim;   /* 128 */
+  int n_phases;   /* 2 * num_layers + 1 (LL tag = epoch * n_phases + phase) */
+  float rms_eps;
+} tps_persist_geom;
+
+typedef struct tps_persist_rank {
+  /* weights: arrays of num_layers device pointers (bf16, row-major, the rank's shard) */
+  const void* const* w_qkv;
+  const void* const* b_qkv;       /* NULL array: no bias */
+  const void* const* w_o;
+  const void* const* w_gu;        /* interleaved 64-row [gate | up] blocks */
+  const void* const* w_d;
+  const void* const* ln1;
+  const void* const* ln2;
+  const void* embed;
+  const void* ln_f;
+  const void* lm_head;
+  void* const* k_cache;           /* per layer [pages][nkv][64][128] */
+  void* const* v_cache;
+  int nq, nkv, ffn, vocab, vocab_off;  /* local query / KV heads, FFN width, vocab rows, offset */
+  int nq_of[8];                   /* query heads of every rank of the group (rank order) */
+  /* slot state (tps_paged_attention / tps_argmax_finalize conventions) */
+  const int* row_slot;
+  int* pos;
+  const int* page_table;
+  int max_pages;
+  int* history;
+  int hist_ld;
+  const int* prompt_len;
+  int* out_tok;
+  float* logits;                  /* [16][vocab] fp32 logits of the step (parity checks) */
+  const float* cos_t;             /* [max_pos][64] */
+  const float* sin_t;
+  void* work;                     /* zero-initialised, tps_persist_work_bytes() bytes */
+  int64_t work_bytes;
+  /* TP exchange (tp > 1): LL areas [2][src][rows][hidden] uint64 and argmax areas
+   * [2][8][16][2] uint64 of every rank (rank order); loopback: this rank plays every peer */
+  int tp, rank, loopback;
+  int64_t ll_par_stride, ll_src_stride;
+  uint64_t* ll_peer[8];
+  uint64_t* ll_mine;
+  uint64_t* am_peer[8];
+  uint64_t* am_mine;
+  uint64_t* epoch;                /* group epoch (advanced by the step) */
+  uint64_t* ctr;                  /* group phase counters (kept at epoch * tp) */
+  uint64_t* trace;                /* probe (or NULL): [CTA][16] %globaltimer marks of layer trace_layer */
+  int trace_layer;
+} tps_persist_rank;
+
+/* sizeof(tps_persist_geom) (which 0) / sizeof(tps_persist_rank) (which 1): binding check. */
+int64_t tps_persist_struct_bytes(int which);
+/* 1 if the persistent step supports this rank's shapes at batch B. */
+int tps_persist_supported(const tps_persist_geom* g, const tps_persist_rank* r, int B);
+/* Bytes of the per-rank workspace (counters, residual, partials, logits) for `ctas` CTAs. */
+int64_t tps_persist_work_bytes(const tps_persist_geom* g, const tps_persist_rank* r, int ctas);
+/* Bytes of a launch context for nranks ranks. */
+int64_t tps_persist_ctx_bytes(const tps_persist_geom* g, int nranks);
+/* Encode the tensor maps and pointer tables of nranks ranks (one process's ranks of one
+ * group: the whole virtual group, or a single rank) for bucket B into dev_ctx (synchronous). */
+int tps_persist_prepare(const tps_persist_geom* g, const tps_persist_rank* ranks, int nranks, int B, int ctas,
+                        void* dev_ctx, void* stream);
+/* One decode step: nranks * ctas CTAs (cooperative), stream-ordered. */
+int tps_persist_launch(const void* dev_ctx, int nranks, int ctas, int B, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

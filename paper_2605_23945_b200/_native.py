@@ -79,7 +79,32 @@ SIGNATURES = {
     "tps_ipc_open": (_i32, [_vp, ctypes.POINTER(_vp)]),
     "tps_ipc_close": (_i32, [_vp]),
     "tps_trace_enable": (_i32, [_vp, _vp, ctypes.c_uint]),
+    "tps_persist_struct_bytes": (_i64, [_i32]),
+    "tps_persist_supported": (_i32, [_vp, _vp, _i32]),
+    "tps_persist_work_bytes": (_i64, [_vp, _vp, _i32]),
+    "tps_persist_ctx_bytes": (_i64, [_vp, _i32]),
+    "tps_persist_prepare": (_i32, [_vp, _vp, _i32, _i32, _i32, _vp, _vp]),
+    "tps_persist_launch": (_i32, [_vp, _i32, _i32, _i32, _vp]),
 }
+
+
+class PersistGeom(ctypes.Structure):
+    """tps_persist_geom (include/tpshift_b200.h)."""
+    _fields_ = [("num_layers", _i32), ("hidden", _i32), ("head_dim", _i32), ("n_phases", _i32),
+                ("rms_eps", _f32)]
+
+
+class PersistRank(ctypes.Structure):
+    """tps_persist_rank (include/tpshift_b200.h)."""
+    _fields_ = [("w_qkv", _vp), ("b_qkv", _vp), ("w_o", _vp), ("w_gu", _vp), ("w_d", _vp), ("ln1", _vp),
+                ("ln2", _vp), ("embed", _vp), ("ln_f", _vp), ("lm_head", _vp), ("k_cache", _vp), ("v_cache", _vp),
+                ("nq", _i32), ("nkv", _i32), ("ffn", _i32), ("vocab", _i32), ("vocab_off", _i32),
+                ("nq_of", _i32 * 8), ("row_slot", _vp), ("pos", _vp), ("page_table", _vp), ("max_pages", _i32), ("history", _vp),
+                ("hist_ld", _i32), ("prompt_len", _vp), ("out_tok", _vp), ("logits", _vp), ("cos_t", _vp),
+                ("sin_t", _vp), ("work", _vp), ("work_bytes", _i64), ("tp", _i32), ("rank", _i32),
+                ("loopback", _i32), ("ll_par_stride", _i64), ("ll_src_stride", _i64), ("ll_peer", _vp * 8),
+                ("ll_mine", _vp), ("am_peer", _vp * 8), ("am_mine", _vp), ("epoch", _vp), ("ctr", _vp), ("trace", _vp),
+                ("trace_layer", _i32)]
 
 
 class TpsWait(ctypes.Structure):

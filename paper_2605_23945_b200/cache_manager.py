@@ -120,7 +120,7 @@ class CacheManager:
             return self.pool[tp]
         comms = {r: GroupComm(tp, r % tp, self.max_batch, self.hidden, self.n_phases, self.world.devices[r])
                  for r in self.world.local_ranks}
-        ptrs = self.world.share({r: {"recv": c.recv, "ll": c.ll, "ctr": c.ctr, "cand": c.cand}
+        ptrs = self.world.share({r: {"recv": c.recv, "ll": c.ll, "ctr": c.ctr, "cand": c.cand, "am": c.am}
                                  for r, c in comms.items()})
         for r, c in comms.items():
             g0 = (r // tp) * tp

@@ -69,6 +69,7 @@ int configure_gemm();
 int configure_attention();
 int configure_copy();
 int configure_decode_ops();
+int configure_persist();
 int reduce_push_ll(const Src& src, const DstList& dst, long long n, const uint64_t* epoch, uint32_t mult,
                    uint32_t add, cudaStream_t st);
 int linear_push_ll(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
@@ -141,6 +142,7 @@ int tps_init(int device, int* sm_count) {
   if (!rc) rc = configure_attention();
   if (!rc) rc = configure_copy();
   if (!rc) rc = configure_decode_ops();
+  if (!rc) rc = configure_persist();
   return rc;
 }
 

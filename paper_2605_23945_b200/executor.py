@@ -83,6 +83,11 @@ LL_CLUSTER_ROWS = int(os.environ.get("TPS_LL_CLUSTER_ROWS", "64"))
 # stage 63.4 -> 65.5 s predicted; Qwen2.5-7B TP2 B <= 32 +2-3 % in loopback)
 LL_CLUSTER_MIN_TP = 4
 FUSE_SOURCES = 16  # LL slots per parity: tp x splits partials of one fused allreduce (one load batch)
+# persistent decode step (csrc/persist.cu): one launch per step for B <= PERSIST_MAX_ROWS.
+# Parity-green but measured slower than the per-kernel step on B200 (TP8 B=1 1.80 vs 1.30 ms,
+# TP1 B=1 4.28 vs 3.00 ms): opt-in (TPS_PERSIST=1 or use_persist)
+PERSIST_MAX_ROWS = 16
+PERSIST = os.environ.get("TPS_PERSIST", "0") == "1"
 
 
 class GroupComm:
@@ -108,6 +113,8 @@ class GroupComm:
         # tags start at 0 and live tags are >= n_phases (epochs start at 1): no stale match
         self.ll = torch.zeros((2, FUSE_SOURCES, FUSE_ROWS, hidden), dtype=torch.int64, device=device)
         self.cand = torch.zeros((max_batch, 64, 2), dtype=torch.int32, device=device)
+        # persistent step's argmax exchange: LL {value, tag} / {index, tag} per (parity, src, row)
+        self.am = torch.zeros((2, 8, PERSIST_MAX_ROWS, 2), dtype=torch.int64, device=device)
         self.ctr = torch.zeros(n_phases, dtype=torch.int64, device=device)
         self.done = torch.zeros(n_phases, dtype=torch.int32, device=device)
         self.epoch = torch.ones(1, dtype=torch.int64, device=device)
@@ -117,11 +124,12 @@ class GroupComm:
         self.loopback = False  # timing harness: this rank plays every peer of its group
         self.peer_ctr: list[int] = []
         self.peer_cand: list[int] = []
+        self.peer_am: list[int] = []
 
     # local export for peers
     def export(self) -> dict:
         return {"recv": self.recv.data_ptr(), "ll": self.ll.data_ptr(), "ctr": self.ctr.data_ptr(),
-                "cand": self.cand.data_ptr()}
+                "cand": self.cand.data_ptr(), "am": self.am.data_ptr()}
 
     def connect(self, tables: list[dict]) -> None:
         assert len(tables) == self.tp
@@ -129,6 +137,7 @@ class GroupComm:
         self.peer_ll = [t["ll"] for t in tables]
         self.peer_ctr = [t["ctr"] for t in tables]
         self.peer_cand = [t["cand"] for t in tables]
+        self.peer_am = [t["am"] for t in tables]
 
     def recv_slot(self, base: int, parity: int, src_rank: int) -> int:
         return base + ((parity * self.tp + src_rank) * self.max_batch * self.hidden) * 4
@@ -251,6 +260,13 @@ class InferExecutor:
             self.grp_n = torch.zeros(prefill_rows, dtype=torch.int32, device=dev)
         self.graphs: dict[int, torch.cuda.CUDAGraph] = {}
         self.launch_stats: dict[int, LaunchStats] = {}
+        # persistent step (csrc/persist.cu) state: workspace, logits, CTAs per rank it was sized for
+        self.use_persist = PERSIST
+        self.p_work: torch.Tensor | None = None
+        self.p_logits: torch.Tensor | None = None
+        self.p_ctas = 0
+        self.p_trace: torch.Tensor | None = None   # tools/persist_trace.py
+        self.p_trace_layer = -1
 
     # ------------------------------------------------------------ shapes ---
     def buckets(self) -> list[int]:
@@ -573,6 +589,95 @@ class InferExecutor:
                                    self.xn.data_ptr(), H, st), "tps_add_norm")
         stats.add("add_norm")
 
+    # ------------------------------------------------ persistent decode step ---
+    def persist_geom(self) -> "nat.PersistGeom":
+        g = self.geom
+        return nat.PersistGeom(num_layers=g.num_layers, hidden=g.hidden, head_dim=g.head_dim,
+                               n_phases=2 * g.num_layers + 1, rms_eps=g.rms_eps)
+
+    def persist_ok(self, B: int) -> bool:
+        """The step for bucket B can run as one persistent launch (csrc/persist.cu): tail
+        batches, head_dim 128, greedy, no timing-probe skips."""
+        if not (self.use_persist and B <= PERSIST_MAX_ROWS and self.geom.head_dim == 128
+                and self.temperature <= 0 and not self.skip and B in self.row_slot):
+            return False
+        if self.comm is not None and self.comm.tp > 8:
+            return False
+        return bool(nat.lib().tps_persist_supported(ctypes.byref(self.persist_geom()),
+                                                     ctypes.byref(self._persist_desc(B, 0)[0]), B))
+
+    def _persist_desc(self, B: int, ctas: int):
+        """tps_persist_rank of this rank for bucket B (and the host arrays it points to)."""
+        g, W, sl = self.geom, self.w, self.slots
+        L = g.num_layers
+        keep = []
+
+        def arr(ptrs):
+            a = nat.ptr_array(ptrs)
+            keep.append(a)
+            return ctypes.cast(a, ctypes.c_void_p)
+
+        r = nat.PersistRank()
+        r.w_qkv = arr([W.tensor_ptr(l, "w_qkv") for l in range(L)])
+        r.b_qkv = arr([W.tensor_ptr(l, "b_qkv") for l in range(L)]) if g.qkv_bias else None
+        r.w_o = arr([W.tensor_ptr(l, "w_o") for l in range(L)])
+        r.w_gu = arr([W.tensor_ptr(l, "w_gu") for l in range(L)])
+        r.w_d = arr([W.tensor_ptr(l, "w_d") for l in range(L)])
+        r.ln1 = arr([W.tensor_ptr(l, "ln1") for l in range(L)])
+        r.ln2 = arr([W.tensor_ptr(l, "ln2") for l in range(L)])
+        r.embed = W.tensor_ptr(-1, "embed")
+        r.ln_f = W.tensor_ptr(-1, "ln_f")
+        r.lm_head = W.tensor_ptr(-1, "lm_head")
+        r.k_cache = arr([self.kv.layer_ptrs(l)[0] for l in range(L)])
+        r.v_cache = arr([self.kv.layer_ptrs(l)[1] for l in range(L)])
+        r.nq, r.nkv, r.ffn, r.vocab, r.vocab_off = self.nq, self.nkv, self.F, self.V, self.shard.vocab[0]
+        for q in range(self.tp):
+            r.nq_of[q] = rank_shard(g, self.tp, q).n_q
+        r.row_slot = self.row_slot[B].data_ptr()
+        r.pos = sl.pos.data_ptr()
+        r.page_table = sl.page_table.data_ptr()
+        r.max_pages = sl.max_pages
+        r.history = sl.history.data_ptr()
+        r.hist_ld = sl.max_len
+        r.prompt_len = self.prompt_len.data_ptr()
+        r.out_tok = self.out_tok.data_ptr()
+        r.logits = self.p_logits.data_ptr() if self.p_logits is not None else None
+        r.cos_t = self.cos.data_ptr()
+        r.sin_t = self.sin.data_ptr()
+        r.work = self.p_work.data_ptr() if self.p_work is not None else None
+        r.work_bytes = self.p_work.numel() if self.p_work is not None else 0
+        cm = self.comm
+        r.tp = self.tp
+        r.rank = self.rank
+        if cm is not None:
+            H = g.hidden
+            r.loopback = 1 if cm.loopback else 0
+            r.ll_par_stride = FUSE_SOURCES * FUSE_ROWS * H
+            r.ll_src_stride = FUSE_ROWS * H
+            for q in range(cm.tp):
+                r.ll_peer[q] = cm.peer_ll[q]
+                r.am_peer[q] = cm.peer_am[q]
+            r.ll_mine = cm.ll.data_ptr()
+            r.am_mine = cm.am.data_ptr()
+            r.epoch = cm.epoch.data_ptr()
+            r.ctr = cm.ctr.data_ptr()
+        if self.p_trace is not None:  # probe: per-CTA phase marks of one layer
+            r.trace = self.p_trace.data_ptr()
+            r.trace_layer = self.p_trace_layer
+        return r, keep
+
+    def persist_alloc(self, ctas: int) -> None:
+        """Workspace (zeroed: step counters start at 0) and logits buffer of the persistent step."""
+        if self.p_ctas == ctas:
+            return
+        r, _ = self._persist_desc(max(b for b in self.row_slot if b <= PERSIST_MAX_ROWS), ctas)
+        n = nat.lib().tps_persist_work_bytes(ctypes.byref(self.persist_geom()), ctypes.byref(r), ctas)
+        if n < 0:
+            raise RuntimeError("tps_persist_work_bytes failed")
+        self.p_work = torch.zeros(int(n), dtype=torch.uint8, device=self.device)
+        self.p_logits = torch.zeros((PERSIST_MAX_ROWS, self.V), dtype=torch.float32, device=self.device)
+        self.p_ctas = ctas
+
     # ----------------------------------------------------------- batching ---
     def set_rows(self, B: int, slots: list[int]) -> None:
         """Bind batch rows of bucket B to sample slots (padding rows -> -1)."""
@@ -606,14 +711,64 @@ class GroupRunner:
         self.graphs: dict[int, torch.cuda.CUDAGraph] = {}
         self.stats: dict[int, LaunchStats] = {}
         self.stream = torch.cuda.current_stream(executors[0].device)
+        self._pctx: dict[int, tuple] = {}          # bucket -> (device launch context, CTAs per rank)
+        self._persist_checked: dict[int, bool] = {}
 
     def set_rows(self, B: int, slots: list[int]) -> None:
         for e in self.ex:
             e.set_rows(B, slots)
 
     def _issue(self, B: int, st: int) -> LaunchStats:
+        if self.persist_ok(B):
+            return self._issue_persist(B, st)
         stats = LaunchStats()
         run_programs([e.program(B, st, stats) for e in self.ex])
+        return stats
+
+    # ------------------------------------------------ persistent decode step ---
+    def persist_ok(self, B: int) -> bool:
+        """One persistent launch per step (csrc/persist.cu) when every rank of this runner
+        takes the shape and the runner drives the whole group (virtual) or one rank of it."""
+        ex0 = self.ex[0]
+        if len(self.ex) not in (1, ex0.tp):
+            return False
+        if B not in self._persist_checked:
+            self._persist_checked[B] = all(e.persist_ok(B) for e in self.ex)
+        return self._persist_checked[B]
+
+    def persist_ctas(self) -> int:
+        sms = torch.cuda.get_device_properties(self.ex[0].device).multi_processor_count
+        return sms // len(self.ex)
+
+    def prepare_persist(self, B: int) -> None:
+        """Encode the tensor maps / pointer tables of bucket B (synchronous; outside capture)."""
+        if B in self._pctx or not self.persist_ok(B):
+            return
+        ctas = self.persist_ctas()
+        descs, keep = [], []
+        for e in self.ex:
+            e.persist_alloc(ctas)
+            r, k = e._persist_desc(B, ctas)
+            descs.append(r)
+            keep.append(k)
+        arr = (nat.PersistRank * len(descs))(*descs)
+        geom = self.ex[0].persist_geom()
+        n = nat.lib().tps_persist_ctx_bytes(ctypes.byref(geom), len(descs))
+        ctx = torch.empty(int(n), dtype=torch.uint8, device=self.ex[0].device)
+        nat.check(nat.lib().tps_persist_prepare(ctypes.byref(geom), arr, len(descs), B, ctas, ctx.data_ptr(),
+                                                torch.cuda.current_stream(self.ex[0].device).cuda_stream),
+                  "tps_persist_prepare")
+        self._pctx[B] = (ctx, ctas)
+
+    def _issue_persist(self, B: int, st: int) -> LaunchStats:
+        if B not in self._pctx:
+            self.prepare_persist(B)
+        ctx, ctas = self._pctx[B]
+        nat.check(nat.lib().tps_persist_launch(ctx.data_ptr(), len(self.ex), ctas, B, st), "tps_persist_launch")
+        for e in self.ex:
+            e._last_lm_srcs = ((e.p_logits.data_ptr(), 1, B * e.V), B)
+        stats = LaunchStats()
+        stats.add("persist_step")
         return stats
 
     def capture(self, B: int) -> None:
@@ -626,6 +781,7 @@ class GroupRunner:
         """
         if B in self.graphs:
             return
+        self.prepare_persist(B)  # (synchronous setup must not run inside the capture)
         g = torch.cuda.CUDAGraph()
         if not hasattr(self, "_cap_stream"):
             self._cap_stream = torch.cuda.Stream(self.ex[0].device)

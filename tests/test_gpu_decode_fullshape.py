@@ -120,11 +120,13 @@ def compare(logits, hist, orc, slots_rows, starts, steps, tol, mean_tol=MEAN_TOL
     return worst
 
 
-def run_long_context(name, tp, ctx, gen=3, layers=2, tol=0.05, noise_floor=False):
+def run_long_context(name, tp, ctx, gen=3, layers=2, tol=0.05, noise_floor=False, persist=False):
     geom = truncated(name, layers)
     B = len(ctx)
     max_len = max(ctx) + gen + 8
     ranks, runner = build(geom, tp, max_batch=max(B, 8), num_slots=B, max_len=max_len)
+    for r in ranks:  # B <= 16: the persistent one-launch step, else the per-kernel step
+        r.executor.use_persist = persist
     gtok = torch.Generator().manual_seed(len(ctx))
     slots = []
     for i, P in enumerate(ctx):
@@ -143,6 +145,7 @@ def run_long_context(name, tp, ctx, gen=3, layers=2, tol=0.05, noise_floor=False
     torch.cuda.synchronize()
     for r in ranks[1:]:
         assert torch.equal(r.slots.history[slots].cpu(), hist)
+    assert runner.persist_ok(bucket) == (persist and B <= 16)
     W = oracle_weights(geom)
     orc = OracleDecoder(geo_dict(geom), W, tp=tp, round_bf16=True, max_len=max_len)
     fp32 = OracleDecoder(geo_dict(geom), W, tp=tp, round_bf16=False, max_len=max_len) if noise_floor else None
@@ -151,24 +154,28 @@ def run_long_context(name, tp, ctx, gen=3, layers=2, tol=0.05, noise_floor=False
         if fp32 is not None:
             fp32.seed_context(b, k, v)
     worst = compare(logits, hist, orc, slots, list(ctx), gen, tol, fp32=fp32)
-    print(f"{name} L={geom.num_layers} tp={tp} ctx={max(ctx)} B={B}: max |logit - oracle| = {worst:.3e}")
+    print(f"{name} L={geom.num_layers} tp={tp} ctx={max(ctx)} B={B} persist={runner.persist_ok(bucket)}: "
+          f"max |logit - oracle| = {worst:.3e}")
     return worst
 
 
+@pytest.mark.parametrize("persist", [True, False])
 @pytest.mark.parametrize("tp", [1, 8])
-def test_config2_qwen7b_shapes_8k_context(tp):
+def test_config2_qwen7b_shapes_8k_context(tp, persist):
     # ragged: 8K, a partial last page, a short context (cluster / split / balanced schedules)
-    run_long_context("qwen2.5-7b", tp, ctx=[8190, 5000, 777, 64])
+    run_long_context("qwen2.5-7b", tp, ctx=[8190, 5000, 777, 64], persist=persist)
 
 
+@pytest.mark.parametrize("persist", [True, False])
 @pytest.mark.parametrize("tp", [1, 8])
-def test_config3_llama8b_shapes_16k_context(tp):
-    run_long_context("llama3-8b", tp, ctx=[16380, 3001])
+def test_config3_llama8b_shapes_16k_context(tp, persist):
+    run_long_context("llama3-8b", tp, ctx=[16380, 3001], persist=persist)
 
 
+@pytest.mark.parametrize("persist", [True, False])
 @pytest.mark.parametrize("tp", [2, 8])
-def test_config4_qwen32b_shapes_16k_context(tp):
-    run_long_context("qwen2.5-32b", tp, ctx=[16380, 9999])
+def test_config4_qwen32b_shapes_16k_context(tp, persist):
+    run_long_context("qwen2.5-32b", tp, ctx=[16380, 9999], persist=persist)
 
 
 def test_config2_qwen7b_wide_batch_2k_context():
@@ -177,9 +184,16 @@ def test_config2_qwen7b_wide_batch_2k_context():
     run_long_context("qwen2.5-7b", 1, ctx=ctx, gen=2)
 
 
-def test_config2_qwen7b_full_depth_tp1():
+@pytest.mark.parametrize("persist", [True, False])
+def test_config2_qwen7b_full_depth_tp1(persist):
     """All 28 layers of Qwen2.5-7B (residual growth over the real depth), 2K context."""
-    run_long_context("qwen2.5-7b", 1, ctx=[2000, 1500], gen=3, layers=None, tol=0.05, noise_floor=True)
+    run_long_context("qwen2.5-7b", 1, ctx=[2000, 1500], gen=3, layers=None, tol=0.05, noise_floor=True,
+                     persist=persist)
+
+
+def test_config2_qwen7b_persist_batch16_tp4():
+    """The persistent step's two-n-tile form (9..16 rows) on ragged contexts at TP4."""
+    run_long_context("qwen2.5-7b", 4, ctx=[3000 - 170 * i for i in range(16)], gen=2, persist=True)
 
 
 @pytest.mark.parametrize("name,tp", [("qwen2.5-7b", 1), ("qwen2.5-7b", 4), ("llama3-8b", 2)])

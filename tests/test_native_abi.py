@@ -65,3 +65,30 @@ def test_sm100a_code_in_library():
     assert "LDTM" in out         # tcgen05.ld (TMEM -> registers)
     assert "sm_100a" in subprocess.run(["cuobjdump", "-lelf", nat.LIB_PATH], capture_output=True,
                                        text=True).stdout
+
+
+def test_persist_struct_binding_matches_header():
+    """The ctypes mirrors of tps_persist_geom / tps_persist_rank have the C layout."""
+    import ctypes
+    if not os.path.exists(nat.LIB_PATH):
+        pytest.skip("library not built")
+    lib = nat.load_library()
+    assert lib.tps_persist_struct_bytes(0) == ctypes.sizeof(nat.PersistGeom)
+    assert lib.tps_persist_struct_bytes(1) == ctypes.sizeof(nat.PersistRank)
+    for name, _ in nat.PersistRank._fields_:  # every field the header declares, in order
+        assert name in open(HEADER).read()
+
+
+def test_persist_shape_support_is_host_only():
+    """tps_persist_supported / tps_persist_work_bytes need no GPU."""
+    import ctypes
+    if not os.path.exists(nat.LIB_PATH):
+        pytest.skip("library not built")
+    lib = nat.load_library()
+    g = nat.PersistGeom(num_layers=28, hidden=3584, head_dim=128, n_phases=57, rms_eps=1e-6)
+    r = nat.PersistRank(nq=4, nkv=1, ffn=2368, vocab=19008, tp=8)
+    assert lib.tps_persist_supported(ctypes.byref(g), ctypes.byref(r), 1) == 1
+    assert lib.tps_persist_supported(ctypes.byref(g), ctypes.byref(r), 17) == 0   # B > 16
+    g64 = nat.PersistGeom(num_layers=2, hidden=256, head_dim=64, n_phases=5, rms_eps=1e-6)
+    assert lib.tps_persist_supported(ctypes.byref(g64), ctypes.byref(r), 1) == 0  # head_dim 64
+    assert lib.tps_persist_work_bytes(ctypes.byref(g), ctypes.byref(r), 148) > 0
