@@ -56,6 +56,20 @@ typedef struct tps_copy_item {
   uint64_t reserved;
 } tps_copy_item;
 
+/* One KV migration move: a migrating sample x a run of n_heads kv heads that
+ * are contiguous in the source and destination pools and pulled from one
+ * source rank (tpshift/reshard.py:113-151, merge-first). Pools are
+ * [L][2][num_pages][n_kv][64][D] bf16; page-table rows are int32. first_item =
+ * exclusive prefix of L * 2 * n_pages over the moves array. */
+typedef struct tps_kv_move {
+  const void* src_kv;          /* source rank's pool base (local or IPC-mapped peer) */
+  const int32_t* src_pages;    /* the sample's page-table row on the source rank */
+  const int32_t* dst_pages;    /* the sample's page-table row on this rank */
+  int32_t src_num_pages, src_nkv, src_head;
+  int32_t dst_head, n_heads, n_pages;  /* n_pages = ceil(kv tokens / 64) */
+  int64_t first_item;
+} tps_kv_move;
+
 /* ---------------------------------------------------------------- setup --- */
 /* Library/ABI version string. */
 const char* tps_version(void);
@@ -285,9 +299,23 @@ int tps_sum_partials(const float* src, int nsrc, int64_t src_stride, int64_t n, 
  * Replaces the All-Gather + Slice of tpshift/reshard.py:80-151. */
 int tps_copy_items(const tps_copy_item* items, int n, int mode, int grid, void* stream);
 
-/* Device barrier over a communication group: +1 on each peer counter, then wait
- * until *my_ctr >= target. */
-int tps_barrier(uint64_t* const* peer_ctrs, int npeers, uint64_t* my_ctr, uint64_t target, void* stream);
+/* Expand n_moves KV moves (device array) into n_items copy items (one per
+ * (layer, k|v, valid page) of each move: n_heads x chunk_bytes contiguous in
+ * both pools) written to items_out, ready for tps_copy_items. Page indices are
+ * read from the page tables on the device, so the host plans O(samples)
+ * descriptors. Out-of-range pages or head runs produce empty items and count
+ * into *bad_pages (may be NULL). Replaces plan_kv_migration's per-chunk plan
+ * (tpshift/reshard.py:113-151). */
+int tps_kv_move_items(const tps_kv_move* moves, int n_moves, int64_t n_items, void* dst_kv, int dst_num_pages,
+                      int dst_nkv, int64_t chunk_bytes, tps_copy_item* items_out, int* bad_pages, void* stream);
+
+/* Device barrier over the node's ranks (the switch's two barriers, tpshift/engine.py:
+ * 206-269): store `epoch` (monotone, one per barrier) into this rank's slot of every
+ * peer's slot array (peer_slots[i] = &peer_i_slots[self_slot]), then wait until
+ * my_slots[j] >= epoch for every j != self_slot, j < nslots. One slot per source, so a
+ * rank already at the next barrier cannot release a slower rank early. */
+int tps_barrier(uint64_t* const* peer_slots, int npeers, const uint64_t* my_slots, int nslots, int self_slot,
+                uint64_t epoch, void* stream);
 
 /* CUDA IPC for the Cache Manager's per-(tp, dp) peer tables
  * (CommGroupPool, tpshift/switchcost.py:76-104). handle: 64 bytes. */

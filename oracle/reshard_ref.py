@@ -75,3 +75,23 @@ class ByteMemory:
         data = [self.view(int(s), int(n)).copy() for s, _, n, _ in items]
         for (s, d, n, _), blob in zip(items, data):
             self.view(int(d), int(n))[:] = blob
+
+
+def expand_kv_moves(mem: "ByteMemory", moves: np.ndarray, dst_kv: int, dst_num_pages: int, dst_nkv: int,
+                    layers: int, chunk: int) -> np.ndarray:
+    """CPU restatement of tps_kv_move_items (csrc/copy.cu kv_move_items_kernel): every move
+    (KV_MOVE_DTYPE record) becomes one copy item per (layer, k|v, valid page), page indices read
+    from the page-table rows the move points at (here: in `mem`). Item order: move-major, then
+    (layer * 2 + k|v), then page -- i.e. item index = first_item + lkv * n_pages + page."""
+    out = []
+    for m in moves:
+        n_pages = int(m["n_pages"])
+        sp = mem.view(int(m["src_pages"]), 4 * n_pages).view(np.int32)
+        dp = mem.view(int(m["dst_pages"]), 4 * n_pages).view(np.int32)
+        nh, snp, snkv = int(m["n_heads"]), int(m["src_num_pages"]), int(m["src_nkv"])
+        for lkv in range(2 * layers):
+            for p in range(n_pages):
+                s = int(m["src_kv"]) + ((lkv * snp + int(sp[p])) * snkv + int(m["src_head"])) * chunk
+                d = dst_kv + ((lkv * dst_num_pages + int(dp[p])) * dst_nkv + int(m["dst_head"])) * chunk
+                out.append((s, d, nh * chunk, 0))
+    return np.asarray(out, dtype=np.int64).reshape(-1, 4)

@@ -74,7 +74,8 @@ SIGNATURES = {
     "tps_epoch_advance": (_i32, [_vp, _vp]),
     "tps_sum_partials": (_i32, [_vp, _i32, _i64, _i64, _vp, _vp]),
     "tps_copy_items": (_i32, [_vp, _i32, _i32, _i32, _vp]),
-    "tps_barrier": (_i32, [_pp, _i32, _vp, ctypes.c_uint64, _vp]),
+    "tps_kv_move_items": (_i32, [_vp, _i32, _i64, _vp, _i32, _i32, _i64, _vp, _vp, _vp]),
+    "tps_barrier": (_i32, [_pp, _i32, _vp, _i32, _i32, ctypes.c_uint64, _vp]),
     "tps_ipc_get_handle": (_i32, [_vp, _vp, ctypes.POINTER(_i64)]),
     "tps_ipc_open": (_i32, [_vp, ctypes.POINTER(_vp)]),
     "tps_ipc_close": (_i32, [_vp]),

@@ -60,6 +60,7 @@ int paged_attention(const void*, const void*, const void*, const int*, const int
                     int, int, int, int, int, float*, float*, float*, unsigned int*, void*, const Src&, const void*,
                     const float*, const float*, cudaStream_t);
 int copy_items(const void*, int, int, int, cudaStream_t);
+int kv_move_items(const void*, int, int64_t, void*, int, int, int64_t, void*, int*, cudaStream_t);
 int prefill_group_positions(int G);
 int paged_prefill_attention(const void* q, const void* k_cache, const void* v_cache, const int* row_slot,
                             const int* row_pos, const int* grp_rows, const int* grp_n, int max_groups,
@@ -83,7 +84,7 @@ int trace_register_attention(uint64_t*, unsigned int*, unsigned int);
 int trace_register_attention_bal(uint64_t*, unsigned int*, unsigned int);
 int trace_register_gemm(uint64_t*, unsigned int*, unsigned int);
 int trace_register_attention_prefill(uint64_t*, unsigned int*, unsigned int);
-int barrier(uint64_t* const*, int, uint64_t*, uint64_t, cudaStream_t);
+int barrier(uint64_t* const*, int, const uint64_t*, int, int, uint64_t, cudaStream_t);
 int ipc_get_handle(const void*, void*, int64_t*);
 int ipc_open(const void*, void**);
 int ipc_close(void*);
@@ -404,8 +405,16 @@ int tps_copy_items(const tps_copy_item* items, int n, int mode, int grid, void* 
   return copy_items(items, n, mode, grid, S(stream));
 }
 
-int tps_barrier(uint64_t* const* peer_ctrs, int npeers, uint64_t* my_ctr, uint64_t target, void* stream) {
-  return barrier(peer_ctrs, npeers, my_ctr, target, S(stream));
+int tps_kv_move_items(const tps_kv_move* moves, int n_moves, int64_t n_items, void* dst_kv, int dst_num_pages,
+                      int dst_nkv, int64_t chunk_bytes, tps_copy_item* items_out, int* bad_pages, void* stream) {
+  static_assert(sizeof(tps_kv_move) == 56, "kv move layout");
+  return kv_move_items(moves, n_moves, n_items, dst_kv, dst_num_pages, dst_nkv, chunk_bytes, items_out, bad_pages,
+                       S(stream));
+}
+
+int tps_barrier(uint64_t* const* peer_slots, int npeers, const uint64_t* my_slots, int nslots, int self_slot,
+                uint64_t epoch, void* stream) {
+  return barrier(peer_slots, npeers, my_slots, nslots, self_slot, epoch, S(stream));
 }
 
 int tps_ipc_get_handle(const void* ptr, void* handle_out, int64_t* offset_out) {

@@ -158,27 +158,99 @@ int copy_items(const void* items, int n, int mode, int grid, cudaStream_t st) {
   return kOk;
 }
 
+// ----------------------------------------------- KV-page migration items ----
+// The Switch Executor's KV plan, expanded on the device from page tables.
+// One move = one migrating sample x one run of kv heads that are contiguous in
+// both pools and come from one source rank. Its items are the (layer, k|v,
+// valid page) triples: every one is a single contiguous n_heads x 16 KB range
+// in both pool layouts [L][2][pages][n_kv][64][D] (kv head is the fastest index
+// above the page's tokens), so the host ships O(samples) descriptors instead of
+// O(samples x layers x pages) copy items (tpshift/reshard.py:113-151).
+struct KVMove {
+  const uint8_t* src_kv;
+  const int32_t* src_pages;
+  const int32_t* dst_pages;
+  int32_t src_num_pages, src_nkv, src_head;
+  int32_t dst_head, n_heads, n_pages;
+  int64_t first_item;
+};
+static_assert(sizeof(KVMove) == 56, "tps_kv_move layout");
+
+__global__ void __launch_bounds__(256) kv_move_items_kernel(const KVMove* __restrict__ moves, int n_moves,
+                                                            int64_t n_items, uint8_t* dst_kv, int dst_num_pages,
+                                                            int dst_nkv, int64_t chunk, CopyItem* __restrict__ out,
+                                                            int* bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_items;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int lo = 0, hi = n_moves - 1;  // last move with first_item <= i
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (moves[mid].first_item <= i) lo = mid; else hi = mid - 1;
+    }
+    const KVMove& m = moves[lo];
+    const int64_t j = i - m.first_item;
+    const int p = (int)(j % m.n_pages);
+    const int64_t lkv = j / m.n_pages;  // layer * 2 + (0: K, 1: V)
+    const int sp = m.src_pages[p], dp = m.dst_pages[p];
+    CopyItem it;
+    if (sp < 0 || sp >= m.src_num_pages || dp < 0 || dp >= dst_num_pages || m.src_head + m.n_heads > m.src_nkv ||
+        m.dst_head + m.n_heads > dst_nkv) {
+      if (bad) atomicAdd(bad, 1);
+      it.src = nullptr; it.dst = nullptr; it.bytes = 0; it.reserved = 0;  // copies nothing
+    } else {
+      it.src = m.src_kv + ((lkv * m.src_num_pages + sp) * m.src_nkv + m.src_head) * chunk;
+      it.dst = dst_kv + ((lkv * dst_num_pages + dp) * dst_nkv + m.dst_head) * chunk;
+      it.bytes = (uint64_t)m.n_heads * chunk;
+      it.reserved = 0;
+    }
+    out[i] = it;
+  }
+}
+
+int kv_move_items(const void* moves, int n_moves, int64_t n_items, void* dst_kv, int dst_num_pages, int dst_nkv,
+                  int64_t chunk_bytes, void* items_out, int* bad, cudaStream_t st) {
+  TPS_CHECK_ARG(n_moves >= 0 && n_items >= 0 && chunk_bytes > 0 && (chunk_bytes & 15) == 0,
+                "kv_move_items: bad sizes");
+  if (n_items == 0) return kOk;
+  TPS_CHECK_ARG(moves && dst_kv && items_out && n_moves > 0, "kv_move_items: null argument");
+  int64_t blocks = (n_items + 255) / 256;
+  if (blocks > 8 * kNumSMs) blocks = 8 * kNumSMs;
+  kv_move_items_kernel<<<(int)blocks, 256, 0, st>>>(reinterpret_cast<const KVMove*>(moves), n_moves, n_items,
+                                                     reinterpret_cast<uint8_t*>(dst_kv), dst_num_pages, dst_nkv,
+                                                     chunk_bytes, reinterpret_cast<CopyItem*>(items_out), bad);
+  TPS_LAUNCH_CHECK();
+  return kOk;
+}
+
 // ------------------------------------------------------ device barrier ----
-// Every rank adds 1 to each peer's counter, then waits for its own counter to
-// reach target (= epoch * (nranks - 1) for a full barrier). Stream ordered.
+// Epoch barrier with one slot per source rank: rank q stores the barrier's epoch
+// into slot q of every peer's slot array, then waits until every peer's slot in its
+// own array holds >= epoch. (A shared counter that every peer increments is not a
+// barrier once ranks may run ahead: a rank that already passed barrier k and
+// arrives at k+1 would add to a counter a slower rank is still checking for k, and
+// let it through before the last rank arrived. Epoch slots cannot be over-counted.)
 constexpr int kMaxPeerArgs = 16;
 struct PeerPtrs {
   uint64_t* p[kMaxPeerArgs];
 };
 
-__global__ void barrier_kernel_v(PeerPtrs peers, int npeers, uint64_t* my_ctr, uint64_t target) {
+__global__ void barrier_kernel_v(PeerPtrs peers, int npeers, const uint64_t* my_slots, int nslots, int self_slot,
+                                 uint64_t epoch) {
   if (threadIdx.x != 0) return;
-  __threadfence_system();
-  for (int i = 0; i < npeers; ++i) red_relaxed_sys_add(peers.p[i], 1ull);
-  wait_counter_geq(my_ctr, target);
+  __threadfence_system();  // everything this stream wrote before the barrier is visible first
+  for (int i = 0; i < npeers; ++i) st_relaxed_sys_u64(peers.p[i], epoch);
+  for (int j = 0; j < nslots; ++j)
+    if (j != self_slot) wait_counter_geq(my_slots + j, epoch);
   __threadfence_system();
 }
 
-int barrier(uint64_t* const* peer_ctrs, int npeers, uint64_t* my_ctr, uint64_t target, cudaStream_t st) {
-  TPS_CHECK_ARG(npeers >= 0 && npeers <= kMaxPeerArgs && my_ctr, "barrier: bad args");
+int barrier(uint64_t* const* peer_slots, int npeers, const uint64_t* my_slots, int nslots, int self_slot,
+            uint64_t epoch, cudaStream_t st) {
+  TPS_CHECK_ARG(npeers >= 0 && npeers <= kMaxPeerArgs && my_slots && nslots >= 0 && nslots <= kMaxPeerArgs + 1,
+                "barrier: bad args");
   PeerPtrs pp{};
-  for (int i = 0; i < npeers; ++i) pp.p[i] = peer_ctrs[i];
-  barrier_kernel_v<<<1, 32, 0, st>>>(pp, npeers, my_ctr, target);
+  for (int i = 0; i < npeers; ++i) pp.p[i] = peer_slots[i];
+  barrier_kernel_v<<<1, 32, 0, st>>>(pp, npeers, my_slots, nslots, self_slot, epoch);
   TPS_LAUNCH_CHECK();
   return kOk;
 }

@@ -139,7 +139,7 @@ def c_float(x: float):
 
 
 def switch_probe(spec, geom, world, tp_to: int, n_samples: int, ctx: int, copy_mode: int = 0,
-                 reps: int = 1) -> dict:
+                 reps: int = 1, alias_replicas: bool = False, use_graphs: bool = True) -> dict:
     """Switch Executor microbench (BASELINE config 5): one real switch of a running decode.
 
     Builds the layout (spec.initial_tp, world), places `n_samples` live samples at
@@ -156,7 +156,9 @@ def switch_probe(spec, geom, world, tp_to: int, n_samples: int, ctx: int, copy_m
 
     out = []
     for _ in range(reps):
-        be = B200Backend(spec, geom, world, seed=0)
+        be = B200Backend(spec, geom, world, seed=0, alias_replicas=alias_replicas, use_graphs=use_graphs)
+        be.capture_all(every_layout=True)   # what GlobalCoordinator does before a stage
+        be.prepare_switch_items()
         lay = be.layout
         samples = {g: [] for g in range(lay.dp)}
         prompt = torch.zeros(spec.prompt_len, dtype=torch.int32)
@@ -186,12 +188,17 @@ def switch_probe(spec, geom, world, tp_to: int, n_samples: int, ctx: int, copy_m
         # runs every rank's pulls on the one device)
         kms = sum(e0.elapsed_time(e1) for e0, _, e1 in be.copy_events)
         kbytes = sum(nb for _, nb, _ in be.copy_events)
-        marks = t.marks
+        marks = t.marks  # per rank: arrive, released, weights done, KV done, resumed
         t0 = min(be.start[r].elapsed_time(m[0]) for r, m in marks.items())
-        t_end = max(be.start[r].elapsed_time(m[3]) for r, m in marks.items())
+        t_rel = min(be.start[r].elapsed_time(m[1]) for r, m in marks.items())
+        t_end = max(be.start[r].elapsed_time(m[4]) for r, m in marks.items())
+        peer = max((v["nvlink"] for v in t.per_rank.values()), default=0)
+        local = max((v["local"] for v in t.per_rank.values()), default=0)
         out.append({"weights_bytes": t.weight_bytes, "kv_bytes": t.kv_bytes, "nvlink_bytes": t.nvlink_bytes,
-                    "local_bytes": t.local_bytes, "copy_bytes": kbytes, "copy_kernel_ms": kms,
+                    "local_bytes": t.local_bytes, "max_gpu_peer_bytes": peer, "max_gpu_local_bytes": local,
+                    "copy_bytes": kbytes, "copy_kernel_ms": kms,
                     "copy_gbps": kbytes / (kms / 1e3) / 1e9, "switch_device_ms": t_end - t0,
+                    "release_to_resume_ms": t_end - t_rel, "host_switch_s": t.host_s,
                     "host_plan_s": t.host_plan_s, "host_capture_s": t.host_capture_s,
                     "host_build_s": t.host_build_s, "copy_launches": len(be.copy_events)})
         del be

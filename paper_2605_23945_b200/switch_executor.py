@@ -242,6 +242,122 @@ def plan_kv_pulls(geom: DecoderGeometry, old: Layout, new: Layout, dst_rank: int
     return pieces
 
 
+# One KV move (tps_kv_move, include/tpshift_b200.h): a migrating sample x a run of kv heads that
+# is contiguous in both pools and comes from one source rank; the device expands it into one copy
+# item per (layer, k|v, valid page) reading the page tables (tps_kv_move_items).
+KV_MOVE_DTYPE = np.dtype([("src_kv", "<u8"), ("src_pages", "<u8"), ("dst_pages", "<u8"),
+                          ("src_num_pages", "<i4"), ("src_nkv", "<i4"), ("src_head", "<i4"),
+                          ("dst_head", "<i4"), ("n_heads", "<i4"), ("n_pages", "<i4"), ("first_item", "<i8")])
+assert KV_MOVE_DTYPE.itemsize == 56
+
+# columns of a planned move (plan_kv_moves)
+MV_SRC, MV_SSLOT, MV_SHEAD, MV_DSLOT, MV_DHEAD, MV_NHEADS, MV_NPAGES = range(7)
+
+_HEAD_RUNS: dict = {}
+
+
+def _head_runs(geom: DecoderGeometry, old: Layout, new: Layout, dst_rank: int, old_group: int) -> list[tuple]:
+    """[(src_rank, src_head, dst_head, n_heads)] for the kv heads dst_rank owns under `new`, pulled
+    from old group `old_group`: per head the same source choice as plan_kv_pulls (_pick_source,
+    salt = head), consecutive heads merged while contiguous in both pools and from one rank."""
+    key = (geom.name, geom.num_layers, old, new, dst_rank, old_group)
+    runs = _HEAD_RUNS.get(key)
+    if runs is None:
+        new_sh = rank_shard(geom, new.tp, new.tp_rank(dst_rank))
+        old_shards = [rank_shard(geom, old.tp, r) for r in range(old.tp)]
+        runs = []
+        for h in range(*new_sh.kv_heads):
+            holders = [old_group * old.tp + r for r in range(old.tp)
+                       if old_shards[r].kv_heads[0] <= h < old_shards[r].kv_heads[1]]
+            src = _pick_source(holders, dst_rank, h)
+            sh_ = h - old_shards[old.tp_rank(src)].kv_heads[0]
+            dh_ = h - new_sh.kv_heads[0]
+            if runs and runs[-1][0] == src and runs[-1][1] + runs[-1][3] == sh_ and runs[-1][2] + runs[-1][3] == dh_:
+                runs[-1] = (src, runs[-1][1], runs[-1][2], runs[-1][3] + 1)
+            else:
+                runs.append((src, sh_, dh_, 1))
+        _HEAD_RUNS[key] = runs
+    return runs
+
+
+def plan_kv_moves(geom: DecoderGeometry, old: Layout, new: Layout, dst_rank: int, old_groups, old_slots,
+                  new_slots, kv_lens) -> np.ndarray:
+    """KV moves of the samples placed on dst_rank's new group: int64 [n, 7] rows
+    (src_rank, src_slot, src_head, dst_slot, dst_head, n_heads, n_pages).
+
+    Covers exactly the chunks plan_kv_pulls lists (same sources; head runs merged), but
+    as O(samples) rows: pages are resolved on the device from both ranks' page tables."""
+    rows = []
+    for og, os_, ns, n in zip(old_groups, old_slots, new_slots, kv_lens):
+        npg = pages_for(int(n))
+        if npg == 0:
+            continue
+        for src, sh_, dh_, nh in _head_runs(geom, old, new, dst_rank, int(og)):
+            rows.append((src, int(os_), sh_, int(ns), dh_, nh, npg))
+    return np.asarray(rows, dtype=np.int64).reshape(-1, 7)
+
+
+def kv_move_bytes(geom: DecoderGeometry, moves: np.ndarray, dst_rank: int) -> tuple[int, int]:
+    """(bytes pulled from peers, bytes copied locally) of planned KV moves."""
+    if moves.size == 0:
+        return 0, 0
+    chunk = PAGE * geom.head_dim * 2
+    nb = 2 * geom.num_layers * moves[:, MV_NPAGES] * moves[:, MV_NHEADS] * chunk
+    remote = int(nb[moves[:, MV_SRC] != dst_rank].sum())
+    return remote, int(nb.sum()) - remote
+
+
+def pack_kv_moves(geom: DecoderGeometry, moves: np.ndarray, src: dict[int, dict], dst_pt: int,
+                  pt_row_bytes: int) -> tuple[np.ndarray, int]:
+    """Device descriptors (KV_MOVE_DTYPE) of planned moves and their total item count.
+    src[rank] = {"kv": pool base, "pt": page-table base, "np": pages, "nkv": local kv heads}
+    (pointers valid in this process); dst_pt = this rank's page-table base."""
+    out = np.zeros(len(moves), dtype=KV_MOVE_DTYPE)
+    if len(moves) == 0:
+        return out, 0
+    ranks = moves[:, MV_SRC]
+    uniq = np.unique(ranks)
+    kv = np.zeros(int(uniq.max()) + 1, dtype=np.uint64)
+    pt = np.zeros_like(kv)
+    npg = np.zeros(int(uniq.max()) + 1, dtype=np.int64)
+    nkv = np.zeros_like(npg)
+    for r in uniq:
+        e = src[int(r)]
+        kv[r], pt[r], npg[r], nkv[r] = e["kv"], e["pt"], e["np"], e["nkv"]
+    out["src_kv"] = kv[ranks]
+    out["src_pages"] = pt[ranks] + (moves[:, MV_SSLOT] * pt_row_bytes).astype(np.uint64)
+    out["dst_pages"] = np.uint64(dst_pt) + (moves[:, MV_DSLOT] * pt_row_bytes).astype(np.uint64)
+    out["src_num_pages"] = npg[ranks]
+    out["src_nkv"] = nkv[ranks]
+    out["src_head"] = moves[:, MV_SHEAD]
+    out["dst_head"] = moves[:, MV_DHEAD]
+    out["n_heads"] = moves[:, MV_NHEADS]
+    out["n_pages"] = moves[:, MV_NPAGES]
+    per = 2 * geom.num_layers * moves[:, MV_NPAGES]
+    first = np.cumsum(per) - per
+    out["first_item"] = first
+    return out, int(per.sum())
+
+
+def verify_kv_moves(moves: np.ndarray, n_kv_local: int, slots: int) -> list[str]:
+    """Every (target slot, kv head) written at most once; runs inside the target's heads/slots."""
+    if moves.size == 0:
+        return []
+    issues = []
+    if np.any(moves[:, MV_NHEADS] <= 0) or np.any(moves[:, MV_NPAGES] <= 0):
+        issues.append("empty kv move")
+    if np.any(moves[:, MV_DHEAD] < 0) or np.any(moves[:, MV_DHEAD] + moves[:, MV_NHEADS] > n_kv_local):
+        issues.append("kv move outside the target's kv heads")
+    if np.any(moves[:, MV_DSLOT] < 0) or np.any(moves[:, MV_DSLOT] >= slots):
+        issues.append("kv move outside the target's slots")
+    heads = np.repeat(moves[:, MV_DSLOT] * n_kv_local + moves[:, MV_DHEAD], moves[:, MV_NHEADS])
+    first = np.repeat(np.cumsum(moves[:, MV_NHEADS]) - moves[:, MV_NHEADS], moves[:, MV_NHEADS])
+    heads = heads + (np.arange(heads.size) - first)
+    if np.unique(heads).size != heads.size:
+        issues.append("a (slot, kv head) is written twice")
+    return issues
+
+
 def plan_history_pulls(old: Layout, dst_rank: int, sources: list[KVSource], targets: list[KVTarget],
                        lens: list[int], old_hist_ld: int, new_hist_ld: int) -> Pieces:
     """Token-history rows (prompt + generated so far) of the migrating samples."""

@@ -209,14 +209,17 @@ def test_copy_items_bit_exact(mode):
     assert torch.equal(dst, want)
 
 
-def test_barrier_counters_virtual():
-    ctr = torch.zeros(4, dtype=torch.int64, device="cuda")
-    peers = nat.ptr_array([ctr.data_ptr() + 8 * i for i in range(1, 4)])
-    # this "rank" signals three peers and waits on its own counter, which we pre-arm
-    ctr[0] = 1
-    nat.check(nat.lib().tps_barrier(peers, 3, ctr.data_ptr(), 1, _stream()))
-    torch.cuda.synchronize()
-    assert ctr.tolist() == [1, 1, 1, 1]
+def test_barrier_epoch_slots_virtual():
+    """Rank 0 of 4: stores the epoch into its slot of the three peers' arrays and waits on the
+    three peer slots of its own array (pre-armed here as if the peers had arrived)."""
+    mine = torch.zeros(4, dtype=torch.int64, device="cuda")
+    peer_arrays = torch.zeros((3, 4), dtype=torch.int64, device="cuda")
+    peers = nat.ptr_array([peer_arrays[i].data_ptr() for i in range(3)])  # slot 0 = this rank's
+    for epoch in (1, 2, 5):
+        mine[1:] = epoch
+        nat.check(nat.lib().tps_barrier(peers, 3, mine.data_ptr(), 4, 0, epoch, _stream()))
+        torch.cuda.synchronize()
+        assert peer_arrays[:, 0].tolist() == [epoch] * 3 and peer_arrays[:, 1:].sum() == 0
 
 
 @pytest.mark.parametrize("F,k,b", [(1024, 256, 1), (2368, 3584, 16), (18944, 3584, 64), (512, 512, 300)])

@@ -199,3 +199,77 @@ def test_weight_plan_entry_coverage_check():
         pad.add(sr, so, do, nb)
         pad.add(np.array([0]), np.array([0]), np.array([off + 2 * int(np.prod(shape))]), np.array([2]))
         assert verify_entries(pad, lay)
+
+
+def test_kv_moves_match_the_chunk_plan_and_migrate_bit_exact():
+    """The O(samples) KV moves (expanded from page tables, as tps_kv_move_items does on the
+    device) copy exactly the chunks plan_kv_pulls lists, and the migrated pages are bit-exact."""
+    from oracle.reshard_ref import expand_kv_moves
+    from paper_2605_23945_b200.switch_executor import (kv_move_bytes, pack_kv_moves, plan_kv_moves,
+                                                       verify_kv_moves)
+    geom = GEOS["mini-qwen"]
+    world, L, D = 8, geom.num_layers, geom.head_dim
+    chunk = 64 * D * 2
+    rng = np.random.default_rng(1)
+    for t_old, t_new in [(1, 2), (1, 8), (2, 8), (4, 2), (2, 4), (8, 1), (4, 8)]:
+        old, new = Layout(t_old, world), Layout(t_new, world)
+        n_samples, P, npg_old, npg_new = 6, 8, 64, 80
+        ctx = [int(x) for x in rng.integers(1, 400, n_samples)]
+        old_group = [int(x) for x in rng.integers(0, old.dp, n_samples)]
+        old_slot = [2 + i for i in range(n_samples)]
+        mem = ByteMemory()
+        src = {}
+        perm = rng.permutation(npg_old)
+        for r in range(world):
+            sh = rank_shard(geom, t_old, r % t_old)
+            base = mem.alloc(L * 2 * npg_old * sh.n_kv * chunk)
+            mem.view(base, L * 2 * npg_old * sh.n_kv * chunk)[:] = rng.integers(0, 256, L * 2 * npg_old * sh.n_kv * chunk,
+                                                                                 dtype=np.uint8)
+            pt = mem.alloc(16 * P * 4)
+            for i in range(n_samples):
+                mem.view(pt + 4 * P * old_slot[i], 4 * P)[:] = perm[i * P:(i + 1) * P].astype(np.int32).view(np.uint8)
+            src[r] = {"kv": base, "pt": pt, "np": npg_old, "nkv": sh.n_kv}
+        placement = {g: [i for i in range(n_samples) if i % new.dp == g] for g in range(new.dp)}
+        for dst in range(world):
+            mine = placement[new.group_of(dst)]
+            sh = rank_shard(geom, t_new, dst % t_new)
+            new_slot = [5 + j for j in range(len(mine))]
+            pt_new = mem.alloc(16 * P * 4)
+            tgt_pages = {}
+            dperm = rng.permutation(npg_new).astype(np.int32)  # disjoint page sets per sample
+            for j, i in enumerate(mine):
+                pages = dperm[j * P:(j + 1) * P]
+                tgt_pages[i] = pages
+                mem.view(pt_new + 4 * P * new_slot[j], 4 * P)[:] = pages.view(np.uint8)
+            moves = plan_kv_moves(geom, old, new, dst, [old_group[i] for i in mine], [old_slot[i] for i in mine],
+                                  new_slot, [ctx[i] for i in mine])
+            assert verify_kv_moves(moves, sh.n_kv, 16) == []
+            packed, n_items = pack_kv_moves(geom, moves, src, pt_new, 4 * P)
+            pool = mem.alloc(L * 2 * npg_new * sh.n_kv * chunk)
+            items = expand_kv_moves(mem, packed, pool, npg_new, sh.n_kv, L, chunk)
+            assert len(items) == n_items
+            # same bytes, same sources as the per-chunk plan
+            srcs = [KVSource(old_group=old_group[i], slot=old_slot[i], pages=tuple(int(p) for p in perm[i * P:(i + 1) * P]))
+                    for i in mine]
+            tgts = [KVTarget(slot=new_slot[j], pages=tuple(int(p) for p in tgt_pages[i])) for j, i in enumerate(mine)]
+            kp = plan_kv_pulls(geom, old, new, dst, srcs, tgts, [ctx[i] for i in mine], npg_old, npg_new)
+            ref = to_items(kp, {r: src[r]["kv"] for r in src}, pool)
+            split = []
+            for s, d, n, _ in items:
+                for k in range(n // chunk):
+                    split.append((s + k * chunk, d + k * chunk, chunk, 0))
+            assert sorted(map(tuple, ref.tolist())) == sorted(split)
+            assert sum(kv_move_bytes(geom, moves, dst)) == int(ref[:, 2].sum()) if len(ref) else True
+            assert kv_move_bytes(geom, moves, dst) == nvlink_bytes(kp, dst)
+            mem.execute(items)
+            for s, d, n, _ in ref:
+                assert np.array_equal(mem.view(int(s), int(n)), mem.view(int(d), int(n)))
+
+
+def test_kv_move_plan_rejects_double_writes():
+    from paper_2605_23945_b200.switch_executor import verify_kv_moves
+    ok = np.array([[0, 1, 0, 3, 0, 2, 4], [1, 2, 0, 4, 0, 2, 4]], dtype=np.int64)
+    assert verify_kv_moves(ok, 2, 8) == []
+    dup = np.array([[0, 1, 0, 3, 0, 2, 4], [1, 2, 1, 3, 1, 1, 4]], dtype=np.int64)
+    assert verify_kv_moves(dup, 2, 8)
+    assert verify_kv_moves(np.array([[0, 1, 0, 9, 0, 1, 4]], dtype=np.int64), 2, 8)
