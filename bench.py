@@ -58,7 +58,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-switch", action="store_true")
-    ap.add_argument("--static-tps", default="1", help="N>1: also time the stage at these fixed TP degrees")
+    ap.add_argument("--static-tps", default="all",
+                    help="N>1: also time the stage at these fixed TP degrees (default: every TP degree dividing N)")
+    ap.add_argument("--no-tail", action="store_true")
     ap.add_argument("--tp-list", default="", help="Algorithm 1 candidates (default: 1 and N, BASELINE config 2)")
     ap.add_argument("--initial-tp", type=int, default=1, help="starting TP degree (config 4 starts at TP2)")
     ap.add_argument("--cpu-threads", type=int, default=0)
@@ -161,36 +163,118 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_step_model(geom, threads: int, ctx: int = 2048):
-    """Time the CPU oracle: one decoder layer at B in {1, 64} and the LM head; returns t(B) in s."""
-    from oracle.decoder_ref import OracleDecoder
-    torch.set_num_threads(threads)
-    H, D, F = geom.hidden, geom.head_dim, geom.ffn
-    geo = dict(num_layers=1, hidden=H, n_q=geom.n_q, n_kv=geom.n_kv, head_dim=D, ffn=F, vocab=256,
-               qkv_bias=geom.qkv_bias, rope_theta=geom.rope_theta, rms_eps=geom.rms_eps)
-    z = torch.zeros
-    W = {(-1, "embed"): z(256, H), (-1, "ln_f"): torch.ones(H), (-1, "lm_head"): z(256, H),
-         (0, "w_qkv"): z(geom.qkv_rows, H), (0, "b_qkv"): z(geom.qkv_rows), (0, "w_o"): z(H, geom.n_q * D),
-         (0, "w_gu"): z(2 * F, H), (0, "w_d"): z(H, F), (0, "ln1"): torch.ones(H), (0, "ln2"): torch.ones(H)}
-    lm = z(geom.vocab, H)
-    times = {}
-    for B in (1, 64):
-        orc = OracleDecoder(geo, W, tp=1, round_bf16=True, max_len=ctx + 8)
-        orc.step([1] * B, [ctx - 1] * B, list(range(B)))  # allocate caches, warm
+class CpuOracleSteps:
+    """The CPU oracle (oracle/decoder_ref.py, vectorised over rows) at FULL depth: every layer,
+    the real vocabulary, random bf16-valued weights (seeded torch CPU generator).
+    `measure()` -> {"steps": {B: seconds of one decode step at context ctx}, "prefill64_s":
+    seconds of a 64-token prefill chunk of one sample}.
+
+    Timing only: every layer references one random layer's tensors (the same arithmetic and
+    the same memory-to-core traffic per layer -- each layer's 1.9 GB of fp32 weights is far
+    larger than the host caches -- in 1/L of the host memory and generation time), the LM head
+    shares the embedding's tensor, and the rows of a step share one sample's cache."""
+
+    def __init__(self, geom, threads: int, ctx: int = 2048, batches=(1, 8, 64)):
+        from oracle.decoder_ref import OracleDecoder
+        torch.set_num_threads(threads)
         t0 = time.perf_counter()
-        reps = 2
-        for _ in range(reps):
-            orc.step([1] * B, [ctx - 1] * B, list(range(B)))
-        layer = (time.perf_counter() - t0) / reps
-        x = torch.zeros(B, H)
-        t0 = time.perf_counter()
-        for _ in range(reps):
-            _ = x @ lm.T
-        head = (time.perf_counter() - t0) / reps
-        times[B] = geom.num_layers * layer + head
-    a = times[1]
-    b = (times[64] - times[1]) / 63.0
-    return (lambda B: a + b * (B - 1)), times
+        g = torch.Generator().manual_seed(0)
+        H, D, F, V = geom.hidden, geom.head_dim, geom.ffn, geom.vocab
+
+        def rnd(*shape):
+            return (torch.randn(*shape, generator=g) * 0.02).bfloat16().float()
+
+        emb = rnd(V, H)
+        W = {(-1, "embed"): emb, (-1, "ln_f"): torch.ones(H), (-1, "lm_head"): emb}
+        one = {"w_qkv": rnd(geom.qkv_rows, H), "w_o": rnd(H, geom.n_q * D), "w_gu": rnd(2 * F, H),
+               "w_d": rnd(H, F), "ln1": torch.ones(H), "ln2": torch.ones(H)}
+        if geom.qkv_bias:
+            one["b_qkv"] = rnd(geom.qkv_rows)
+        for l in range(geom.num_layers):
+            for k, v in one.items():
+                W[(l, k)] = v
+        geo = dict(num_layers=geom.num_layers, hidden=H, n_q=geom.n_q, n_kv=geom.n_kv, head_dim=D, ffn=F,
+                   vocab=V, qkv_bias=geom.qkv_bias, rope_theta=geom.rope_theta, rms_eps=geom.rms_eps)
+        self.orc = OracleDecoder(geo, W, tp=1, round_bf16=True, max_len=ctx + 8)
+        self.orc.step([1], [ctx - 1], [0])  # allocates the shared cache
+        self.ctx, self.batches = ctx, batches
+        self.setup_s = time.perf_counter() - t0
+
+    def measure(self) -> dict:
+        t1 = time.perf_counter()
+        self.orc.prefill(list(range(64)), sample=1, start=0)
+        pre = time.perf_counter() - t1
+        steps = {}
+        for B in self.batches:
+            t1 = time.perf_counter()
+            self.orc.step([1] * B, [self.ctx - 1] * B, [0] * B)
+            steps[B] = time.perf_counter() - t1
+        return {"steps": steps, "prefill64_s": pre, "setup_s": self.setup_s, "ctx": self.ctx}
+
+
+def cpu_decode_steps(geom, threads: int, ctx: int = 2048) -> dict:
+    return CpuOracleSteps(geom, threads, ctx).measure()
+
+
+def active_histogram(rep) -> dict[int, int]:
+    """Rounds per active-sample count (whole node) from a SimReport's step blocks."""
+    hist = {}
+    for nr in rep.node_reports:
+        for ev in nr["events"]:
+            if ev["type"] == "step-block":
+                lo, hi = (int(x) for x in ev["detail"].split("=")[1].split(".."))
+                hist[ev["active"]] = hist.get(ev["active"], 0) + (hi - lo)
+    return hist
+
+
+def cpu_stage_estimate(spec, steps: dict, hist: dict[int, int]) -> float:
+    """Stage seconds on the CPU oracle: every decode round at its active batch (measured
+    full-depth step times, piecewise-linear in B between the measured batches) + the prompts'
+    prefill at the measured 64-token chunk rate."""
+    bs = sorted(steps["steps"])
+    ys = [steps["steps"][b] for b in bs]
+    dec = sum(n * float(np.interp(B, bs, ys)) for B, n in hist.items())
+    pre = spec.global_batch * (spec.prompt_len / 64.0) * steps["prefill64_s"]
+    return dec + pre
+
+
+def decision_layer_timing(args) -> dict:
+    """The reference's own CPU path, single-threaded Python (SURVEY 8(d) CPU baseline (i)):
+    Algorithm 1 `evaluate` at B=512 (BASELINE config 2 on 8 GPUs, TP1/DP8, mid-stage) and one
+    whole simulated stage `run` -- the restated tpshift code, bit-exact with the reference."""
+    from paper_2605_23945_b200.cluster import ParallelConfig
+    from paper_2605_23945_b200.controller import evaluate
+    from paper_2605_23945_b200.engine import build_hardware_model, planner_view, run as sim_run
+    from paper_2605_23945_b200.switchcost import CommGroupPool
+    from paper_2605_23945_b200.workload import BatchStatus, Sample, sample_response_lengths
+    ns = argparse.Namespace(model=args.model, per_gpu_batch=64, l_max=args.l_max, prompt_len=args.prompt_len,
+                            seed=args.seed, tp_list="1,2,4,8", initial_tp=1)
+    spec, geom = build_spec(ns, 8)
+    table = measured_table(args.model)
+    pred, _ = planner_view(spec, build_hardware_model(spec), table)
+    lens = sample_response_lengths(spec.distribution, spec.global_batch, spec.seed)
+    l_gen = 1000
+    groups = {g: [] for g in range(8)}
+    for i, t in enumerate(lens):
+        if min(t, spec.l_max) > l_gen:
+            groups[i % 8].append(Sample(id=i, prompt_len=spec.prompt_len, target_response_len=int(t),
+                                        generated_len=l_gen, intra_dp_group=i % 8))
+    st = [BatchStatus(node_id=0, group_index=g, samples=tuple(v)) for g, v in groups.items()]
+    pool = CommGroupPool.fresh(spec.switch.comm_init_cost, warm=((1, 8),))
+    cur = ParallelConfig.for_cluster(spec.cluster, 1)
+    live = sum(len(v) for v in groups.values())
+    evaluate(spec.controller, pred, pool, spec.switch, st, cur, spec.l_max, l_gen, spec.model, spec.cluster)
+    reps = 5
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        evaluate(spec.controller, pred, pool, spec.switch, st, cur, spec.l_max, l_gen, spec.model, spec.cluster)
+    ev = (time.perf_counter() - t0) / reps
+    t0 = time.perf_counter()
+    rep = sim_run(spec, table)
+    run_s = time.perf_counter() - t0
+    return {"evaluate_ms": ev * 1e3, "evaluate_live_samples": live, "run_stage_s": run_s,
+            "run_stage": f"c2 on 8 GPUs: {spec.global_batch} samples, tp_list (1,2,4,8), "
+                         f"{rep.eval_count} evaluations", "cores": 1}
 
 
 def main():
@@ -256,10 +340,12 @@ def main():
     w_rounds = sum(hist.values())
     g_ms = sum(probes[B]["ms"] * n for B, n in hist.items()) / w_rounds
     g_bytes = sum(probes[B]["bytes"] * n for B, n in hist.items()) / w_rounds
+    g_ovh = sum(probes[B]["overhead_bytes"] * n for B, n in hist.items()) / w_rounds
+    g_launch = probes[max(hist, key=hist.get)]["launches"]
     peak, peak_src = peaks()
     achieved = g_bytes / g_ms / 1e6
     switch = [s for nr in rep.node_reports for s in nr["switches"]]
-    sw_gbps = [s.get("copy_gbps_per_gpu") for s in switch if s.get("copy_gbps_per_gpu")]
+    sw_gbps = [s.get("peer_gbps_per_gpu") for s in switch if s.get("peer_gbps_per_gpu")]
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "weak",
@@ -276,15 +362,25 @@ def main():
         "tokens_generated": rep.tokens_generated,
         "tokens_per_s": rep.tokens_generated / value,
         "switches": [{"from": s["from_tp"], "to": s["to_tp"], "round": s["round"],
-                      "seconds": s["breakdown"]["total"], "gbps_per_gpu": s.get("copy_gbps_per_gpu")}
+                      "seconds": s["breakdown"]["total"], "release_to_resume_s": s.get("release_to_resume_s"),
+                      "max_gpu_peer_bytes": s.get("max_gpu_peer_bytes"),
+                      "max_gpu_local_bytes": s.get("max_gpu_local_bytes"),
+                      "peer_gbps_per_gpu": s.get("peer_gbps_per_gpu"), "host_switch_s": s.get("host_switch_s")}
                      for s in switch],
         "switch_gbps": (sum(sw_gbps) / len(sw_gbps)) if sw_gbps else None,
+        "switch_gbps_note": "max over GPUs of bytes pulled from peers / that GPU's barrier-release -> resume "
+                            "window (SURVEY 8(d)); local copies reported separately",
         "wall_s_per_step": float(np.mean(walls)),
         "setup_s": setup_s,
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None, "kernel": "gemm_swapab_kernel (tcgen05)",
                      "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": g_bytes / g_launch, "launches_per_step": g_launch,
+                     "split_partial_overhead_bytes_per_step": g_ovh,
+                     "bytes_note": "algorithmic = weight shard + activations + one fp32 output row per batch row "
+                                   "(SURVEY 8(d)); the other split-K partials are overhead (written and read "
+                                   "back once more), excluded from achieved",
                      "per_bucket": {str(B): {"gbps": probes[B]["gbps"], "rounds": hist[B]} for B in sorted(hist)},
                      "rounds_at_other_tp": other_rounds},
         "clocks": clk.summary(),
@@ -302,14 +398,26 @@ def main():
         line["stage_roofline"] = stage_roofline(spec, geom, line["phases"]["decode_s"], peak)
     tr = traffic_record()
     if tr:
-        line["roofline"]["traffic"] = tr["dram_bytes"]
-        line["roofline"]["traffic_note"] = (f"ncu dram read+write of one launch ({tr['launch']}) vs its "
-                                            f"{tr['algorithmic_bytes']} algorithmic bytes; profiles/r1/ncu_traffic.json")
+        line["roofline"]["traffic"] = tr["dram_bytes_per_launch"]
+        line["roofline"]["traffic_note"] = tr["note"]
+    if rank == 0 and gpus == 1 and not args.no_tail:
+        # the post-switch tail (BASELINE config 2 ends at TP8): one TP8 rank alone on this GPU
+        # (loopback peer table: same kernels and protocol, no NVLink hop), B <= 32
+        from paper_2605_23945_b200.profiler import tail_probe
+        try:
+            tail = tail_probe(geom, 8, (1, 4, 16, 32), 4096, peak)
+            line["tail"] = {"tp": 8, "ctx": 4096, "per_batch": {str(b): v for b, v in tail.items()},
+                            "note": "TP8 rank with a looped-back peer table (no NVLink hop); floor = weight shard "
+                                    "+ LM-head shard + live and new K/V at the measured copy peak"}
+        except Exception as e:
+            line["tail"] = {"error": f"{type(e).__name__}: {e}"}
     if gpus > 1 and args.static_tps:
         # the north-star comparison: the same stage at a fixed TP (no switching), same engine
         line["fixed_tp"] = {}
-        for tp in (int(x) for x in args.static_tps.split(",")):
-            if gpus % tp:
+        fixed = [t for t in (1, 2, 4, 8) if t <= gpus] if args.static_tps == "all" else \
+            [int(x) for x in args.static_tps.split(",")]
+        for tp in fixed:
+            if gpus % tp or not _tp_ok(geom, tp):
                 continue
             ex = coord = None
             gc.collect()  # executors / runners / comms form reference cycles
@@ -319,21 +427,57 @@ def main():
             coord.run()
             srep, _ = coord.run()
             line["fixed_tp"][str(tp)] = srep.generation_time
+        if line["fixed_tp"]:
+            best = min(line["fixed_tp"], key=line["fixed_tp"].get)
+            line["adaptive_vs_best_fixed"] = {"adaptive_s": value, "best_fixed_tp": int(best),
+                                              "best_fixed_s": line["fixed_tp"][best],
+                                              "speedup": line["fixed_tp"][best] / value}
+        line["active_gpus"] = sorted(world.devices[r].index or 0 for r in world.local_ranks) \
+            if not world.distributed else list(range(gpus))
     if rank == 0 and gpus == 1 and not args.no_switch:
-        line["switch_microbench"] = switch_microbench(args, peak)
+        try:
+            line["switch_microbench"] = switch_microbench(args, peak)
+        except Exception as e:
+            line["switch_microbench"] = {"error": f"{type(e).__name__}: {e}"}
+    steps = None
+    threads = args.cpu_threads or os.cpu_count()
     if rank == 0 and gpus == 1 and not args.no_cpu:
-        threads = args.cpu_threads or os.cpu_count()
-        step_t, raw = cpu_step_model(geom, threads)
-        est = (args.prompt_len - 1) * step_t(spec.global_batch)
-        for B, n in hist.items():
-            est += n * step_t(B)
-        line["cpu_baseline"] = {"value": est, "unit": UNIT, "cores": threads, "kind": "port",
-                                "sample": f"CPU oracle: 1 decoder layer + LM head timed at B=1 "
-                                          f"({raw[1]*1e3:.0f} ms/step x28 layers) and B=64 "
-                                          f"({raw[64]*1e3:.0f} ms/step), ctx 2048, extrapolated over the "
-                                          f"stage's {sum(hist.values())} rounds and prefill"}
+        try:
+            steps = cpu_decode_steps(geom, threads, ctx=stage_mean_context(spec))
+        except Exception as e:  # the bench line must still print
+            steps = None
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": threads, "kind": "port",
+                                    "sample": f"CPU oracle failed: {type(e).__name__}: {e}"}
+    if rank == 0 and gpus == 1 and not args.no_cpu and steps is not None:
+        est = cpu_stage_estimate(spec, steps, active_histogram(rep))
+        depth = f"full depth ({geom.num_layers} layers"
+        line["cpu_baseline"] = {
+            "value": est, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": (f"CPU oracle at {depth}, vocab {geom.vocab}, torch fp32 "
+                       f"with bf16 rounding, {threads} threads): decode steps measured at B="
+                       + ",".join(f"{b} ({t:.2f} s)" for b, t in steps["steps"].items())
+                       + f" at ctx {steps['ctx']} (the stage's round-weighted mean context) and a 64-token "
+                         f"prefill chunk ({steps['prefill64_s']:.2f} s); the stage = its "
+                         f"{sum(active_histogram(rep).values())} rounds at their active batch "
+                         f"(interpolated in B) + {spec.global_batch} prompts' prefill"),
+            "measured_steps_s": {str(b): t for b, t in steps["steps"].items()}}
+        try:
+            line["cpu_baseline"]["decision_layer"] = decision_layer_timing(args)
+        except Exception as e:
+            line["cpu_baseline"]["decision_layer"] = {"error": f"{type(e).__name__}: {e}"}
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def stage_mean_context(spec) -> int:
+    """Round-weighted mean context of a stage's active samples (prompt + generated so far)."""
+    from paper_2605_23945_b200.workload import sample_response_lengths
+    lens = np.minimum(np.asarray(sample_response_lengths(spec.distribution, spec.global_batch, spec.seed)),
+                      spec.l_max)
+    r = np.arange(int(lens.max()))
+    active = (lens[None, :] > r[:, None])
+    ctx = (spec.prompt_len + r)[:, None] * active
+    return int(round(float(ctx.sum() / max(1, active.sum())) / 64.0) * 64)
 
 
 def stage_roofline(spec, geom, decode_s: float, peak_gbps: float) -> dict:
@@ -372,9 +516,21 @@ def measured_table(model: str):
 
 
 def traffic_record():
+    """ncu DRAM traffic of the projection GEMM per launch (profiles/r2/ncu_traffic.json, from
+    `ncu --set full` of one QKV / O / gate-up / down launch each at B=64, averaged like
+    `achieved`); falls back to the round-1 single-launch record."""
+    try:
+        with open(os.path.join(HERE, "profiles", "r2", "ncu_traffic.json")) as fh:
+            d = json.load(fh)["gemm_swapab_kernel"]
+        return {"dram_bytes_per_launch": d["dram_bytes_per_launch"], "note": d["note"]}
+    except Exception:
+        pass
     try:
         with open(os.path.join(HERE, "profiles", "r1", "ncu_traffic.json")) as fh:
-            return json.load(fh)["gemm_swapab_kernel"]
+            d = json.load(fh)["gemm_swapab_kernel"]
+        return {"dram_bytes_per_launch": d["dram_bytes"],
+                "note": f"ncu dram read+write of one launch ({d['launch']}) vs its {d['algorithmic_bytes']} "
+                        f"algorithmic bytes; profiles/r1/ncu_traffic.json"}
     except Exception:
         return None
 
@@ -399,46 +555,50 @@ def switch_microbench(args, hbm_peak):
             "copy_kernel_ms": r["copy_kernel_ms"], "copy_gbps": r["copy_gbps"],
             "roofline": {"bound": "hbm", "achieved": 2 * r["copy_gbps"], "peak": hbm_peak, "unit": "GB/s",
                          "frac": 2 * r["copy_gbps"] / hbm_peak, "note": "read+write bytes of the copy kernels"},
-            "switch_device_ms": r["switch_device_ms"], "host_plan_s": r["host_plan_s"],
-            "host_capture_s": r["host_capture_s"]}
+            "switch_device_ms": r["switch_device_ms"], "release_to_resume_ms": r["release_to_resume_ms"],
+            "max_gpu_peer_bytes": r["max_gpu_peer_bytes"], "max_gpu_local_bytes": r["max_gpu_local_bytes"],
+            "host_switch_s": r["host_switch_s"], "host_plan_s": r["host_plan_s"],
+            "host_capture_s": r["host_capture_s"],
+            "note": "every rank on this GPU: a peer pull is an HBM copy; switch_device_ms runs from the first "
+                    "rank's arrival at the opening barrier to the last rank's resume, host work included"}
 
 
 def reference_arm(args):
-    """The reference-side CPU path: the oracle port on the host cores (rank 0 only)."""
+    """The reference-side CPU path on the host cores (rank 0 only): the CPU oracle port of the
+    decode step at full depth (the reference itself has no decode arithmetic),
+    timed per step and composed over the stage's rounds, plus the reference's own decision
+    layer (evaluate / run, restated bit-exact) timed single-threaded."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from paper_2605_23945_b200.engine import run as sim_run
-    from paper_2605_23945_b200.models import geometry
     spec, geom = build_spec(args, max(1, args.gpus))
     threads = args.cpu_threads or os.cpu_count()
-    # the stage's round profile (batch per round) comes from the reference's own loop on the
-    # analytic model: identical samples, lengths and block structure
-    import dataclasses
+    # the stage's round profile (active batch per round) comes from the reference's own loop
+    # on the analytic model: identical samples, lengths and block structure
     rep = sim_run(dataclasses.replace(spec, mode="static"))
-    hist = {}
-    for nr in rep.node_reports:
-        for ev in nr["events"]:
-            if ev["type"] == "step-block":
-                lo, hi = (int(x) for x in ev["detail"].split("=")[1].split(".."))
-                hist[ev["active"]] = hist.get(ev["active"], 0) + (hi - lo)
+    hist = active_histogram(rep)
+    ctx = stage_mean_context(spec)
+    cpu = CpuOracleSteps(geom, threads, ctx)
+    for _ in range(args.warmup):  # warm-up passes: one B=1 step each (the full pass is ~30 s)
+        cpu.orc.step([1], [ctx - 1], [0])
     vals = []
-    for _ in range(args.warmup + args.steps):
-        step_t, raw = cpu_step_model(geom, threads)
-        est = (args.prompt_len - 1) * step_t(spec.global_batch)
-        for B, n in hist.items():
-            est += n * step_t(B)
-        vals.append(est)
-    value = float(np.mean(vals[args.warmup:]))
-    sample = (f"CPU oracle (torch fp32, {threads} threads): 1 decoder layer + LM head at B=1 and B=64, ctx "
-              f"2048, extrapolated to {geom.num_layers} layers and the stage's {sum(hist.values())} rounds")
+    for _ in range(args.steps):
+        steps = cpu.measure()
+        vals.append(cpu_stage_estimate(spec, steps, hist))
+    value = float(np.mean(vals))
+    sample = (f"CPU oracle (torch fp32 with bf16 rounding, {threads} threads) at full depth: decode steps at B="
+              + ",".join(str(b) for b in steps["steps"]) + f", ctx {ctx}, and a 64-token prefill chunk, "
+              f"composed over the stage's {sum(hist.values())} rounds at their active batch")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False,
         "scaling": "weak", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
-        "config": {"workload": f"c2-weak: {args.model}, {args.per_gpu_batch} samples, l_max {args.l_max}",
+        "config": {"workload": f"c2-weak: {args.model}, {args.per_gpu_batch} samples/GPU, l_max {args.l_max}",
                    "model": args.model, "global_batch": spec.global_batch},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
+                         "measured_steps_s": {str(b): t for b, t in steps["steps"].items()},
+                         "decision_layer": decision_layer_timing(args)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 

@@ -71,6 +71,13 @@ typedef struct tps_kv_move {
 } tps_kv_move;
 
 /* ---------------------------------------------------------------- setup --- */
+/* Soft watchdog: a device wait that exceeds its 20 s budget prints, raises this word
+ * (nonzero code) and abandons its wait instead of trapping; every wait that has lasted
+ * over 1 ms polls it and abandons too. Results computed after a raise are garbage: the
+ * host must check the word (the Python binding does on every checked call) and fail. */
+unsigned int tps_abort_status(void);
+void tps_abort_clear(void);
+
 /* Library/ABI version string. */
 const char* tps_version(void);
 /* Last error text of the calling thread (valid until the next failing call). */

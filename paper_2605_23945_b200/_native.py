@@ -73,6 +73,8 @@ SIGNATURES = {
     "tps_argmax_finalize": (_i32, [_pp, _i32, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _i32, _vp, _vp]),
     "tps_epoch_advance": (_i32, [_vp, _vp]),
     "tps_sum_partials": (_i32, [_vp, _i32, _i64, _i64, _vp, _vp]),
+    "tps_abort_status": (ctypes.c_uint32, []),
+    "tps_abort_clear": (None, []),
     "tps_copy_items": (_i32, [_vp, _i32, _i32, _i32, _vp]),
     "tps_kv_move_items": (_i32, [_vp, _i32, _i64, _vp, _i32, _i32, _i64, _vp, _vp, _vp]),
     "tps_barrier": (_i32, [_pp, _i32, _vp, _i32, _i32, ctypes.c_uint64, _vp]),
@@ -146,8 +148,20 @@ def lib():
     return _lib if _lib is not None else load_library()
 
 
+def check_abort(what: str = "") -> None:
+    """Raise if a device watchdog fired (the soft-abort word, include/tpshift_b200.h): the work
+    queued since is garbage. The word is cleared so the process can continue after reporting."""
+    code = lib().tps_abort_status()
+    if code:
+        lib().tps_abort_clear()
+        raise RuntimeError(f"libtpshift_b200 device watchdog fired (code {code}){': ' + what if what else ''}; "
+                           f"results since are invalid")
+
+
 def check(rc: int, what: str = "") -> None:
     if rc == TPS_OK:
+        if _lib is not None and _lib.tps_abort_status():
+            check_abort(what)
         return
     msg = lib().tps_last_error().decode(errors="replace")
     text = f"{what}: {msg}" if what else msg

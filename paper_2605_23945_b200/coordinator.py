@@ -721,6 +721,7 @@ class B200Backend:
             out["groups"][f"{ep}:{g}"] = {
                 "prefill": s.elapsed_time(tl.prefill_end) / 1e3 if tl.prefill_end is not None else None,
                 "rounds": [s.elapsed_time(e) / 1e3 for e in tl.rounds]}
+        nat.check_abort("generation stage")
         for r, bad in self._bad.items():
             if int(bad.item()):
                 raise PlanVerificationError(f"rank {r}: {int(bad.item())} KV copy items pointed outside a pool")

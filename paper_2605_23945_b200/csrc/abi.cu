@@ -4,6 +4,7 @@
 #include <stdio.h>
 
 #include <string>
+#include <vector>
 
 #include "../../include/tpshift_b200.h"
 #include "common.cuh"
@@ -120,6 +121,35 @@ static WaitSpec make_wait(const tps_wait* w) {
 
 static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// ---- soft-abort word (common.cuh): one host-mapped word per process, its device address
+// installed in every translation unit's copy of g_abort_word on every initialised device
+static std::vector<AbortSetter>& abort_setters() {
+  static std::vector<AbortSetter> v;
+  return v;
+}
+int register_abort_setter(AbortSetter f) {
+  abort_setters().push_back(f);
+  return (int)abort_setters().size();
+}
+static unsigned int* g_abort_host = nullptr;
+
+static int install_abort_word() {
+  if (!g_abort_host) {
+    void* p = nullptr;
+    TPS_CUDA_TRY(cudaHostAlloc(&p, 64, cudaHostAllocMapped | cudaHostAllocPortable));
+    g_abort_host = static_cast<unsigned int*>(p);
+    *reinterpret_cast<volatile unsigned int*>(g_abort_host) = 0u;
+  }
+  void* dptr = nullptr;
+  TPS_CUDA_TRY(cudaHostGetDevicePointer(&dptr, g_abort_host, 0));
+  for (AbortSetter f : abort_setters()) {
+    const int e = f(static_cast<unsigned int*>(dptr));
+    if (e != 0)
+      return fail(kCuda, std::string("abort word: ") + cudaGetErrorString(static_cast<cudaError_t>(e)));
+  }
+  return kOk;
+}
+
 }  // namespace tps
 
 using namespace tps;
@@ -129,6 +159,14 @@ extern "C" {
 const char* tps_version(void) { return "tpshift_b200 1.1 (sm_100a; tcgen05 GEMM, paged GQA decode, P2P switch, PDL)"; }
 
 const char* tps_last_error(void) { return g_last_error.c_str(); }
+
+unsigned int tps_abort_status(void) {
+  return g_abort_host ? *reinterpret_cast<volatile unsigned int*>(g_abort_host) : 0u;
+}
+
+void tps_abort_clear(void) {
+  if (g_abort_host) *reinterpret_cast<volatile unsigned int*>(g_abort_host) = 0u;
+}
 
 int tps_init(int device, int* sm_count) {
   TPS_CUDA_TRY(cudaSetDevice(device));
@@ -144,6 +182,7 @@ int tps_init(int device, int* sm_count) {
   if (!rc) rc = configure_copy();
   if (!rc) rc = configure_decode_ops();
   if (!rc) rc = configure_persist();
+  if (!rc) rc = install_abort_word();
   return rc;
 }
 

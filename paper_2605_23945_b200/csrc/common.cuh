@@ -1,8 +1,12 @@
 // Shared device/host helpers for libtpshift_b200 (sm_100a only).
 //
-// Every spin loop in this library is bounded by a watchdog (globaltimer based):
-// a protocol bug turns into a trapped kernel (a loud CUDA error) instead of a
-// hung GPU.
+// Every spin loop in this library is bounded by a watchdog (globaltimer based).
+// A watchdog that fires does not trap (a trapped kernel leaves the device faulted,
+// which on a shared GPU pool takes the GPU out of service): it prints, raises the
+// library's abort word and abandons its wait; every other wait that has lasted
+// over 1 ms polls the word and abandons too, so a protocol bug drains the queued
+// work in seconds. The host sees the abort on its next checked call
+// (tps_abort_status -> RuntimeError): a loud failure, results discarded.
 #pragma once
 
 #include <cuda.h>
@@ -69,8 +73,47 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
   return t;
 }
 
-// Watchdog budget for every device-side wait: 20 s. Exceeding it traps.
+// Watchdog budget for every device-side wait: 20 s. Exceeding it raises the abort word.
 constexpr uint64_t kWatchdogNs = 20ull * 1000ull * 1000ull * 1000ull;
+// A wait polls the abort word once it has lasted this long (the fast path never reads it).
+constexpr uint64_t kAbortPollNs = 1000ull * 1000ull;
+
+// ------------------------------------------------------------ soft abort ---
+// One host-mapped word (allocated by tps_init) shared by every translation unit: each TU
+// holds its own copy of the pointer, set through the setter it registers here.
+static __device__ unsigned int* g_abort_word = nullptr;
+using AbortSetter = int (*)(unsigned int*);
+int register_abort_setter(AbortSetter f);  // host side, abi.cu
+namespace {
+int set_abort_word_in_this_tu(unsigned int* p) {
+  return (int)cudaMemcpyToSymbol(g_abort_word, &p, sizeof(p));
+}
+const int g_abort_registered = register_abort_setter(&set_abort_word_in_this_tu);
+}  // namespace
+
+__device__ __forceinline__ bool abort_raised() {
+  const unsigned int* w = g_abort_word;
+  return w != nullptr && *reinterpret_cast<const volatile unsigned int*>(w) != 0u;
+}
+static __device__ __noinline__ void raise_abort(unsigned int code) {
+  unsigned int* w = g_abort_word;
+  if (w != nullptr) {
+    *reinterpret_cast<volatile unsigned int*>(w) = code;
+    __threadfence_system();
+  }
+}
+// true when a wait that started at t0 must be abandoned (watchdog fired here -- the caller
+// prints first -- or raised elsewhere)
+__device__ __forceinline__ bool wait_abandoned(uint64_t t0, bool* fired) {
+  const uint64_t dt = globaltimer_ns() - t0;
+  if (dt < kAbortPollNs) return false;
+  if (abort_raised()) return true;
+  if (dt > kWatchdogNs) {
+    *fired = true;
+    return true;
+  }
+  return false;
+}
 
 __device__ __forceinline__ float bf2f(__nv_bfloat16 v) { return __bfloat162float(v); }
 __device__ __forceinline__ __nv_bfloat16 f2bf(float v) { return __float2bfloat16_rn(v); }
@@ -118,10 +161,14 @@ __device__ __forceinline__ void wait_counter_geq(const uint64_t* p, uint64_t tar
   const uint64_t t0 = globaltimer_ns();
   while (ld_acquire_sys(p) < target) {
     __nanosleep(64);
-    if (globaltimer_ns() - t0 > kWatchdogNs) {
-      printf("tps watchdog: counter %p stuck at %llu < %llu\n", (const void*)p,
-             (unsigned long long)ld_acquire_sys(p), (unsigned long long)target);
-      __trap();
+    bool fired = false;
+    if (wait_abandoned(t0, &fired)) {
+      if (fired) {
+        printf("tps watchdog: counter %p stuck at %llu < %llu\n", (const void*)p,
+               (unsigned long long)ld_acquire_sys(p), (unsigned long long)target);
+        raise_abort(1);
+      }
+      return;
     }
   }
 }
@@ -161,10 +208,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
   const uint64_t t0 = globaltimer_ns();
   while (!mbar_try_wait(bar, parity)) {
-    if (globaltimer_ns() - t0 > kWatchdogNs) {
-      printf("tps watchdog: mbarrier wait timed out (block %d thread %d)\n", blockIdx.x,
-             threadIdx.x);
-      __trap();
+    bool fired = false;
+    if (wait_abandoned(t0, &fired)) {
+      if (fired) {
+        printf("tps watchdog: mbarrier wait timed out (block %d thread %d)\n", blockIdx.x, threadIdx.x);
+        raise_abort(2);
+      }
+      return;
     }
   }
 }

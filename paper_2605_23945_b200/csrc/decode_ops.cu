@@ -197,10 +197,14 @@ __device__ __forceinline__ float4 ll_sum4(const uint64_t* base, int n, long long
           const uint64_t* p = base + (long long)(i0 + j) * stride + off4 * 4;
           const uint64_t t0 = globaltimer_ns();
           do {
-            if (globaltimer_ns() - t0 > kWatchdogNs) {
-              printf("tps watchdog: LL source %d of %d (base %p, element %lld) tag %u != %u\n", i0 + j, n,
-                     (const void*)base, off4 * 4, (unsigned)(a[j].x >> 32), want);
-              __trap();
+            bool fired = false;
+            if (wait_abandoned(t0, &fired)) {
+              if (fired) {
+                printf("tps watchdog: LL source %d of %d (base %p, element %lld) tag %u != %u\n", i0 + j, n,
+                       (const void*)base, off4 * 4, (unsigned)(a[j].x >> 32), want);
+                raise_abort(3);
+              }
+              break;
             }
             a[j] = ld_relaxed_sys_v2u64(p);
             c[j] = ld_relaxed_sys_v2u64(p + 2);

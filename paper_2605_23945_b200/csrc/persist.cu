@@ -151,9 +151,13 @@ __device__ __forceinline__ void wait_geq(const unsigned long long* p, unsigned l
   if (ld_rlx(p) < target) {
     const uint64_t t0 = globaltimer_ns();
     while (ld_rlx(p) < target) {
-      if (globaltimer_ns() - t0 > kWatchdogNs) {
-        printf("tps persist watchdog: wait %d block %d at %llu < %llu\n", what, blockIdx.x, ld_rlx(p), target);
-        __trap();
+      bool fired = false;
+      if (wait_abandoned(t0, &fired)) {
+        if (fired) {
+          printf("tps persist watchdog: wait %d block %d at %llu < %llu\n", what, blockIdx.x, ld_rlx(p), target);
+          raise_abort(4);
+        }
+        break;
       }
     }
   }
@@ -756,10 +760,14 @@ __device__ void norm_slices(const RankDev& R, const Geo& g, const Smem& S, int c
               const uint64_t* p = pp[a] + pc * R.ll_src_stride;
               const uint64_t t0 = globaltimer_ns();
               do {
-                if (globaltimer_ns() - t0 > kWatchdogNs) {
-                  printf("tps persist watchdog: LL phase %d block %d item %d piece %d tag %u != %u\n", phase,
-                         blockIdx.x, i, pc, (unsigned)(t.x >> 32), want);
-                  __trap();
+                bool fired = false;
+                if (wait_abandoned(t0, &fired)) {
+                  if (fired) {
+                    printf("tps persist watchdog: LL phase %d block %d item %d piece %d tag %u != %u\n", phase,
+                           blockIdx.x, i, pc, (unsigned)(t.x >> 32), want);
+                    raise_abort(5);
+                  }
+                  break;
                 }
                 t = ld_relaxed_sys_v2u64(p);
               } while ((uint32_t)(t.x >> 32) != want || (uint32_t)(t.y >> 32) != want);
@@ -1075,9 +1083,13 @@ __device__ void finish_argmax(const RankDev& R, const Geo& g, const Smem& S, uin
       const uint64_t* p = R.am_mine + (((size_t)par * kMaxTP + q) * kMaxB + b) * 2;
       const uint64_t t0 = globaltimer_ns();
       while ((uint32_t)(v[q].x >> 32) != want || (uint32_t)(v[q].y >> 32) != want) {
-        if (globaltimer_ns() - t0 > kWatchdogNs) {
-          printf("tps persist watchdog: argmax src %d row %d\n", q, b);
-          __trap();
+        bool fired = false;
+        if (wait_abandoned(t0, &fired)) {
+          if (fired) {
+            printf("tps persist watchdog: argmax src %d row %d\n", q, b);
+            raise_abort(6);
+          }
+          break;
         }
         v[q] = ld_relaxed_sys_v2u64(p);
       }

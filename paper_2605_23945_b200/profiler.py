@@ -36,8 +36,10 @@ def gemm_probe(ex: InferExecutor, B: int, reps: int = 2) -> dict:
     """Time every projection family at batch B over all layers (working set >> L2).
 
     Returns {family: {"ms": avg launch ms, "bytes": algorithmic bytes per launch,
-    "n": launches}} plus "total" over one decode step's projections. Algorithmic
-    bytes = weight shard + activations read + fp32 partials written.
+    "overhead_bytes": split-K partial bytes beyond one output, "n": launches}} plus "total"
+    over one decode step's projections. Algorithmic bytes (SURVEY 8(d) units) = weight shard +
+    activations read + one fp32 output row per batch row; the extra fp32 partials of a
+    split-K launch (written, then read back by the consumer) are overhead, not algorithmic.
     """
     g = ex.geom
     lib = nat.lib()
@@ -46,7 +48,8 @@ def gemm_probe(ex: InferExecutor, B: int, reps: int = 2) -> dict:
     xs = {"w_qkv": ex.xn, "w_o": ex.attn, "w_gu": ex.xn, "w_d": ex.act}
     fams = [(f, [(l, f) for l in range(g.num_layers)]) for f in ("w_qkv", "w_o", "w_gu", "w_d")]
     fams.append(("lm_head", [(-1, "lm_head")] * max(1, g.num_layers // 4)))
-    tot_ms = tot_b = 0.0
+    tot_ms = tot_b = tot_o = 0.0
+    launches = 0
     for fam, keys in fams:
         x = xs.get(fam, ex.xn)
         w0 = ex.w[keys[0]]
@@ -66,12 +69,49 @@ def gemm_probe(ex: InferExecutor, B: int, reps: int = 2) -> dict:
         torch.cuda.synchronize()
         nl = reps * len(keys)
         ms = e0.elapsed_time(e1) / nl
-        byt = n * k * 2 + B * k * 2 + s * B * n * 4  # weights + activations + fp32 split partials
-        out[fam] = {"ms": ms, "bytes": byt, "n": len(keys) if fam != "lm_head" else 1, "splits": s}
+        byt = n * k * 2 + B * k * 2 + B * n * 4  # weights + activations + one fp32 output
+        ovh = (s - 1) * B * n * 4  # the other split partials (written + read back: x2 on HBM)
+        out[fam] = {"ms": ms, "bytes": byt, "overhead_bytes": ovh, "n": len(keys) if fam != "lm_head" else 1,
+                    "splits": s}
         per_step = g.num_layers if fam != "lm_head" else 1
         tot_ms += ms * per_step
         tot_b += byt * per_step
-    out["total"] = {"ms": tot_ms, "bytes": tot_b, "gbps": tot_b / tot_ms / 1e6}
+        tot_o += ovh * per_step
+        launches += per_step
+    out["total"] = {"ms": tot_ms, "bytes": tot_b, "overhead_bytes": tot_o, "launches": launches,
+                    "gbps": tot_b / tot_ms / 1e6}
+    return out
+
+
+def tail_probe(geom, tp: int, batches, ctx: int, peak_gbps: float, n: int = 30) -> dict:
+    """Post-switch tail steps (SURVEY 8(d) "tail = post-switch B <= 32"): one TP-`tp` rank alone on
+    the device (loopback peer table, `loopback_rank`), graph-replayed steps at context `ctx` per
+    batch, vs the rank's HBM floor = weight shards (linears + LM-head shard) + live K/V + new K/V
+    at the measured copy peak. Returns {B: {"ms", "floor_ms", "frac", "kernels"}}."""
+    from .kvcache import pages_for
+    from .models import rank_shard
+    from .shards import arena_layout
+    maxb = max(batches)
+    r, runner = loopback_rank(geom, tp, maxb, maxb, ctx + 256, maxb * pages_for(ctx + 256))
+    slots = [admit([r], i, [1, 2, 3], max_ctx=ctx + 200) for i in range(maxb)]
+    sh = rank_shard(geom, tp, 0)
+    lay = arena_layout(geom, sh)
+    emb = geom.vocab * geom.hidden * 2
+    w = lay.total_bytes - emb  # embedding rows are gathered, not streamed
+    kv_tok = geom.num_layers * 2 * sh.n_kv * geom.head_dim * 2
+    out = {}
+    for B in batches:
+        bk = r.executor.bucket(B)
+        runner.set_rows(bk, slots[:B])
+        r.slots.pos[:] = ctx
+        ms = step_probe(runner, bk, n)
+        byt = w + B * (ctx + 1) * kv_tok
+        floor = byt / (peak_gbps * 1e9) * 1e3
+        out[B] = {"ms": ms, "floor_ms": floor, "frac": floor / ms, "bytes": byt,
+                  "kernels": runner.kernels_per_step(bk)}
+    del r, runner
+    gc.collect()
+    torch.cuda.empty_cache()
     return out
 
 
