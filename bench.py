@@ -509,10 +509,12 @@ def stage_phases(rep, meas) -> dict:
 def measured_table(model: str):
     """The B200 Offline Profiler's table for this model (presets/b200_<model>_profile.csv,
     measured by tools/profile_b200.py): Algorithm 1's Latency Predictor is fitted to it.
-    None (the analytic b200.cfg calibration) when the model has not been profiled."""
+    None (the analytic b200.cfg calibration) when the model has not been profiled. The measured
+    points are made monotone in context and batch first (profiler.monotone_table)."""
     from paper_2605_23945_b200.latency import load_table
+    from paper_2605_23945_b200.profiler import monotone_table
     path = os.path.join(HERE, "paper_2605_23945_b200", "presets", f"b200_{model}_profile.csv")
-    return load_table(path) if os.path.exists(path) else None
+    return monotone_table(load_table(path)) if os.path.exists(path) else None
 
 
 def traffic_record():

@@ -358,6 +358,41 @@ def verify_kv_moves(moves: np.ndarray, n_kv_local: int, slots: int) -> list[str]
     return issues
 
 
+_WEIGHT_BYTES: dict = {}
+
+
+def switch_bytes_per_gpu(geom: DecoderGeometry, old: Layout, new: Layout, merged, old_group, kv_len) -> dict:
+    """{target rank: (bytes pulled from peers, bytes copied locally)} of a migrate switch as the
+    Switch Executor runs it: the weight pulls (plan_weight_pulls, memoised), the KV moves
+    (plan_kv_moves' head runs, one per (sample, kv-head run)) and the token-history rows.
+    merged[g] lists the samples of new group g; old_group(s) / kv_len(s) give a sample's group
+    before the switch and its cached positions."""
+    chunk = PAGE * geom.head_dim * 2
+    out = {}
+    for r in range(new.world):
+        key = (geom.name, geom.num_layers, old, new, r)
+        if key not in _WEIGHT_BYTES:
+            _WEIGHT_BYTES[key] = nvlink_bytes(cached_weight_pulls(geom, old, new, r), r)
+        nv, loc = _WEIGHT_BYTES[key]
+        g = new.group_of(r)
+        for smp in (merged[g] if g < len(merged) else ()):
+            og, n = int(old_group(smp)), int(kv_len(smp))
+            npg = pages_for(n)
+            for src, _, _, nh in _head_runs(geom, old, new, r, og):
+                b = 2 * geom.num_layers * npg * nh * chunk
+                if src == r:
+                    loc += b
+                else:
+                    nv += b
+            hsrc = _pick_source(old.ranks_of_group(og), r, 0)
+            if hsrc == r:
+                loc += 4 * (n + 1)
+            else:
+                nv += 4 * (n + 1)
+        out[r] = (nv, loc)
+    return out
+
+
 def plan_history_pulls(old: Layout, dst_rank: int, sources: list[KVSource], targets: list[KVTarget],
                        lens: list[int], old_hist_ld: int, new_hist_ld: int) -> Pieces:
     """Token-history rows (prompt + generated so far) of the migrating samples."""

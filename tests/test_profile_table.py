@@ -66,3 +66,39 @@ def test_bench_stage_roofline_units():
     assert r["rounds"] == 3104 and r["bytes"] > r["rounds"] * w
     assert abs(r["decode_floor_s"] - r["bytes"] / 6547.2e9) < 1e-9
     assert 0.6 < r["frac"] < 0.8
+
+
+def test_bench_cpu_stage_estimate_composes_measured_steps():
+    """cpu_baseline: the stage = every round at its active batch (piecewise-linear between the
+    measured full-depth step times) + the prompts' prefill at the 64-token chunk rate."""
+    import argparse
+    import bench
+    ns = argparse.Namespace(model="qwen2.5-7b", per_gpu_batch=64, l_max=8192, prompt_len=512, seed=4, tp_list="",
+                            initial_tp=1)
+    spec, _ = bench.build_spec(ns, 1)
+    steps = {"steps": {1: 1.0, 8: 2.0, 64: 9.0}, "prefill64_s": 0.5}
+    hist = {1: 10, 4: 3, 64: 2, 36: 1}
+    got = bench.cpu_stage_estimate(spec, steps, hist)
+    dec = 10 * 1.0 + 3 * (1.0 + 3 / 7) + 2 * 9.0 + 1 * (2.0 + 7.0 * 28 / 56)
+    assert abs(got - (dec + 64 * 8 * 0.5)) < 1e-9
+    rep = run(dataclasses.replace(spec, mode="static"))
+    h = bench.active_histogram(rep)
+    assert sum(h.values()) == 3104 and max(h) == 64
+    assert 512 < bench.stage_mean_context(spec) < 8704
+
+
+def test_switch_rate_is_max_gpu_peer_bytes_over_release_to_resume():
+    """RecordedBackend's switch record: per GPU, bytes pulled from peers over that
+    GPU's barrier-release -> resume window; the rate is the max over GPUs; local bytes apart."""
+    from paper_2605_23945_b200.coordinator import RecordedBackend
+    sw = {"ranks": {0: [1.0, 1.1, 1.2, 1.3, 1.4], 1: [1.05, 1.1, 1.25, 1.32, 1.5]},
+          "per_rank": {0: {"nvlink": 30e9, "local": 5e9}, 1: {"nvlink": 20e9, "local": 1e9}},
+          "nvlink_bytes": 50e9, "local_bytes": 6e9, "kv_bytes": 1e9, "weight_bytes": 55e9,
+          "host_plan_s": 0.001, "host_capture_s": 0.0, "host_build_s": 0.0, "host_s": 0.002,
+          "state_method": "migrate"}
+    rb = RecordedBackend([{"groups": {}, "switches": [sw]}])
+    rb.nswitch = 1
+    rec = rb.switch_record_extra(None)
+    assert abs(rec["release_to_resume_s"] - 0.4) < 1e-12
+    assert rec["max_gpu_peer_bytes"] == 30e9 and rec["max_gpu_local_bytes"] == 5e9
+    assert abs(rec["peer_gbps_per_gpu"] - max(30 / 0.3, 20 / 0.4)) < 1e-9

@@ -18,9 +18,13 @@ ap.add_argument("--gpus", default="1,2,4,8")
 ap.add_argument("--per-gpu-batch", type=int, default=64)
 ap.add_argument("--l-max", type=int, default=8192)
 ap.add_argument("--tp-list", default="", help="Algorithm 1 candidates (default 1,N as bench.py)")
+ap.add_argument("--raw", action="store_true", help="the measured table as is (default: monotone fit, as bench.py)")
 a = ap.parse_args()
 tab = load_table(a.table or os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                          "paper_2605_23945_b200", "presets", f"b200_{a.model}_profile.csv"))
+if not a.raw:
+    from paper_2605_23945_b200.profiler import monotone_table
+    tab = monotone_table(tab)
 for n in (int(x) for x in a.gpus.split(",")):
     if n % a.initial_tp:
         continue
@@ -28,7 +32,7 @@ for n in (int(x) for x in a.gpus.split(",")):
                             tp_list=a.tp_list, initial_tp=a.initial_tp)
     spec, geom = bench.build_spec(ns, n)
     rep = run(spec, tab, TableBackend(spec, tab))
-    out = {"model": a.model, "gpus": n, "per_gpu_batch": a.per_gpu_batch, "l_max": a.l_max, "tp_list": list(spec.controller.tp_list), "adaptive_s": round(rep.generation_time, 3),
+    out = {"model": a.model, "table": "raw" if a.raw else "monotone", "gpus": n, "per_gpu_batch": a.per_gpu_batch, "l_max": a.l_max, "tp_list": list(spec.controller.tp_list), "adaptive_s": round(rep.generation_time, 3),
            "switches": [[s["from_tp"], s["to_tp"], s["round"], round(s["breakdown"]["total"], 3)]
                         for nr in rep.node_reports for s in nr["switches"]], "static_s": {}}
     for tp in (1, 2, 4, 8):
