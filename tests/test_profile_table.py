@@ -102,3 +102,46 @@ def test_switch_rate_is_max_gpu_peer_bytes_over_release_to_resume():
     assert abs(rec["release_to_resume_s"] - 0.4) < 1e-12
     assert rec["max_gpu_peer_bytes"] == 30e9 and rec["max_gpu_local_bytes"] == 5e9
     assert abs(rec["peer_gbps_per_gpu"] - max(30 / 0.3, 20 / 0.4)) < 1e-9
+
+
+def test_monotone_table_is_monotone_and_close_to_the_measurement(table):
+    from paper_2605_23945_b200.profiler import monotone_table
+    sm = monotone_table(table)
+    raw = {(p.tp, p.batch, p.ctx_len): p for p in table.points}
+    fit = {(p.tp, p.batch, p.ctx_len): p for p in sm.points}
+    assert raw.keys() == fit.keys() and sm.token_cap == table.token_cap
+    for k, p in fit.items():
+        assert abs(p.decode_latency - raw[k].decode_latency) <= 0.03 * raw[k].decode_latency
+        assert p.prefill_latency == raw[k].prefill_latency
+    for axis in (2, 1):
+        groups = {}
+        for k in fit:
+            groups.setdefault((k[0], k[1]) if axis == 2 else (k[0], k[2]), []).append(k)
+        for ks in groups.values():
+            ys = [fit[k].decode_latency for k in sorted(ks, key=lambda k: k[axis])]
+            assert all(b >= a - 1e-15 for a, b in zip(ys, ys[1:]))
+
+
+def test_table_backend_switch_bytes_match_the_executed_plans():
+    """switch_bytes_per_gpu (what TableBackend prices) = the weight pull plans' bytes + the KV
+    chunk plan's bytes + history rows, per target rank, split into peer and local."""
+    from paper_2605_23945_b200.models import geometry
+    from paper_2605_23945_b200.switch_executor import (KVSource, KVTarget, Layout, cached_weight_pulls,
+                                                       nvlink_bytes, plan_kv_pulls, switch_bytes_per_gpu)
+    from paper_2605_23945_b200.workload import Sample
+    geom = geometry("mini-qwen")
+    old, new = Layout(2, 8), Layout(4, 8)
+    samples = [Sample(id=i, prompt_len=8, target_response_len=100, generated_len=20 + 37 * i, intra_dp_group=i % 4)
+               for i in range(6)]
+    merged = [[s for s in samples if s.id % 2 == g] for g in range(2)]
+    got = switch_bytes_per_gpu(geom, old, new, merged, lambda s: s.intra_dp_group, lambda s: s.context_len - 1)
+    for r in range(8):
+        nv, loc = nvlink_bytes(cached_weight_pulls(geom, old, new, r), r)
+        mine = merged[new.group_of(r)]
+        src = [KVSource(old_group=s.intra_dp_group, slot=0, pages=tuple(range(40))) for s in mine]
+        tgt = [KVTarget(slot=0, pages=tuple(range(40))) for s in mine]
+        kp = plan_kv_pulls(geom, old, new, r, src, tgt, [s.context_len - 1 for s in mine], 64, 64)
+        a, b = nvlink_bytes(kp, r)
+        h_nv = sum(4 * s.context_len for s in mine if r not in old.ranks_of_group(s.intra_dp_group))
+        h_loc = sum(4 * s.context_len for s in mine if r in old.ranks_of_group(s.intra_dp_group))
+        assert got[r] == (nv + a + h_nv, loc + b + h_loc), r
