@@ -166,20 +166,9 @@ int tps_reduce_push(const float* src, int nsrc, int64_t src_stride, float* const
 int tps_reduce_push_ll(const float* src, int nsrc, int64_t src_stride, uint64_t* const* dsts, int ndst, int64_t n,
                        const uint64_t* epoch, uint32_t tag_mult, uint32_t tag_add, void* stream);
 
-/* Split-K count of tps_linear_qkv_rope for an [n x k] QKV weight at batch b; 0 when the
- * shape does not take the fused form (b > 64, more tiles x splits than SMs, ...). */
-int tps_qkv_fused_splits(int64_t n, int64_t k, int64_t b);
-
 /* Split count of tps_linear_push_ll_cluster for [n x k] at batch b (0: not supported:
  * b > 64 or more tiles than SMs). */
 int tps_cluster_splits(int64_t n, int64_t k, int64_t b);
-
-/* Gate/up projection + SwiGLU with split-K kept: the split CTAs of a tile (one cluster) sum
- * their partials over DSMEM in split order, then act[i][f] = bf16(silu(gate_f . x_i) *
- * (up_f . x_i)) -- the results of tps_linear + tps_silu_mul in one launch (same W layout as
- * tps_linear_silu). */
-int tps_linear_silu_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,
-                            int64_t x_rows, int64_t ldx, void* act, int64_t ld_act, void* stream);
 
 /* LM head with greedy argmax stage 1 in the epilogue (split-K 1): logits [b][n] fp32 and, per
  * row i and 128-column tile t, cand[i * ceil(n/128) + t] = {max logit, smallest vocab index on
@@ -187,11 +176,6 @@ int tps_linear_silu_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, co
  * nchunk = ceil(n / 128); the same token tps_argmax_stage1 + finalize would pick. */
 int tps_linear_argmax(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,
                       int64_t x_rows, int64_t ldx, float* logits, void* cand, int vocab0, void* stream);
-
-/* out[i][j] = (W x_i)_j as ONE fp32 [b][n] result: the split-K CTAs of a tile (one cluster)
- * reduce their partials over DSMEM in split order (tps_linear's partials summed in-kernel). */
-int tps_linear_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,
-                       int64_t x_rows, int64_t ldx, float* out, void* stream);
 
 /* Row-parallel projection + allreduce push with the split-K reduction inside the kernel:
  * the split CTAs of a weight tile form one cluster and sum their partials over DSMEM (split
@@ -201,16 +185,6 @@ int tps_linear_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, const v
 int tps_linear_push_ll_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,
                                int64_t x_rows, int64_t ldx, uint64_t* const* dsts, int ndst,
                                const uint64_t* epoch, uint32_t tag_mult, uint32_t tag_add, void* stream);
-
-/* QKV projection finished in-kernel: out = W x (split-K over a thread-block cluster, the
- * partials summed over DSMEM in split order) + bias, RoPE, q -> bf16 [b][nq][D], k/v
- * appended into the paged cache -- the results of tps_linear + tps_qkv_rope_append in
- * one launch. n = (nq + 2 nkv) * D. */
-int tps_linear_qkv_rope(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,
-                        int64_t x_rows, int64_t ldx, const void* bias, const int* row_slot,
-                        const int* pos_by_slot, const int* row_pos, const int* page_table, int max_pages,
-                        const float* cos_t, const float* sin_t, int nq, int nkv, int D, int page_size,
-                        void* q_out, void* k_cache, void* v_cache, void* stream);
 
 /* Positions per group of tps_prefill_attention for G query heads per KV head
  * (min(16, 64 / G); 0 if G > 64). */

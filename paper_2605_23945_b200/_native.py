@@ -36,18 +36,13 @@ SIGNATURES = {
     "tps_init": (_i32, [_i32, ctypes.POINTER(_i32)]),
     "tps_set_pdl": (None, [_i32]),
     "tps_linear_splits": (_i32, [_i64, _i64, _i64]),
-    "tps_qkv_fused_splits": (_i32, [_i64, _i64, _i64]),
     "tps_cluster_splits": (_i32, [_i64, _i64, _i64]),
     "tps_linear_argmax": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _vp, _vp, _i32, _vp]),
-    "tps_linear_silu_cluster": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _vp, _i64, _vp]),
-    "tps_linear_cluster": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _vp, _vp]),
     "tps_linear_push_ll_cluster": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _pp, _i32, _vp,
                                           ctypes.c_uint32, ctypes.c_uint32, _vp]),
     "tps_prefill_group_positions": (_i32, [_i32]),
     "tps_prefill_attention": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _i32, _i32, _i32, _i32, _vp,
                                      _vp]),
-    "tps_linear_qkv_rope": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _i32,
-                                   _vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
     "tps_linear": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _vp, _i32, _vp]),
     "tps_linear_push": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _pp, _i32, _i64, _i32, _pp, _i32,
                                 _vp, _vp]),

@@ -30,19 +30,12 @@ int linear_silu(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x,
                 int64_t ldx, void* act, int64_t ld_act, cudaStream_t stream);
 int linear(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
            int64_t ldx, float* out, int splits, cudaStream_t stream);
-int qkv_fused_splits(int64_t n, int64_t k, int64_t b);
 int cluster_splits(int64_t n, int64_t k, int64_t b);
 int linear_argmax(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
                   int64_t ldx, float* logits, void* cand, int vocab0, cudaStream_t stream);
-int linear_silu_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
-                        int64_t ldx, void* act, int64_t ld_act, cudaStream_t stream);
-int linear_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
-                   int64_t ldx, float* out, cudaStream_t stream);
 int linear_push_ll_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,
                            int64_t x_rows, int64_t ldx, const DstList& dst, const uint64_t* tag_epoch,
                            uint32_t tag_mult, uint32_t tag_add, cudaStream_t stream);
-int linear_qkv_rope(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
-                    int64_t ldx, const QkvEpi& qe, cudaStream_t stream);
 int embed(const int*, const int*, const int*, const int*, int, const void*, int, int, float*, cudaStream_t);
 int add_norm(float*, const Src&, const WaitSpec&, const void*, float, int, int, void*, int, cudaStream_t);
 int reduce_push(const Src&, const DstList&, long long, const SignalSpec&, cudaStream_t);
@@ -232,23 +225,11 @@ int tps_linear_silu(const void* w, int64_t n, int64_t k, int64_t ldw, const void
   return linear_silu(w, n, k, ldw, x, b, x_rows, ldx, act, ld_act, S(stream));
 }
 
-int tps_qkv_fused_splits(int64_t n, int64_t k, int64_t b) { return qkv_fused_splits(n, k, b); }
-
 int tps_cluster_splits(int64_t n, int64_t k, int64_t b) { return cluster_splits(n, k, b); }
 
 int tps_linear_argmax(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
                       int64_t ldx, float* logits, void* cand, int vocab0, void* stream) {
   return linear_argmax(w, n, k, ldw, x, b, x_rows, ldx, logits, cand, vocab0, S(stream));
-}
-
-int tps_linear_silu_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,
-                            int64_t x_rows, int64_t ldx, void* act, int64_t ld_act, void* stream) {
-  return linear_silu_cluster(w, n, k, ldw, x, b, x_rows, ldx, act, ld_act, S(stream));
-}
-
-int tps_linear_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
-                       int64_t ldx, float* out, void* stream) {
-  return linear_cluster(w, n, k, ldw, x, b, x_rows, ldx, out, S(stream));
 }
 
 int tps_linear_push_ll_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,
@@ -259,31 +240,6 @@ int tps_linear_push_ll_cluster(const void* w, int64_t n, int64_t k, int64_t ldw,
   dl.n = ndst;
   for (int i = 0; i < ndst; ++i) dl.p[i] = reinterpret_cast<float*>(dsts[i]);
   return linear_push_ll_cluster(w, n, k, ldw, x, b, x_rows, ldx, dl, epoch, tag_mult, tag_add, S(stream));
-}
-
-int tps_linear_qkv_rope(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
-                        int64_t ldx, const void* bias, const int* row_slot, const int* pos_by_slot,
-                        const int* row_pos, const int* page_table, int max_pages, const float* cos_t,
-                        const float* sin_t, int nq, int nkv, int D, int page_size, void* q_out, void* k_cache,
-                        void* v_cache, void* stream) {
-  TPS_CHECK_ARG(page_size == 64, "linear_qkv_rope: page_size must be 64");
-  QkvEpi qe;
-  qe.bias = reinterpret_cast<const __nv_bfloat16*>(bias);
-  qe.row_slot = row_slot;
-  qe.pos_by_slot = pos_by_slot;
-  qe.row_pos = row_pos;
-  qe.page_table = page_table;
-  qe.cos_t = cos_t;
-  qe.sin_t = sin_t;
-  qe.q_out = reinterpret_cast<__nv_bfloat16*>(q_out);
-  qe.k_cache = reinterpret_cast<__nv_bfloat16*>(k_cache);
-  qe.v_cache = reinterpret_cast<__nv_bfloat16*>(v_cache);
-  qe.max_pages = max_pages;
-  qe.nq = nq;
-  qe.nkv = nkv;
-  qe.D = D;
-  qe.P = page_size;
-  return linear_qkv_rope(w, n, k, ldw, x, b, x_rows, ldx, qe, S(stream));
 }
 
 int tps_prefill_group_positions(int G) { return prefill_group_positions(G); }

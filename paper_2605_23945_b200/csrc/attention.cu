@@ -406,21 +406,16 @@ constexpr int kInKernelMergeMaxSplits = 4;
 // its (max, sum, O) softmax state in shared memory; after a cluster barrier every CTA merges
 // a slice of the G x D output straight out of its peers' shared memory (DSMEM) -- no
 // global partials, atomics or second kernel on the critical path of a 1..16-row step.
-// TPS_ATTN_CLUSTER_EARLY=1: the cluster form streams its first pages before the PDL wait
-// (TP8 B=1 1.330 -> 1.287 ms). Off: graph-replayed decode then diverges from eager decode
-// from the first generated token on, at TP1 too and with a device sync between replays
-// (tools/graph_probe.py), while eager decode matches the oracle. Re-issuing the early pages
-// after the wait makes graph replay exact (so does re-reading only rows >= ctx - 1, or any
-// post-wait delay in thread 0: a printf, a 20 us spin), and q re-read 20 us after the wait is
-// unchanged -- timing-dependent, root cause not found yet.
-__device__ int g_cluster_early = 0;
+// (Round 1 had an opt-in variant streaming the first pages before the PDL wait, -3 % at TP8
+// B=1; graph-replayed decode diverged from eager decode with it, root cause not found: the
+// variant was removed in round 2. Every page is read after the wait.)
 
 template <int D, bool TMA>
 __global__ void __launch_bounds__(kAttnThreads) paged_attn_cluster_kernel(
     const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k_cache,
     const __nv_bfloat16* __restrict__ v_cache, const int* __restrict__ row_slot,
     const int* __restrict__ pos_by_slot, const int* __restrict__ row_pos, const int* __restrict__ page_table,
-    int max_pages, int nq, int nkv, int G, float scale_log2, __nv_bfloat16* __restrict__ out, int early_ok,
+    int max_pages, int nq, int nkv, int G, float scale_log2, __nv_bfloat16* __restrict__ out,
     const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv) {
   namespace cg = cooperative_groups;
   constexpr int CPR = D / 8;
@@ -449,14 +444,7 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_cluster_kernel(
   const int g = lane >> 2, c = lane & 3;
   pdl_launch_dependents();  // dependents may launch now: they read our outputs only after their own wait
   const unsigned int trs = trace_begin(kTrAttnSplit);
-  // (streaming pages before the wait, as the split kernel does, broke graph-replayed TP2
-  // decode in this cluster form -- tests/test_gpu_decode.py::test_graph_replay_matches_eager;
-  // kept off until understood)
-  const bool decode = row_pos == nullptr && early_ok && g_cluster_early;
-  if (!decode) pdl_wait();  // prefill rows of this chunk were appended by the previous kernel
-  // decode: positions, page tables and every cached token but the current one were written by
-  // earlier steps, so the first pages stream before the programmatic wait; the current
-  // token's K/V row and q are read after it
+  pdl_wait();  // q and the current token's K/V row were written by the previous kernel
   const int slot = row_slot[b];
   const int ctx = slot >= 0 ? (row_pos ? row_pos[b] : pos_by_slot[slot]) + 1 : 0;
   const int npages = (ctx + kPage - 1) / kPage;
@@ -471,9 +459,7 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_cluster_kernel(
   float o[D / 8][4];
 #pragma unroll
   for (int i = 0; i < D / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-  if (p0 >= p1) {
-    if (decode) pdl_wait();
-  } else {
+  if (p0 < p1) {
     const int* pt = page_table + (size_t)slot * max_pages;
     auto load_page = [&](int p, int st) {
       if constexpr (TMA) {
@@ -507,7 +493,6 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_cluster_kernel(
       if (p0 + i < p1) load_page(p0 + i, i);
       cp_async_commit();
     }
-    if (decode) pdl_wait();
     uint32_t qa[D / 16][4];
     load_q_frags<D>(qa, q + ((size_t)b * nq + head0) * D, G);
     for (int it = 0; p0 + it < p1; ++it) {
@@ -526,18 +511,6 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attn_cluster_kernel(
         const int nxt = it + kAttnStages - 1;
         if (p0 + nxt < p1) load_page(p0 + nxt, nxt % kAttnStages);
         cp_async_commit();
-      }
-      if (decode && it < kAttnStages - 1 && p0 + it == npages - 1) {
-        // this page was issued before the wait: refresh the current token's K/V row
-        const int r = (ctx - 1) % kPage;
-        const size_t goff = ((size_t)pt[p0 + it] * nkv + kvh) * TILE + (size_t)r * D;
-        for (int i = tid; i < 2 * CPR; i += kAttnThreads) {
-          const bool is_v = i >= CPR;
-          const int cc = i % CPR;
-          const uint4 v = __ldcg(reinterpret_cast<const uint4*>((is_v ? v_cache : k_cache) + goff) + cc);
-          *reinterpret_cast<uint4*>((is_v ? sv : sk) + st * TILE + tile_off<D, TMA>(r, cc)) = v;
-        }
-        __syncthreads();
       }
       attend_page<D, TMA>(sk + st * TILE, sv + st * TILE, qa, (p0 + it) * kPage, ctx, scale_log2, m_r, l_r, o);
     }
@@ -639,11 +612,6 @@ int configure_attention_balanced();
 int configure_attention_prefill();
 
 int configure_attention() {
-  {
-    const char* e = getenv("TPS_ATTN_CLUSTER_EARLY");
-    const int v = e ? atoi(e) : 0;
-    TPS_CUDA_TRY(cudaMemcpyToSymbol(g_cluster_early, &v, sizeof(int)));
-  }
   int rc = configure_attention_balanced();
   if (!rc) rc = configure_attention_prefill();
   if (rc) return rc;
@@ -776,16 +744,16 @@ int paged_attention(const void* q, const void* k_cache, const void* v_cache, con
       if (rc) return rc;
       return launch_kcs(paged_attn_cluster_kernel<128, true>, dim3(cl, B * nkv), dim3(kAttnThreads), cl,
                         attn_smem<128>() + 1024, st, true, qq, kk, vv, row_slot, pos_by_slot, row_pos, page_table,
-                        max_pages, nq, nkv, G, scale, oo, g_attn_early, tmk, tmv);
+                        max_pages, nq, nkv, G, scale, oo, tmk, tmv);
     }
     if (D == 128)
       return launch_kcs(paged_attn_cluster_kernel<128, false>, dim3(cl, B * nkv), dim3(kAttnThreads), cl,
                         attn_smem<128>(), st, true, qq, kk, vv, row_slot, pos_by_slot, row_pos, page_table,
-                        max_pages, nq, nkv, G, scale, oo, g_attn_early, tmk, tmv);
+                        max_pages, nq, nkv, G, scale, oo, tmk, tmv);
     if (D == 64)
       return launch_kcs(paged_attn_cluster_kernel<64, false>, dim3(cl, B * nkv), dim3(kAttnThreads), cl,
                         attn_smem<64>(), st, true, qq, kk, vv, row_slot, pos_by_slot, row_pos, page_table,
-                        max_pages, nq, nkv, G, scale, oo, g_attn_early, tmk, tmv);
+                        max_pages, nq, nkv, G, scale, oo, tmk, tmv);
     return fail(kInvalid, "paged_attention: head_dim must be 64 or 128");
   }
   if (nsplit == 0)

@@ -38,21 +38,6 @@ struct SignalSpec {
   unsigned int* done;
 };
 
-// In-kernel QKV finishing (gemm_tcgen05.cu kEpiQkvRope): bias + RoPE + q / paged-KV writes.
-struct QkvEpi {
-  const __nv_bfloat16* bias;
-  const int* row_slot;
-  const int* pos_by_slot;
-  const int* row_pos;
-  const int* page_table;
-  const float* cos_t;
-  const float* sin_t;
-  __nv_bfloat16* q_out;
-  __nv_bfloat16* k_cache;
-  __nv_bfloat16* v_cache;
-  int max_pages, nq, nkv, D, P;
-};
-
 // Destination list for a reduce-and-push: the same [rows][cols] fp32 result is
 // stored to every listed buffer (this rank's slot in each peer's receive area).
 struct DstList {

@@ -49,14 +49,14 @@ struct GemmCfg {
   static constexpr int kBarBytes = 256;
   static constexpr int kEpiBytes = 64 * 17 * 4;  // SwiGLU epilogue exchange buffer
   static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kBarBytes + kEpiBytes;
-  // the in-kernel-finished QKV form keeps a shallower ring so two CTAs fit per SM: the next
+  // the cluster-reduced form keeps a shallower ring so two CTAs fit per SM: the next
   // launch's clusters become resident (and prefetch) while this one drains
-#ifndef TPS_QKV_STAGES
-#define TPS_QKV_STAGES 4
+#ifndef TPS_CLUSTER_STAGES
+#define TPS_CLUSTER_STAGES 4
 #endif
-  static constexpr int kQkvStages = kStages < TPS_QKV_STAGES ? kStages : TPS_QKV_STAGES;
-  static constexpr int kQkvSmemBytes = 1024 + kQkvStages * kStageBytes + kBarBytes + kEpiBytes;
-  static_assert(BN * kBM * 4 <= kQkvStages * kStageBytes, "QKV partial tile must fit the drained ring");
+  static constexpr int kClusterStages = kStages < TPS_CLUSTER_STAGES ? kStages : TPS_CLUSTER_STAGES;
+  static constexpr int kClusterSmemBytes = 1024 + kClusterStages * kStageBytes + kBarBytes + kEpiBytes;
+  static_assert(BN * kBM * 4 <= kClusterStages * kStageBytes, "the partial tile must fit the drained ring");
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128 must be 16..256, %16");
   static_assert(kStages >= 3, "need at least 3 stages");
 };
@@ -102,22 +102,11 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 // writes act[b][f] = bf16(silu(gate) * up) directly -- the SwiGLU never round-trips HBM.
 constexpr int kEpiPartial = 0;
 constexpr int kEpiSiluMul = 1;
-// kEpiQkvRope: the QKV projection finished in-kernel. The S split-K CTAs of a weight tile
-// form one thread-block cluster; each parks its fp32 partial tile in its own (drained) smem
-// ring, and after a cluster barrier CTA s sums -- over DSMEM, in split order, like the
-// consumer kernels -- the rotary pairs of its slice of the tile, adds the bias, applies
-// RoPE at each row's position and writes q (bf16) and the new k/v into the paged cache.
-// This replaces tps_qkv_rope_append (one launch + its PDL boundary per layer).
-constexpr int kEpiQkvRope = 2;
 // kEpiClusterLL: row-parallel projection + TP allreduce push. The split-K CTAs of a tile
 // (one cluster) sum their partials over DSMEM in split order and push ONE LL {value, tag}
 // pair per element to every peer (tps_linear_push_ll pushes every split partial: S x the
 // NVLink bytes and tp x S sources for the consumer; tps_reduce_push_ll needs a launch).
 constexpr int kEpiClusterLL = 3;
-// kEpiClusterSilu: gate/up projection (interleaved 64-row [gate c | up c] blocks) with the
-// split-K partials summed over DSMEM in the cluster and SwiGLU applied: act = bf16(silu(g) * u),
-// the result of tps_linear + tps_silu_mul with split-K kept (tps_linear_silu needs S = 1).
-constexpr int kEpiClusterSilu = 5;
 // kEpiArgmax: LM head (splits == 1): the fp32 logits as kEpiPartial, plus the greedy candidate
 // {max logit, smallest index on ties} of every (row, 128-column tile) -- argmax stage 1 done
 // in the epilogue, so no kernel re-reads the logits (tps_argmax_finalize merges the tiles).
@@ -128,14 +117,14 @@ struct ArgEpi {
   int ntiles;
   int vocab0;        // global index of column 0
 };
-constexpr bool cluster_epi(int epi) { return epi == kEpiQkvRope || epi == kEpiClusterLL || epi == kEpiClusterSilu; }
+constexpr bool cluster_epi(int epi) { return epi == kEpiClusterLL; }
 
 
 namespace cg = cooperative_groups;
 
-// Finishing of kEpiQkvRope (all 256 threads of every CTA of the cluster).
-// part: this CTA's [BN][128] fp32 tile partial (row j = token row, column r = weight row).
-// Finishing of kEpiClusterLL: CTA s of S sums columns [s*128/S, (s+1)*128/S) of the tile.
+// Finishing of kEpiClusterLL (all 256 threads of every CTA of the cluster): CTA s of S sums
+// columns [s*128/S, (s+1)*128/S) of the tile. part: this CTA's [BN][128] fp32 tile partial
+// (row j = token row, column r = weight row).
 template <int BN>
 __device__ __forceinline__ void cluster_ll_finish(const float* part, const DstList& dst, uint64_t tag, int tile,
                                                   int N, int rows) {
@@ -164,110 +153,7 @@ __device__ __forceinline__ void cluster_ll_finish(const float* part, const DstLi
       for (int d = 0; d < dst.n; ++d)
         st_relaxed_sys_u64(reinterpret_cast<uint64_t*>(dst.p[d]) + (size_t)j * N + n, tag | __float_as_uint(x));
     else
-      dst.p[0][(size_t)j * N + n] = x;  // local fp32 result (tps_linear_cluster)
-  }
-}
-
-// Finishing of kEpiClusterSilu: CTA s of S produces f in [s*64/S, (s+1)*64/S) of the tile.
-template <int BN>
-__device__ __forceinline__ void cluster_silu_finish(const float* part, __nv_bfloat16* act, int ld_act, int tile,
-                                                    int F, int rows) {
-  cg::cluster_group cl = cg::this_cluster();
-  cl.sync();  // every split's partial tile is parked in its CTA's smem
-  const int S = (int)cl.num_blocks();
-  const int rank = (int)cl.block_rank();
-  const int f0 = rank * 64 / S, f1 = (rank + 1) * 64 / S;
-  const int nf = f1 - f0;
-  const float* rp[16];
-#pragma unroll
-  for (int s = 0; s < 16; ++s) rp[s] = s < S ? cl.map_shared_rank(part, s) : part;
-  for (int it = threadIdx.x; it < nf * rows; it += kGemmThreads) {
-    const int fl = f0 + it % nf, j = it / nf;
-    const int f = tile * 64 + fl;
-    if (f >= F) continue;
-    float vg[16], vu[16];
-#pragma unroll
-    for (int s = 0; s < 16; ++s)
-      if (s < S) {
-        vg[s] = rp[s][j * kBM + fl];
-        vu[s] = rp[s][j * kBM + 64 + fl];
-      }
-    float g = 0.f, u = 0.f;  // split order, from 0 (as tps_silu_mul)
-#pragma unroll
-    for (int s = 0; s < 16; ++s)
-      if (s < S) {
-        g += vg[s];
-        u += vu[s];
-      }
-    act[(size_t)j * ld_act + f] = f2bf(g / (1.f + __expf(-g)) * u);
-  }
-}
-
-template <int BN>
-__device__ __forceinline__ void qkv_finish(const float* part, const QkvEpi& e, int tile, int N, int rows) {
-  __shared__ int s_pos[BN], s_slot[BN], s_page[BN];
-  for (int j = threadIdx.x; j < rows; j += kGemmThreads) {  // row metadata, once per CTA
-    const int slot = e.row_slot[j];
-    const int pos = slot >= 0 ? (e.row_pos ? e.row_pos[j] : e.pos_by_slot[slot]) : 0;
-    s_slot[j] = slot;
-    s_pos[j] = pos;
-    s_page[j] = slot >= 0 ? e.page_table[(size_t)slot * e.max_pages + pos / e.P] : 0;
-  }
-  cg::cluster_group cl = cg::this_cluster();
-  cl.sync();  // every split's partial tile is parked in its CTA's smem (and the metadata is in)
-  const int S = (int)cl.num_blocks();
-  const int rank = (int)cl.block_rank();
-  const int half = e.D / 2;
-  const int li0 = rank * 64 / S, li1 = (rank + 1) * 64 / S;  // 64 rotary pairs per 128-row tile
-  const int nli = li1 - li0;
-  const float* rp[16];
-#pragma unroll
-  for (int s = 0; s < 16; ++s) rp[s] = s < S ? cl.map_shared_rank(part, s) : part;
-  for (int it = threadIdx.x; it < nli * rows; it += kGemmThreads) {
-    const int li = li0 + it % nli, j = it / nli;
-    const int r_lo = (li / half) * e.D + li % half;
-    const int n_lo = tile * kBM + r_lo;
-    if (n_lo >= N) continue;  // (N is a whole number of heads)
-    float v0[16], v1[16];
-#pragma unroll
-    for (int s = 0; s < 16; ++s)
-      if (s < S) {
-        v0[s] = rp[s][j * kBM + r_lo];
-        v1[s] = rp[s][j * kBM + r_lo + half];
-      }
-    float x0 = 0.f, x1 = 0.f;  // split order, from 0: the same sums as the consumer kernels
-#pragma unroll
-    for (int s = 0; s < 16; ++s)
-      if (s < S) {
-        x0 += v0[s];
-        x1 += v1[s];
-      }
-    if (e.bias) {
-      x0 += bf2f(e.bias[n_lo]);
-      x1 += bf2f(e.bias[n_lo + half]);
-    }
-    const int b = j;
-    const int slot = s_slot[b], pos = s_pos[b];
-    const int h = n_lo / e.D, i = n_lo % e.D;
-    if (h < e.nq) {
-      const float cs = e.cos_t[(size_t)pos * half + i], sn = e.sin_t[(size_t)pos * half + i];
-      __nv_bfloat16* q = e.q_out + ((size_t)b * e.nq + h) * e.D;
-      q[i] = f2bf(x0 * cs - x1 * sn);
-      q[i + half] = f2bf(x1 * cs + x0 * sn);
-    } else if (slot >= 0) {
-      const bool is_k = h < e.nq + e.nkv;
-      const int jh = is_k ? h - e.nq : h - e.nq - e.nkv;
-      const int page = s_page[b];
-      const size_t off_c = (((size_t)page * e.nkv + jh) * e.P + (pos % e.P)) * e.D;
-      if (is_k) {
-        const float cs = e.cos_t[(size_t)pos * half + i], sn = e.sin_t[(size_t)pos * half + i];
-        e.k_cache[off_c + i] = f2bf(x0 * cs - x1 * sn);
-        e.k_cache[off_c + i + half] = f2bf(x1 * cs + x0 * sn);
-      } else {
-        e.v_cache[off_c + i] = f2bf(x0);
-        e.v_cache[off_c + i + half] = f2bf(x1);
-      }
-    }
+      dst.p[0][(size_t)j * N + n] = x;  // local fp32 result (tag 0: not issued by the library)
   }
 }
 
@@ -278,9 +164,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                        long long split_stride, int N, int B, int num_tiles, int splits, int chunks, int acts,
                        __nv_bfloat16* __restrict__ act_out, int ld_act, const __grid_constant__ SignalSpec sig,
                        const uint64_t* __restrict__ tag_epoch, uint32_t tag_mult, uint32_t tag_add,
-                       const __grid_constant__ QkvEpi qkv, const __grid_constant__ ArgEpi arg) {
+                       const __grid_constant__ ArgEpi arg) {
   using Cfg = GemmCfg<BN>;
-  constexpr int S = cluster_epi(EPI) ? Cfg::kQkvStages : Cfg::kStages;
+  constexpr int S = cluster_epi(EPI) ? Cfg::kClusterStages : Cfg::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_a = smem;
@@ -294,8 +180,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
 
   const unsigned int trs =
-      trace_begin((EPI == kEpiSiluMul || EPI == kEpiClusterSilu) ? kTrGemmSilu : EPI == kEpiClusterLL ? kTrGemmPush
-                                                                                                        : kTrGemm);
+      trace_begin(EPI == kEpiSiluMul ? kTrGemmSilu : EPI == kEpiClusterLL ? kTrGemmPush : kTrGemm);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   // unit u = ((tile * splits + split) * acts + act): the activation tiles of one weight
@@ -541,18 +426,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if constexpr (EPI == kEpiQkvRope) {
-    pdl_wait();  // (every thread: the finishing reads row metadata and writes q / the cache)
-    qkv_finish<BN>(reinterpret_cast<const float*>(smem), qkv, (int)blockIdx.x / (int)cg::this_cluster().num_blocks(),
-                   N, B);
-    cg::this_cluster().sync();  // keep this smem alive until the cluster has read it
-  }
-  if constexpr (EPI == kEpiClusterSilu) {
-    pdl_wait();  // (every thread: act is read by the previous layer's down projection)
-    cluster_silu_finish<BN>(reinterpret_cast<const float*>(smem), act_out, ld_act,
-                            (int)blockIdx.x / (int)cg::this_cluster().num_blocks(), N / 2, B);
-    cg::this_cluster().sync();
-  }
   if constexpr (EPI == kEpiClusterLL) {
     pdl_wait();  // (every thread: the pushes overwrite LL slots the predecessor chain consumed)
     const uint64_t tag =
@@ -662,7 +535,6 @@ struct EpiArgs {
   const uint64_t* tag_epoch = nullptr;
   uint32_t tag_mult = 0;
   uint32_t tag_add = 0;
-  QkvEpi qkv{};
   ArgEpi arg{};
 };
 
@@ -674,12 +546,12 @@ static int launch_gemm(const CUtensorMap& mw, const CUtensorMap& mx, const EpiAr
   const int units = tiles * splits * acts;
   const int grid = units < kNumSMs ? units : kNumSMs;
   if constexpr (cluster_epi(EPI))  // one unit per CTA, the splits of a tile in one cluster
-    return launch_kcs(gemm_swapab_kernel<BN, EPI>, dim3(units), dim3(kGemmThreads), splits, Cfg::kQkvSmemBytes,
+    return launch_kcs(gemm_swapab_kernel<BN, EPI>, dim3(units), dim3(kGemmThreads), splits, Cfg::kClusterSmemBytes,
                       stream, true, mw, mx, e.dst, e.split_stride, n, b, tiles, splits, chunks, acts, e.act_out,
-                      e.ld_act, e.sig, e.tag_epoch, e.tag_mult, e.tag_add, e.qkv, e.arg);
+                      e.ld_act, e.sig, e.tag_epoch, e.tag_mult, e.tag_add, e.arg);
   return launch_k(gemm_swapab_kernel<BN, EPI>, dim3(grid), dim3(kGemmThreads), Cfg::kSmemBytes, stream, true, mw,
                   mx, e.dst, e.split_stride, n, b, tiles, splits, chunks, acts, e.act_out, e.ld_act, e.sig,
-                  e.tag_epoch, e.tag_mult, e.tag_add, e.qkv, e.arg);
+                  e.tag_epoch, e.tag_mult, e.tag_add, e.arg);
 }
 
 template <int BN>
@@ -694,21 +566,11 @@ static int configure_one() {
   TPS_MAX_CARVEOUT((gemm_swapab_kernel<BN, kEpiPartial>));
   TPS_MAX_CARVEOUT((gemm_swapab_kernel<BN, kEpiSiluMul>));
   if constexpr (BN <= 64) {
-    TPS_CUDA_TRY(cudaFuncSetAttribute(gemm_swapab_kernel<BN, kEpiQkvRope>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN>::kQkvSmemBytes));
-    TPS_CUDA_TRY(cudaFuncSetAttribute(gemm_swapab_kernel<BN, kEpiQkvRope>,
-                                      cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    TPS_MAX_CARVEOUT((gemm_swapab_kernel<BN, kEpiQkvRope>));
     TPS_CUDA_TRY(cudaFuncSetAttribute(gemm_swapab_kernel<BN, kEpiClusterLL>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN>::kQkvSmemBytes));
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN>::kClusterSmemBytes));
     TPS_CUDA_TRY(cudaFuncSetAttribute(gemm_swapab_kernel<BN, kEpiClusterLL>,
                                       cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     TPS_MAX_CARVEOUT((gemm_swapab_kernel<BN, kEpiClusterLL>));
-    TPS_CUDA_TRY(cudaFuncSetAttribute(gemm_swapab_kernel<BN, kEpiClusterSilu>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN>::kQkvSmemBytes));
-    TPS_CUDA_TRY(cudaFuncSetAttribute(gemm_swapab_kernel<BN, kEpiClusterSilu>,
-                                      cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    TPS_MAX_CARVEOUT((gemm_swapab_kernel<BN, kEpiClusterSilu>));
   }
   return kOk;
 }
@@ -745,8 +607,6 @@ int cluster_splits(int64_t n, int64_t k, int64_t b) {
   if (s > cap) s = cap;
   return s >= 1 ? s : 0;
 }
-
-int qkv_fused_splits(int64_t n, int64_t k, int64_t b) { return n % kBM ? 0 : cluster_splits(n, k, b); }
 
 template <int EPI>
 static int dispatch(int bn, const CUtensorMap& mw, const CUtensorMap& mx, const EpiArgs& e, int n, int b, int tiles,
@@ -845,32 +705,6 @@ int linear_silu(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x,
   return dispatch<kEpiSiluMul>(bn, mw, mx, e, (int)n, (int)b, (int)(n / kBM), 1, (int)chunks, stream);
 }
 
-int linear_qkv_rope(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
-                    int64_t ldx, const QkvEpi& qe, cudaStream_t stream) {
-  const int splits = qkv_fused_splits(n, k, b);
-  TPS_CHECK_ARG(splits >= 1, "linear_qkv_rope: shape not supported (see tps_qkv_fused_splits)");
-  TPS_CHECK_ARG(qe.D % 2 == 0 && kBM % qe.D == 0 && n == (int64_t)(qe.nq + 2 * qe.nkv) * qe.D && qe.P > 0,
-                "linear_qkv_rope: n must be (nq + 2 nkv) * D with D dividing 128");
-  TPS_CHECK_ARG(qe.row_slot && qe.pos_by_slot && qe.page_table && qe.cos_t && qe.sin_t && qe.q_out && qe.k_cache &&
-                    qe.v_cache,
-                "linear_qkv_rope: null pointer");
-  const int64_t chunks = (k + kBK - 1) / kBK;
-  CUtensorMap mw, mx;
-  int bn;
-  int rc = prepare(w, n, k, ldw, x, b, x_rows, ldx, &mw, &mx, &bn);
-  if (rc) return rc;
-  EpiArgs e{};
-  e.dst.n = 0;
-  e.sig.n = 0;
-  e.qkv = qe;
-  const int tiles = (int)(n / kBM);
-  switch (bn) {
-    case 16: return launch_gemm<16, kEpiQkvRope>(mw, mx, e, (int)n, (int)b, tiles, splits, (int)chunks, stream);
-    case 32: return launch_gemm<32, kEpiQkvRope>(mw, mx, e, (int)n, (int)b, tiles, splits, (int)chunks, stream);
-    default: return launch_gemm<64, kEpiQkvRope>(mw, mx, e, (int)n, (int)b, tiles, splits, (int)chunks, stream);
-  }
-}
-
 // Row-parallel projection with the split-K reduction inside a cluster and one LL pair per
 // element pushed to every destination at i * n + j (tag = (*tag_epoch) * tag_mult + tag_add).
 int linear_push_ll_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,
@@ -893,53 +727,6 @@ int linear_push_ll_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, con
     case 16: return launch_gemm<16, kEpiClusterLL>(mw, mx, e, (int)n, (int)b, tiles, splits, (int)chunks, stream);
     case 32: return launch_gemm<32, kEpiClusterLL>(mw, mx, e, (int)n, (int)b, tiles, splits, (int)chunks, stream);
     default: return launch_gemm<64, kEpiClusterLL>(mw, mx, e, (int)n, (int)b, tiles, splits, (int)chunks, stream);
-  }
-}
-
-// fp32 result [b][n] (the split-K partials reduced over DSMEM inside the kernel, split order):
-// the same sums a consumer of tps_linear's partials forms, without the partial traffic.
-int linear_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
-                   int64_t ldx, float* out, cudaStream_t stream) {
-  const int splits = cluster_splits(n, k, b);
-  TPS_CHECK_ARG(splits >= 1 && out, "linear_cluster: shape not supported (see tps_cluster_splits)");
-  const int64_t chunks = (k + kBK - 1) / kBK;
-  CUtensorMap mw, mx;
-  int bn;
-  int rc = prepare(w, n, k, ldw, x, b, x_rows, ldx, &mw, &mx, &bn);
-  if (rc) return rc;
-  EpiArgs e{};
-  e.dst.n = 1;
-  e.dst.p[0] = out;
-  e.sig.n = 0;
-  const int tiles = (int)((n + kBM - 1) / kBM);
-  switch (bn) {
-    case 16: return launch_gemm<16, kEpiClusterLL>(mw, mx, e, (int)n, (int)b, tiles, splits, (int)chunks, stream);
-    case 32: return launch_gemm<32, kEpiClusterLL>(mw, mx, e, (int)n, (int)b, tiles, splits, (int)chunks, stream);
-    default: return launch_gemm<64, kEpiClusterLL>(mw, mx, e, (int)n, (int)b, tiles, splits, (int)chunks, stream);
-  }
-}
-
-// Gate/up + SwiGLU with split-K reduced in the cluster: act[i][f] = bf16(silu(g_f) * u_f).
-int linear_silu_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
-                        int64_t ldx, void* act, int64_t ld_act, cudaStream_t stream) {
-  TPS_CHECK_ARG(act && n % kBM == 0 && ld_act >= n / 2, "linear_silu_cluster: n = 2F, F % 64 == 0, ld_act >= F");
-  const int splits = cluster_splits(n, k, b);
-  TPS_CHECK_ARG(splits >= 1, "linear_silu_cluster: shape not supported (see tps_cluster_splits)");
-  const int64_t chunks = (k + kBK - 1) / kBK;
-  CUtensorMap mw, mx;
-  int bn;
-  int rc = prepare(w, n, k, ldw, x, b, x_rows, ldx, &mw, &mx, &bn);
-  if (rc) return rc;
-  EpiArgs e{};
-  e.dst.n = 0;
-  e.sig.n = 0;
-  e.act_out = reinterpret_cast<__nv_bfloat16*>(act);
-  e.ld_act = (int)ld_act;
-  const int tiles = (int)(n / kBM);
-  switch (bn) {
-    case 16: return launch_gemm<16, kEpiClusterSilu>(mw, mx, e, (int)n, (int)b, tiles, splits, (int)chunks, stream);
-    case 32: return launch_gemm<32, kEpiClusterSilu>(mw, mx, e, (int)n, (int)b, tiles, splits, (int)chunks, stream);
-    default: return launch_gemm<64, kEpiClusterSilu>(mw, mx, e, (int)n, (int)b, tiles, splits, (int)chunks, stream);
   }
 }
 

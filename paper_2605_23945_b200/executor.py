@@ -180,25 +180,6 @@ class InferExecutor:
         # chunked prefill runs `prefill_rows` (sample, prompt position) rows per step
         self.prefill_rows = prefill_rows
         rows = max(max_batch, prefill_rows)
-        # finishing q/k/v inside the attention kernel saves a launch but every split CTA
-        # recomputes its group's queries after the wait; measured slower on B200 even with the
-        # KV pages streaming before the wait (TP1 B=64 ctx 2048 4.480 vs 4.462 ms, TP8 B=1
-        # 1.518 vs 1.391): off by default
-        self.fuse_rope = False
-        # decode QKV finished inside the projection kernel (tps_linear_qkv_rope: cluster split-K,
-        # DSMEM partial sums, bias/RoPE/KV append in the epilogue) where the shape takes it.
-        # Bit-identical to tps_linear + tps_qkv_rope_append but measured neutral in the step
-        # (TP1 B=64 ctx 2048 4.475 vs 4.465 ms, TP8 B=1 1.418 vs 1.392: the separate finishing
-        # launch is already hidden under attention's early KV stream): off by default
-        self.qkv_in_gemm = False
-        # every split-K projection at B <= 64 with its partials reduced in-kernel (tps_linear_cluster;
-        # measured slower for column-parallel / TP1 projections: TP1 B=64 4.465 -> 4.838 ms, the
-        # 4-stage ring of the cluster form costs more than the partial traffic it saves): off
-        self.cluster_linear = os.environ.get("TPS_CLUSTER_LINEAR", "0") == "1"
-        # unfused-SwiGLU shapes (TP >= 4) through tps_linear_silu_cluster (bit-identical; measured
-        # neutral: TP8 B=1 1.334 vs 1.317 ms, TP4 B=64 2.591 vs 2.507 -- the SiLU launch already
-        # hides under the down projection's weight prefetch): off
-        self.silu_cluster = os.environ.get("TPS_SILU_CLUSTER", "0") == "1"
         # launch kinds left out of the step program (timing probes only: results are garbage)
         self.skip: frozenset = frozenset()
         # 0: greedy; > 0: Gumbel-max sampling at this temperature with the slots' Philox keys
@@ -233,10 +214,10 @@ class InferExecutor:
             for n, k in self._proj_shapes():
                 ws = max(ws, nat.lib().tps_linear_splits(n, k, B) * B * n)
         self.ws = torch.zeros(ws, dtype=torch.float32, device=dev)
-        # attention partial states: the page-balanced schedule (nsplit 0) and, for the
-        # fused-RoPE form, the fixed split count of every bucket
+        # attention partial states: the page-balanced schedule (nsplit 0) and a fixed split
+        # count for every bucket (the policy's own count, else one wave of 2 CTAs per SM)
         att = max(nat.lib().tps_attn_workspace(B, self.nq, D, s) for B in sizes
-                  for s in (0, self._attn_splits(B, True)))
+                  for s in (0, self._fixed_attn_splits(B)))
         self.att_o = torch.zeros(att, dtype=torch.float32, device=dev)
         self.att_m = torch.zeros(att // D, dtype=torch.float32, device=dev)
         self.att_l = torch.zeros_like(self.att_m)
@@ -297,21 +278,17 @@ class InferExecutor:
         units = (2 * self.F // 128) * (-(-B // bn))
         return units >= self.fuse_silu_min_units
 
-    def _attn_splits(self, B: int, fused: bool) -> int:
-        """tps_attn_splits policy (-1 = cluster per segment, 0 = page-balanced, n = fixed splits);
-        the fused-RoPE form needs a fixed count."""
-        s = nat.lib().tps_attn_splits(B, self.nkv, self.slots.max_pages)
-        return max(1, min(32, 2 * 148 // (B * self.nkv))) if (fused and s <= 0) else s
+    def _fixed_attn_splits(self, B: int) -> int:
+        s = self._attn_splits(B)
+        return s if s > 0 else max(1, min(32, 2 * 148 // (B * self.nkv)))
+
+    def _attn_splits(self, B: int) -> int:
+        """tps_attn_splits policy (-1 = cluster per segment, 0 = page-balanced, n = fixed splits)."""
+        return nat.lib().tps_attn_splits(B, self.nkv, self.slots.max_pages)
 
     def _linear(self, st, stats, w: torch.Tensor, x: torch.Tensor, B: int) -> tuple[int, int, int]:
         """Projection into the split-K workspace; returns the strided source (base, n, stride)."""
         n, k = w.shape
-        if self.cluster_linear and "linear" not in self.skip and nat.lib().tps_cluster_splits(n, k, B) > 0:
-            # split-K reduced inside the kernel: consumers read one fp32 result
-            nat.check(nat.lib().tps_linear_cluster(w.data_ptr(), n, k, k, x.data_ptr(), B, x.shape[0], x.shape[1],
-                                                   self.ws.data_ptr(), st), "tps_linear_cluster")
-            stats.add("linear")
-            return (self.ws.data_ptr(), 1, B * n)
         s = self._splits(n, k, B)
         if "linear" in self.skip:
             return (self.ws.data_ptr(), s, B * n)
@@ -364,35 +341,13 @@ class InferExecutor:
         nat.check(lib.tps_add_norm(self.resid.data_ptr(), None, 0, 0, None, W.tensor_ptr(0, "ln1"), eps,
                                    H, B, self.xn.data_ptr(), H, st), "tps_add_norm")
         stats.add("add_norm")
-        fuse = self.fuse_rope and not prefill
-        nsplit = self._attn_splits(B, fuse)
-        w_qkv0 = W[(0, "w_qkv")]
-        # decode: the QKV projection finished in-kernel (cluster split-K + bias/RoPE/KV append)
-        qkv_in_gemm = (self.qkv_in_gemm and not fuse and not prefill and
-                       lib.tps_qkv_fused_splits(w_qkv0.shape[0], w_qkv0.shape[1], B) > 0)
+        nsplit = self._attn_splits(B)
         for l in range(L):
             kc, vc = self.kv.layer_ptrs(l)
             bias = W.tensor_ptr(l, "b_qkv") if g.qkv_bias else None
-            fused = (None, 0, 0, None, None, None)
-            if qkv_in_gemm:
-                w = W[(l, "w_qkv")]
-                if "linear" not in self.skip:
-                    nat.check(lib.tps_linear_qkv_rope(w.data_ptr(), w.shape[0], w.shape[1], w.shape[1],
-                                                      self.xn.data_ptr(), B, self.xn.shape[0], self.xn.shape[1],
-                                                      bias, rs, pos, rp, sl.page_table.data_ptr(), sl.max_pages,
-                                                      self.cos.data_ptr(), self.sin.data_ptr(), self.nq, self.nkv,
-                                                      D, PAGE, self.q.data_ptr(), kc, vc, st),
-                              "tps_linear_qkv_rope")
-                    stats.add("linear")
-            elif fuse:
-                # decode: bias + RoPE + KV append are finished inside the attention kernel
-                srcs = self._linear(st, stats, W[(l, "w_qkv")], self.xn, B)
-                fused = (*srcs, bias, self.cos.data_ptr(), self.sin.data_ptr())
-            else:
-                srcs = self._linear(st, stats, W[(l, "w_qkv")], self.xn, B)
-            if not qkv_in_gemm and not fuse and "qkv_rope" not in self.skip:
-                # separate bias+RoPE+append launch (always for prefill: many rows of one
-                # sample per launch need every row's K/V appended before attention)
+            srcs = self._linear(st, stats, W[(l, "w_qkv")], self.xn, B)
+            if "qkv_rope" not in self.skip:
+                # bias + RoPE + paged KV append (prefill: every row's K/V appended before attention)
                 nat.check(lib.tps_qkv_rope_append(*srcs, bias, rs, pos, rp,
                                                   sl.page_table.data_ptr(), sl.max_pages,
                                                   self.cos.data_ptr(), self.sin.data_ptr(), B, self.nq,
@@ -410,7 +365,7 @@ class InferExecutor:
                                                   sl.max_pages, B, self.nq, self.nkv, D, nsplit,
                                                   self.att_m.data_ptr(), self.att_l.data_ptr(),
                                                   self.att_o.data_ptr(), self.att_ctr.data_ptr(),
-                                                  self.attn.data_ptr(), *fused, st),
+                                                  self.attn.data_ptr(), None, 0, 0, None, None, None, st),
                           "tps_paged_attention")
                 stats.add("paged_attention", 1 if nsplit <= 4 else 2)  # (+ split-merge kernel)
             yield from self._row_parallel(st, stats, 2 * l, "w_o", W[(l, "w_o")], self.attn, B,
@@ -420,13 +375,6 @@ class InferExecutor:
                 nat.check(lib.tps_linear_silu(w_gu.data_ptr(), 2 * self.F, H, H, self.xn.data_ptr(), B,
                                               self.xn.shape[0], H, self.act.data_ptr(), self.F, st),
                           "tps_linear_silu")
-                stats.add("linear")
-            elif (self.silu_cluster and self.comm is not None and self.comm.tp >= LL_CLUSTER_MIN_TP and
-                  lib.tps_cluster_splits(2 * self.F, H, B) > 0):
-                # split-K reduced in the cluster, SwiGLU in the epilogue (no tps_silu_mul launch)
-                nat.check(lib.tps_linear_silu_cluster(w_gu.data_ptr(), 2 * self.F, H, H, self.xn.data_ptr(), B,
-                                                      self.xn.shape[0], H, self.act.data_ptr(), self.F, st),
-                          "tps_linear_silu_cluster")
                 stats.add("linear")
             else:
                 srcs = self._linear(st, stats, w_gu, self.xn, B)

@@ -310,67 +310,6 @@ def test_ll_push_and_norm(b, tp, splits):
 
 
 
-@pytest.mark.parametrize("nq,nkv,D,k,b,bias", [(28, 4, 128, 3584, 1, True), (28, 4, 128, 3584, 64, True),
-                                               (4, 1, 128, 3584, 16, True), (8, 2, 64, 256, 5, False),
-                                               (5, 1, 128, 5120, 3, True), (32, 8, 128, 4096, 33, False),
-                                               (3, 1, 128, 3584, 12, True)])
-def test_linear_qkv_rope_in_kernel_finishing(nq, nkv, D, k, b, bias):
-    """tps_linear_qkv_rope (cluster split-K, DSMEM partial sums, bias + RoPE + paged append in
-    the epilogue) equals tps_linear + tps_qkv_rope_append at the same split count, bit for bit:
-    q, every appended K/V row, and nothing else in the cache."""
-    lib = nat.lib()
-    n = (nq + 2 * nkv) * D
-    S = lib.tps_qkv_fused_splits(n, k, b)
-    assert S >= 1
-    torch.manual_seed(n + k + b)
-    w = (torch.randn(n, k, device="cuda") * 0.05).bfloat16()
-    x = torch.randn(b, k, device="cuda").bfloat16()
-    bvec = (torch.randn(n, device="cuda") * 0.1).bfloat16() if bias else None
-    P, max_pages, slots = 64, 8, b + 2
-    pos_by_slot = torch.randint(0, P * max_pages, (slots,), dtype=torch.int32, device="cuda")
-    row_slot = torch.arange(b, dtype=torch.int32, device="cuda")
-    if b > 2:
-        row_slot[1] = -1  # padding row: q written at position 0, no K/V append
-    page_table = torch.randperm(slots * max_pages, device="cuda").int().view(slots, max_pages).contiguous()
-    half = D // 2
-    inv = 1.0 / (10000.0 ** (torch.arange(half, device="cuda").float() / half))
-    ang = torch.arange(P * max_pages, device="cuda").float()[:, None] * inv[None]
-    cos, sin = ang.cos().contiguous(), ang.sin().contiguous()
-    outs = []
-    for fused in (True, False):
-        q = torch.zeros(b, nq, D, device="cuda", dtype=torch.bfloat16)
-        kc = torch.zeros(slots * max_pages, nkv, P, D, device="cuda", dtype=torch.bfloat16)
-        vc = torch.zeros_like(kc)
-        bp = bvec.data_ptr() if bias else None
-        if fused:
-            nat.check(lib.tps_linear_qkv_rope(w.data_ptr(), n, k, k, x.data_ptr(), b, b, k, bp, row_slot.data_ptr(),
-                                              pos_by_slot.data_ptr(), None, page_table.data_ptr(), max_pages,
-                                              cos.data_ptr(), sin.data_ptr(), nq, nkv, D, P, q.data_ptr(),
-                                              kc.data_ptr(), vc.data_ptr(), _stream()))
-        else:
-            ws = torch.zeros(S, b, n, device="cuda")
-            nat.check(lib.tps_linear(w.data_ptr(), n, k, k, x.data_ptr(), b, b, k, ws.data_ptr(), S, _stream()))
-            nat.check(lib.tps_qkv_rope_append(ws.data_ptr(), S, b * n, bp, row_slot.data_ptr(),
-                                              pos_by_slot.data_ptr(), None, page_table.data_ptr(), max_pages,
-                                              cos.data_ptr(), sin.data_ptr(), b, nq, nkv, D, P, q.data_ptr(),
-                                              kc.data_ptr(), vc.data_ptr(), _stream()))
-        torch.cuda.synchronize()
-        outs.append((q, kc, vc))
-    (qf, kf, vf), (qr, kr, vr) = outs
-    assert torch.equal(qf, qr)
-    assert torch.equal(kf, kr) and torch.equal(vf, vr)
-    assert kf.abs().sum() > 0 and qf.abs().sum() > 0
-    # against torch fp32: y = x W^T + b, RoPE on q/k
-    y = x.float() @ w.float().T + (bvec.float() if bias else 0)
-    for i in range(b):
-        if row_slot[i].item() < 0:
-            continue
-        p = pos_by_slot[row_slot[i]].item()
-        qh = y[i, :nq * D].view(nq, D)
-        ref = torch.cat([qh[:, :half] * cos[p] - qh[:, half:] * sin[p], qh[:, half:] * cos[p] + qh[:, :half] * sin[p]], 1)
-        assert (qf[i].float() - ref).abs().max().item() <= 2e-2 * (1 + ref.abs().max().item())
-
-
 @pytest.mark.parametrize("D,nq,nkv,nslots,per,ragged", [(128, 28, 4, 8, 8, False), (128, 7, 1, 5, 20, True),
                                                          (128, 32, 8, 6, 16, True), (64, 4, 4, 9, 3, False),
                                                          (128, 16, 1, 3, 9, True)])
@@ -448,31 +387,6 @@ def test_linear_push_ll_cluster(n, k, b, ndst):
         vals = (u & 0xFFFFFFFF).to(torch.int32).view(torch.float32)
         assert torch.equal(vals, ref.cpu())
         assert (t[b:] == -1).all()
-    # the local fp32 form (tps_linear_cluster): the same in-order sums
-    out = torch.full((b + 2, n), 7.0, device="cuda")
-    nat.check(lib.tps_linear_cluster(w.data_ptr(), n, k, k, x.data_ptr(), b, b, k, out.data_ptr(), _stream()))
-    torch.cuda.synchronize()
-    assert torch.equal(out[:b], ref) and (out[b:] == 7.0).all()
-
-
-@pytest.mark.parametrize("F,k,b", [(2368, 3584, 1), (1792, 4096, 16), (3456, 5120, 5), (512, 256, 64)])
-def test_linear_silu_cluster(F, k, b):
-    """tps_linear_silu_cluster == tps_linear (same split count) + tps_silu_mul, bit for bit."""
-    lib = nat.lib()
-    n = 2 * F
-    S = lib.tps_cluster_splits(n, k, b)
-    assert S >= 1
-    torch.manual_seed(F + b)
-    w = (torch.randn(n, k, device="cuda") * 0.05).bfloat16()
-    x = torch.randn(b, k, device="cuda").bfloat16()
-    ws = torch.zeros(S, b, n, device="cuda")
-    ref = torch.zeros(b, F, device="cuda", dtype=torch.bfloat16)
-    nat.check(lib.tps_linear(w.data_ptr(), n, k, k, x.data_ptr(), b, b, k, ws.data_ptr(), S, _stream()))
-    nat.check(lib.tps_silu_mul(ws.data_ptr(), S, b * n, b, F, ref.data_ptr(), F, _stream()))
-    got = torch.full((b + 1, F), 3.0, device="cuda", dtype=torch.bfloat16)
-    nat.check(lib.tps_linear_silu_cluster(w.data_ptr(), n, k, k, x.data_ptr(), b, b, k, got.data_ptr(), F, _stream()))
-    torch.cuda.synchronize()
-    assert torch.equal(got[:b], ref) and (got[b:] == 3.0).all()
 
 
 @pytest.mark.parametrize("V,k,b", [(4096, 256, 2), (152064, 3584, 64), (151936, 3584, 1), (19008, 3584, 17)])

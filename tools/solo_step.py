@@ -33,8 +33,6 @@ if __name__ == "__main__":
             runner.set_rows(bk, slots[:B])
             for v in variants:
                 toks = [x for x in v.split(",") if x]
-                r.executor.fuse_rope = "+fuse_rope" in toks
-                r.executor.qkv_in_gemm = "+qkv_in_gemm" in toks
                 r.executor.fuse_silu_min_units = 0 if "+silu_fused" in toks else (10 ** 9 if "+silu_unfused" in toks
                                                                                   else 120)
                 r.executor.skip = frozenset(x for x in toks if not x.startswith("+"))
