@@ -585,16 +585,17 @@ int configure_gemm() {
   return rc;
 }
 
-// TPS_QKV_CLUSTER=<n>: largest split-K cluster of the in-kernel QKV finishing (default 8,
-// the portable cluster size; 16 is allowed, 0 turns the fused form off)
+// TPS_QKV_CLUSTER=<n>: largest split-K cluster of the cluster-reduced projection (default 8,
+// the portable cluster size; 16 is allowed, 0 turns the cluster form off). (The name is
+// round 1's, when the QKV projection had a cluster epilogue too.)
 static int g_qkv_cluster = [] {
   const char* v = getenv("TPS_QKV_CLUSTER");
   return v ? atoi(v) : 8;
 }();
 
-// Split count of the in-kernel-finished QKV projection, 0 when the shape does not take it:
-// b <= 64 (one activation tile), every (tile, split) unit on its own SM (one wave), the
-// splits of a tile within one cluster.
+// Split count of a cluster-reduced projection (tps_linear_push_ll_cluster), 0 when the shape
+// does not take it: b <= 64 (one activation tile), every (tile, split) unit on its own SM
+// (one wave), the splits of a tile within one cluster.
 int cluster_splits(int64_t n, int64_t k, int64_t b) {
   if (g_qkv_cluster <= 0 || b < 1 || b > 64) return 0;
   const int64_t tiles = (n + kBM - 1) / kBM;
