@@ -64,6 +64,11 @@ def parse():
     ap.add_argument("--tp-list", default="", help="Algorithm 1 candidates (default: 1 and N, BASELINE config 2)")
     ap.add_argument("--initial-tp", type=int, default=1, help="starting TP degree (config 4 starts at TP2)")
     ap.add_argument("--cpu-threads", type=int, default=0)
+    ap.add_argument("--virtual", type=int, default=0,
+                    help="run an N-rank virtual world on this one GPU (every rank shares the device: a "
+                         "functional / memory run of a multi-GPU config, not a throughput number)")
+    ap.add_argument("--alias-replicas", action="store_true",
+                    help="with --virtual: DP replicas of a TP rank share one weight arena")
     return ap.parse_args()
 
 
@@ -286,14 +291,15 @@ def main():
     from paper_2605_23945_b200.coordinator import GlobalCoordinator
     from paper_2605_23945_b200.profiler import gemm_probe
 
-    gpus = max(1, args.gpus)
-    world = World.from_env() if gpus > 1 else World.virtual(1)
+    gpus = args.virtual or max(1, args.gpus)
+    world = World.virtual(args.virtual) if args.virtual else (World.from_env() if gpus > 1 else World.virtual(1))
     rank = world.local_ranks[0]
     dev = world.devices[rank]
     spec, geom = build_spec(args, gpus)
     table = measured_table(args.model)
     t_setup = time.perf_counter()
-    coord = GlobalCoordinator(spec, geom, world, seed=0, table=table)
+    coord = GlobalCoordinator(spec, geom, world, seed=0, table=table,
+                              **({"alias_replicas": True} if args.alias_replicas else {}))
     setup_s = time.perf_counter() - t_setup
     for _ in range(args.warmup):
         coord.run()
@@ -384,7 +390,11 @@ def main():
                      "per_bucket": {str(B): {"gbps": probes[B]["gbps"], "rounds": hist[B]} for B in sorted(hist)},
                      "rounds_at_other_tp": other_rounds},
         "clocks": clk.summary(),
+        "peak_hbm_gb": torch.cuda.max_memory_allocated(dev) / 2 ** 30,
     }
+    if args.virtual:
+        line["virtual_world"] = (f"{args.virtual} ranks on one GPU (functional / memory run: every rank's kernels "
+                                 f"share the device, so times are not N-GPU times)")
     if e2e:
         line["e2e"] = e2e
     if table is not None:
@@ -423,7 +433,8 @@ def main():
             gc.collect()  # executors / runners / comms form reference cycles
             torch.cuda.empty_cache()
             sspec = dataclasses.replace(spec, mode="static", initial_tp=tp)
-            coord = GlobalCoordinator(sspec, geom, world, seed=0, table=table)
+            coord = GlobalCoordinator(sspec, geom, world, seed=0, table=table,
+                                      **({"alias_replicas": True} if args.alias_replicas else {}))
             coord.run()
             srep, _ = coord.run()
             line["fixed_tp"][str(tp)] = srep.generation_time

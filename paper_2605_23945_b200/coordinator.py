@@ -830,7 +830,7 @@ class GlobalCoordinator:
 
     def __init__(self, spec: ScenarioSpec, geom: DecoderGeometry, world: World | None = None, seed: int = 0,
                  table=None, use_graphs: bool = True, copy_mode: int = 1, host_io: bool = False,
-                 state_method: str | None = None, temperature: float = 0.0):
+                 state_method: str | None = None, temperature: float = 0.0, **backend_opts):
         self.spec = spec
         self.geom = geom
         self.world = world or World.virtual(spec.cluster.gpus_per_node)
@@ -838,7 +838,7 @@ class GlobalCoordinator:
         self.seed = seed
         self.backend = B200Backend(spec, geom, self.world, seed=seed, use_graphs=use_graphs,
                                    copy_mode=copy_mode, host_io=host_io, state_method=state_method,
-                                   temperature=temperature)
+                                   temperature=temperature, **backend_opts)
         self.setup_capture_s = self.backend.capture_all(every_layout=True)
         self.setup_items_s = self.backend.prepare_switch_items()
         self.runs = 0

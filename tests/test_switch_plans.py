@@ -201,17 +201,25 @@ def test_weight_plan_entry_coverage_check():
         assert verify_entries(pad, lay)
 
 
-def test_kv_moves_match_the_chunk_plan_and_migrate_bit_exact():
+@pytest.mark.parametrize("gname", ["mini-qwen", "tiny", "mini-llama"])
+def test_kv_moves_match_the_chunk_plan_and_migrate_bit_exact(gname):
     """The O(samples) KV moves (expanded from page tables, as tps_kv_move_items does on the
-    device) copy exactly the chunks plan_kv_pulls lists, and the migrated pages are bit-exact."""
+    device) copy exactly the chunks plan_kv_pulls lists, and the migrated pages are bit-exact --
+    with KV heads replicated (tp > n_kv: mini-qwen, tiny) and split (mini-llama)."""
     from oracle.reshard_ref import expand_kv_moves
+    from paper_2605_23945_b200.models import geometry as _geometry
     from paper_2605_23945_b200.switch_executor import (kv_move_bytes, pack_kv_moves, plan_kv_moves,
                                                        verify_kv_moves)
-    geom = GEOS["mini-qwen"]
+    geom = _geometry(gname)
     world, L, D = 8, geom.num_layers, geom.head_dim
     chunk = 64 * D * 2
     rng = np.random.default_rng(1)
     for t_old, t_new in [(1, 2), (1, 8), (2, 8), (4, 2), (2, 4), (8, 1), (4, 8)]:
+        try:
+            geom.check_tp(t_old)
+            geom.check_tp(t_new)
+        except Exception:
+            continue
         old, new = Layout(t_old, world), Layout(t_new, world)
         n_samples, P, npg_old, npg_new = 6, 8, 64, 80
         ctx = [int(x) for x in rng.integers(1, 400, n_samples)]
