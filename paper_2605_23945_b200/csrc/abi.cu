@@ -126,7 +126,10 @@ int register_abort_setter(AbortSetter f) {
 }
 static unsigned int* g_abort_host = nullptr;
 
-static int install_abort_word() {
+static int install_abort_word(int device) {
+  static std::vector<int> done;  // devices whose translation units hold the pointer already
+  for (int d : done)
+    if (d == device) return kOk;
   if (!g_abort_host) {
     void* p = nullptr;
     TPS_CUDA_TRY(cudaHostAlloc(&p, 64, cudaHostAllocMapped | cudaHostAllocPortable));
@@ -140,6 +143,7 @@ static int install_abort_word() {
     if (e != 0)
       return fail(kCuda, std::string("abort word: ") + cudaGetErrorString(static_cast<cudaError_t>(e)));
   }
+  done.push_back(device);
   return kOk;
 }
 
@@ -175,7 +179,7 @@ int tps_init(int device, int* sm_count) {
   if (!rc) rc = configure_copy();
   if (!rc) rc = configure_decode_ops();
   if (!rc) rc = configure_persist();
-  if (!rc) rc = install_abort_word();
+  if (!rc) rc = install_abort_word(device);
   return rc;
 }
 
