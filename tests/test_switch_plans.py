@@ -281,3 +281,38 @@ def test_kv_move_plan_rejects_double_writes():
     dup = np.array([[0, 1, 0, 3, 0, 2, 4], [1, 2, 1, 3, 1, 1, 4]], dtype=np.int64)
     assert verify_kv_moves(dup, 2, 8)
     assert verify_kv_moves(np.array([[0, 1, 0, 9, 0, 1, 4]], dtype=np.int64), 2, 8)
+
+
+def test_kv_moves_edge_cases():
+    """Empty target groups, samples with no cached positions yet, and one-position contexts."""
+    from paper_2605_23945_b200.switch_executor import (kv_move_bytes, pack_kv_moves, plan_kv_moves,
+                                                       verify_kv_moves)
+    geom = GEOS["mini-qwen"]
+    old, new = Layout(1, 4), Layout(2, 4)
+    empty = plan_kv_moves(geom, old, new, 0, [], [], [], [])
+    assert empty.shape == (0, 7) and verify_kv_moves(empty, 1, 4) == []
+    assert kv_move_bytes(geom, empty, 0) == (0, 0)
+    packed, n = pack_kv_moves(geom, empty, {}, 0, 64)
+    assert n == 0 and len(packed) == 0
+    mv = plan_kv_moves(geom, old, new, 1, [2, 3], [0, 1], [0, 1], [0, 1])  # kv_len 0 -> no pages
+    assert mv.shape[0] == 1 and int(mv[0, 6]) == 1                         # kv_len 1 -> one page
+    chunk = 64 * geom.head_dim * 2
+    nb = sum(kv_move_bytes(geom, mv, 1))
+    assert nb == 2 * geom.num_layers * int(mv[0, 5]) * chunk
+
+
+def test_weight_plan_identity_transition_is_all_local():
+    """tp -> the same tp (a regroup): every byte is copied locally, none pulled."""
+    geom = GEOS["mini-qwen"]
+    for tp in (1, 2):
+        lay = Layout(tp, 4)
+        for r in range(4):
+            nv, loc = nvlink_bytes(plan_weight_pulls(geom, lay, lay, r), r)
+            assert nv == 0 and loc == arena_layout(geom, rank_shard(geom, tp, r % tp)).total_bytes - \
+                _padding(geom, tp, r % tp)
+
+
+def _padding(geom, tp, r):
+    lay = arena_layout(geom, rank_shard(geom, tp, r))
+    payload = sum(2 * int(np.prod(shape)) for _, shape in lay.entries.values())
+    return lay.total_bytes - payload
