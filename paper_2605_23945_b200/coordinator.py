@@ -201,6 +201,8 @@ class B200Backend:
             want = max(1, -(-per_node // lay.dp))
             dev = self.world.devices[self.world.local_ranks[0]]
             free = torch.cuda.mem_get_info(dev)[0] + torch.cuda.memory_reserved(dev) - torch.cuda.memory_allocated(dev)
+            if self.world.distributed and os.environ.get("TPS_SHARE_DEVICE") == "1":
+                free //= self.world.gpus  # every rank's process allocates on this one device
             cap = want  # (a virtual world holds every rank on one device)
             while cap > 0 and self.layout_bytes(lay, cap) > free - self.mem_headroom:
                 cap = cap * 3 // 4 if cap > 4 else cap - 1
