@@ -144,8 +144,7 @@ class B200Backend:
         self._staging: dict[int, tuple] = {}          # per rank: pinned + device staging area of a switch
         self.mem_headroom = int(mem_headroom_gb * 2 ** 30)
         self.ranks, self.runners = self._build_layout(self.layout, weights_seed=seed)
-        self._layouts[self.layout.tp] = {"ranks": self.ranks, "runners": self.runners,
-                                         "cap": {g: self.max_batch for g in self.local_groups()}}
+        self._layouts[self.layout.tp] = {"ranks": self.ranks, "runners": self.runners, "cap": self.max_batch}
         self.preplan_s = self.preplan()
         # every candidate layout is built (buffers, executors, communicators; graphs are
         # captured with the initial layout's) before the stage, within an HBM budget, so a
@@ -206,11 +205,14 @@ class B200Backend:
             cap = want  # (a virtual world holds every rank on one device)
             while cap > 0 and self.layout_bytes(lay, cap) > free - self.mem_headroom:
                 cap = cap * 3 // 4 if cap > 4 else cap - 1
+            # one capacity on every process (each builds, shares and rebuilds the same layouts:
+            # the peer-pointer exchanges are collectives)
+            cap = min(self.world.allgather(cap))
             if cap <= 0:
                 continue  # built at the switch instead (host time on the critical path)
-            need = {g: cap for g in self.local_groups(lay)}
-            ranks, runners = self._build_layout(lay, weights_seed=None, per_group=need)
-            self._layouts[tp] = {"ranks": ranks, "runners": runners, "cap": dict(need)}
+            ranks, runners = self._build_layout(lay, weights_seed=None,
+                                                per_group={g: cap for g in self.local_groups(lay)})
+            self._layouts[tp] = {"ranks": ranks, "runners": runners, "cap": cap}
             out[tp] = cap
         return out
 
@@ -259,19 +261,20 @@ class B200Backend:
         return RankState(w, kv, st, ex, comm)
 
     def _use_layout(self, lay: Layout, per_group: dict[int, int] | None) -> bool:
-        """Make `lay` current: reuse the cached ranks/runners of this TP degree when every
-        local group's slot capacity suffices (slot tables and page pools reset), else build
-        it (new buffers, weights filled by the switch's pulls) and cache it. True if built."""
-        need = {g: max(1, self.max_batch if per_group is None else per_group.get(g, 0))
-                for g in self.local_groups(lay)}
+        """Make `lay` current: reuse the cached ranks/runners of this TP degree when its slot
+        capacity (one per layout, the same for every group) holds the largest group of the
+        placement (slot tables and page pools reset), else build it (new buffers, weights
+        filled by the switch's pulls) and cache it. The placement covers every group and is the
+        same on every process, so every process rebuilds the same layouts. True if built."""
+        need = max(1, self.max_batch) if per_group is None else max([1] + list(per_group.values()))
         c = self._layouts.get(lay.tp)
-        if c is not None and all(c["cap"].get(g, 0) >= n for g, n in need.items()):
+        if c is not None and c["cap"] >= need:
             for rs in c["ranks"].values():
                 rs.slots.reset()
                 rs.kv.reset()
             self.ranks, self.runners = c["ranks"], c["runners"]
             return False
-        cap = {g: max(n, c["cap"].get(g, 0) if c else 0) for g, n in need.items()}
+        cap = max(need, c["cap"] if c else 0)
         if c is not None and lay.tp != self.spec.initial_tp:
             # grown: the smaller cached layout of this degree is dropped first (bounded HBM:
             # at most one layout per candidate degree is ever held)
@@ -280,7 +283,8 @@ class B200Backend:
             self._shared = {k: v for k, v in self._shared.items() if k[0] != lay.tp}
             self._witems = {k: v for k, v in self._witems.items() if lay not in (k[0], k[1])}
             gc.collect()
-        self.ranks, self.runners = self._build_layout(lay, weights_seed=None, per_group=cap)
+        self.ranks, self.runners = self._build_layout(lay, weights_seed=None,
+                                                      per_group={g: cap for g in self.local_groups(lay)})
         self._layouts[lay.tp] = {"ranks": self.ranks, "runners": self.runners, "cap": cap}
         return True
 
