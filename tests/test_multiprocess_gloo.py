@@ -105,3 +105,78 @@ def test_spmd_decisions_and_distributed_pull_plans():
             want = expected_shard(geo, full, 8, dst, layer, fam).contiguous().view(torch.int16).numpy()
             want = want.view(np.uint8).ravel()
             assert np.array_equal(mem.view(base + off, want.size), want), (dst, layer, fam)
+
+
+def _kv_worker(rank, world, port, q):
+    """Each process owns ranks {rank, rank + world, ...} of an 8-GPU node. As in
+    B200Backend._execute_switch: every process reports where its groups' samples sit, the
+    reports are all-gathered, and each process plans the KV moves of its own target ranks."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2605_23945_b200.cache_manager import World
+        from paper_2605_23945_b200.models import geometry
+        from paper_2605_23945_b200.switch_executor import Layout, plan_kv_moves
+
+        w = World(gpus=world, local_ranks=[rank], devices={rank: torch.device("cpu")}, distributed=True)
+        geom = geometry("mini-qwen")
+        old, new = Layout(2, 8), Layout(8, 8)
+        mine = [r for r in range(8) if r % world == rank]
+        # old placement: sample i in old group i % 4 at slot 1 + i // 4; the lead rank of a group
+        # reports it (the group's ranks live in different processes)
+        here = {i: (i % 4, 1 + i // 4) for i in range(10) if (i % 4) * old.tp in mine}
+        where = {}
+        for part in w.allgather(here):
+            where.update(part)
+        plans = {}
+        for dst in mine:
+            ids = list(range(10))  # TP8/DP1: every sample lands on the one group
+            moves = plan_kv_moves(geom, old, new, dst, [where[i][0] for i in ids], [where[i][1] for i in ids],
+                                  [2 + i for i in ids], [37 * i + 5 for i in ids])
+            plans[dst] = moves.tolist()
+        q.put((rank, w.allgather(plans)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_distributed_kv_move_plans_cover_every_head_once():
+    """The union of the per-process KV-move plans (each process planning only its target ranks
+    from the all-gathered placement) moves every (sample, kv head) each target rank owns exactly
+    once, from a rank of the sample's old group that holds that head."""
+    import numpy as np
+
+    from paper_2605_23945_b200.models import geometry, rank_shard
+    from paper_2605_23945_b200.switch_executor import Layout, plan_kv_moves
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_kv_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    merged = {}
+    for part in out[0][1]:
+        merged.update(part)
+    assert sorted(merged) == list(range(8))
+    geom = geometry("mini-qwen")
+    old, new = Layout(2, 8), Layout(8, 8)
+    for dst, rows in merged.items():
+        sh = rank_shard(geom, 8, dst)
+        got = set()
+        for src, sslot, shead, dslot, dhead, nh, npg in rows:
+            assert src // old.tp == (dslot - 2) % 4 and sslot == 1 + (dslot - 2) // 4  # the sample's old group / slot
+            osh = rank_shard(geom, old.tp, src % old.tp)
+            for h in range(nh):
+                gh = osh.kv_heads[0] + shead + h
+                assert gh == sh.kv_heads[0] + dhead + h  # same global kv head on both sides
+                got.add((dslot, dhead + h))
+            assert npg == -(-(37 * (dslot - 2) + 5) // 64)
+        assert got == {(2 + i, h) for i in range(10) for h in range(sh.n_kv)}
+        # the same plan a single process makes
+        ids = list(range(10))
+        ref = plan_kv_moves(geom, old, new, dst, [i % 4 for i in ids], [1 + i // 4 for i in ids],
+                            [2 + i for i in ids], [37 * i + 5 for i in ids])
+        assert np.array_equal(np.asarray(rows, dtype=np.int64).reshape(-1, 7), ref)
