@@ -485,7 +485,7 @@ class B200Backend:
                                     count=n)
                 if not recompute:
                     moves = plan_kv_moves(self.geom, old, new, r, og, oslot, nslot, ctx - 1)
-                    check(verify_kv_moves(moves, rs.kv.n_kv, rs.slots.num_slots), "kv move plan")
+                    check(verify_kv_moves(moves, rs.kv.n_kv, rs.slots.num_slots, nslot[ctx - 1 > 0]), "kv move plan")
                     kv_nv, kv_loc = kv_move_bytes(self.geom, moves, r)
                     packed, n_items = pack_kv_moves(self.geom, moves, src, rs.slots.page_table.data_ptr(),
                                                     rs.slots.page_table.stride(0) * 4)

@@ -339,10 +339,12 @@ def pack_kv_moves(geom: DecoderGeometry, moves: np.ndarray, src: dict[int, dict]
     return out, int(per.sum())
 
 
-def verify_kv_moves(moves: np.ndarray, n_kv_local: int, slots: int) -> list[str]:
-    """Every (target slot, kv head) written at most once; runs inside the target's heads/slots."""
+def verify_kv_moves(moves: np.ndarray, n_kv_local: int, slots: int, expect_slots=None) -> list[str]:
+    """Every (target slot, kv head) written at most once; runs inside the target's heads/slots;
+    with `expect_slots`, every kv head of each of those slots (the migrated samples that have
+    cached positions) written exactly once and no other slot touched."""
     if moves.size == 0:
-        return []
+        return ["kv heads of migrated samples not covered"] if expect_slots is not None and len(expect_slots) else []
     issues = []
     if np.any(moves[:, MV_NHEADS] <= 0) or np.any(moves[:, MV_NPAGES] <= 0):
         issues.append("empty kv move")
@@ -355,6 +357,11 @@ def verify_kv_moves(moves: np.ndarray, n_kv_local: int, slots: int) -> list[str]
     heads = heads + (np.arange(heads.size) - first)
     if np.unique(heads).size != heads.size:
         issues.append("a (slot, kv head) is written twice")
+    if expect_slots is not None:
+        want = (np.asarray(expect_slots, dtype=np.int64)[:, None] * n_kv_local +
+                np.arange(n_kv_local, dtype=np.int64)[None, :]).ravel()
+        if not np.array_equal(np.sort(heads), np.sort(want)):
+            issues.append("kv heads of migrated samples not covered exactly once")
     return issues
 
 
