@@ -13,8 +13,12 @@
  *       tps_reduce_push + the waiting tps_add_norm.
  *   (2) the switch seam       _commit_switch, tpshift/engine.py:206-269, and the
  *       plans it executes, plan_weight_reshard / plan_kv_migration
- *       (tpshift/reshard.py:80-151): tps_copy_items, tps_barrier; the
+ *       (tpshift/reshard.py:80-151): tps_copy_items (weight pulls), tps_kv_move_items
+ *       (plan_kv_migration's pages, expanded on the device), tps_barrier; the
  *       communication-group pool (tpshift/switchcost.py:76-104) is the IPC set.
+ *
+ * Device waits are bounded: a wait over its budget raises the soft-abort word
+ * (tps_abort_status) and abandons instead of trapping.
  *
  * Conventions: every entry point takes raw device pointers, integer sizes and a
  * cudaStream_t passed as void*; calls are stream-ordered and asynchronous; the
