@@ -145,3 +145,12 @@ def test_table_backend_switch_bytes_match_the_executed_plans():
         h_nv = sum(4 * s.context_len for s in mine if r not in old.ranks_of_group(s.intra_dp_group))
         h_loc = sum(4 * s.context_len for s in mine if r in old.ranks_of_group(s.intra_dp_group))
         assert got[r] == (nv + a + h_nv, loc + b + h_loc), r
+
+
+def test_bench_decision_layer_timing_runs_the_reference_path():
+    """cpu_baseline.decision_layer: Algorithm 1 at B=512 (config 2 on 8 GPUs) and a whole
+    simulated stage, timed single-threaded."""
+    import argparse
+    import bench
+    d = bench.decision_layer_timing(argparse.Namespace(model="qwen2.5-7b", l_max=8192, prompt_len=512, seed=4))
+    assert d["evaluate_live_samples"] > 400 and d["evaluate_ms"] > 0 and d["run_stage_s"] > 0
