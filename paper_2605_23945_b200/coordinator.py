@@ -151,6 +151,8 @@ class B200Backend:
         # switch only moves bytes (recapture is the switch's largest fixed cost)
         if prebuild is None:
             prebuild = os.environ.get("TPS_PREBUILD", "1") == "1"
+        # a static stage (or a disabled controller) never switches: nothing to prepare
+        prebuild = prebuild and spec.mode != "static" and spec.controller.enabled
         self.prebuilt: dict[int, int] = self.prebuild() if prebuild else {}
 
     def preplan(self) -> float:
