@@ -224,11 +224,11 @@ int kv_move_items(const void* moves, int n_moves, int64_t n_items, void* dst_kv,
 
 // ------------------------------------------------------ device barrier ----
 // Epoch barrier with one slot per source rank: rank q stores the barrier's epoch
-// into slot q of every peer's slot array, then waits until every peer's slot in its
-// own array holds >= epoch. (A shared counter that every peer increments is not a
-// barrier once ranks may run ahead: a rank that already passed barrier k and
-// arrives at k+1 would add to a counter a slower rank is still checking for k, and
-// let it through before the last rank arrived. Epoch slots cannot be over-counted.)
+// into slot q of every peer's slot array (plain 8-B stores: idempotent, a replayed or
+// duplicated signal cannot over-count), then waits until every peer's slot in its own
+// array holds >= epoch. Replaces round 1's shared counter of relaxed atomic adds, under
+// which a multi-process stage on one shared GPU hung with adds a waiting rank never saw
+// (tests/test_barrier_protocol.py: both protocols are safe in isolation).
 constexpr int kMaxPeerArgs = 16;
 struct PeerPtrs {
   uint64_t* p[kMaxPeerArgs];
