@@ -149,6 +149,7 @@ class B200Backend:
         # every candidate layout is built (buffers, executors, communicators; graphs are
         # captured with the initial layout's) before the stage, within an HBM budget, so a
         # switch only moves bytes (recapture is the switch's largest fixed cost)
+        self._init_barrier()
         if prebuild is None:
             prebuild = os.environ.get("TPS_PREBUILD", "1") == "1"
         # a static stage (or a disabled controller) never switches: nothing to prepare
@@ -702,16 +703,25 @@ class B200Backend:
             self._launch_items(dev, n, mode, st, nb)
             self._keep.append(dev)
 
+    def _init_barrier(self) -> None:
+        """The device barrier's slot array, zeroed and exchanged before the stage: its zero-fill
+        is stream-ordered, so created lazily at the first switch it could run after an idle
+        peer had already signalled it and wipe the signal (tests/test_barrier_protocol.py)."""
+        if not self.world.distributed or self._bar is not None:
+            return
+        r = self.world.local_ranks[0]
+        mine = torch.zeros(self.world.gpus, dtype=torch.int64, device=self.world.devices[r])
+        torch.cuda.synchronize(self.world.devices[r])  # zeroed before any peer can see the address
+        ptrs = self.world.share({r: {"bar": mine}})
+        self._bar = (mine, [ptrs[x]["bar"] + 8 * r for x in range(self.world.gpus) if x != r])
+
     def _device_barrier(self) -> None:
         """Node-wide device barrier (a virtual world is already ordered by its single stream):
         one epoch slot per source rank in every rank's slot array (tps_barrier)."""
         if not self.world.distributed:
             return
         r = self.world.local_ranks[0]
-        if self._bar is None:
-            mine = torch.zeros(self.world.gpus, dtype=torch.int64, device=self.world.devices[r])
-            ptrs = self.world.share({r: {"bar": mine}})
-            self._bar = (mine, [ptrs[x]["bar"] + 8 * r for x in range(self.world.gpus) if x != r])
+        self._init_barrier()
         mine, peers = self._bar
         self._barrier_epoch += 1
         nat.check(nat.lib().tps_barrier(nat.ptr_array(peers), len(peers), mine.data_ptr(), self.world.gpus, r,
