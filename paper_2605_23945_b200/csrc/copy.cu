@@ -226,9 +226,9 @@ int kv_move_items(const void* moves, int n_moves, int64_t n_items, void* dst_kv,
 // Epoch barrier with one slot per source rank: rank q stores the barrier's epoch
 // into slot q of every peer's slot array (plain 8-B stores: idempotent, a replayed or
 // duplicated signal cannot over-count), then waits until every peer's slot in its own
-// array holds >= epoch. Replaces round 1's shared counter of relaxed atomic adds, under
-// which a multi-process stage on one shared GPU hung with adds a waiting rank never saw
-// (tests/test_barrier_protocol.py: both protocols are safe in isolation).
+// array holds >= epoch. Replaces round 1's shared counter of relaxed atomic adds, whose
+// lazily queued zero-fill could wipe a fast peer's early add and hang the barrier (a wiped
+// epoch store is superseded by the next barrier's; tests/test_barrier_protocol.py).
 constexpr int kMaxPeerArgs = 16;
 struct PeerPtrs {
   uint64_t* p[kMaxPeerArgs];
