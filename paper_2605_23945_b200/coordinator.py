@@ -157,17 +157,19 @@ class B200Backend:
         self.prebuilt: dict[int, int] = self.prebuild() if prebuild else {}
 
     def preplan(self) -> float:
-        """Plan (and verify) this process's weight pulls for every switch from the initial layout
-        to a wider candidate degree before the stage starts, so a switch's critical path only
-        plans its KV pages (Qwen2.5-7B TP1 -> TP2: ~0.15 s of host planning per rank moved off the
-        switch). Plans are memoised per (geometry, layouts, rank) for the process."""
+        """Plan (and verify) this process's weight pulls for every switch between candidate
+        degrees before the stage starts, so a switch's critical path only plans its KV moves
+        (Qwen2.5-7B TP1 -> TP2: ~0.15 s of host planning per rank moved off the switch). Plans
+        are memoised per (geometry, layouts, rank) for the process."""
         t0 = time.perf_counter()
-        init = Layout(self.spec.initial_tp, self.world.gpus)
-        for tp in self.spec.controller.tp_list:
-            if tp > init.tp and self.world.gpus % tp == 0:
-                new = Layout(tp, self.world.gpus)
-                for r in self.world.local_ranks:
-                    cached_weight_pulls(self.geom, init, new, r)
+        tps = sorted({self.spec.initial_tp} | {t for t in self.spec.controller.tp_list if self.world.gpus % t == 0})
+        if self.spec.mode == "static" or not self.spec.controller.enabled:
+            tps = []
+        for a in tps:
+            for b in tps:
+                if a != b:
+                    for r in self.world.local_ranks:
+                        cached_weight_pulls(self.geom, Layout(a, self.world.gpus), Layout(b, self.world.gpus), r)
         return time.perf_counter() - t0
 
     def layout_bytes(self, lay: Layout, slots: int) -> int:
@@ -591,19 +593,21 @@ class B200Backend:
         return hit
 
     def prepare_switch_items(self) -> float:
-        """Stage the weight copy-item tables of every switch from the initial layout to a prebuilt
-        one (host seconds; before the stage)."""
+        """Stage the weight copy-item tables of every switch between built layouts -- the initial
+        one and every prebuilt candidate, both directions -- before the stage (host seconds), so
+        a multi-stage run (TP1 -> 2 -> 4 -> 8 and back) plans no weight pull at a switch."""
         t0 = time.perf_counter()
-        init = self._layouts.get(self.spec.initial_tp)
-        if init is None:
+        if self.spec.initial_tp not in self._layouts:
             return 0.0
-        old = Layout(self.spec.initial_tp, self.world.gpus)
-        src = self._shared_layout(old, init["ranks"])
-        for tp in self.prebuilt:
-            new = Layout(tp, self.world.gpus)
-            self._shared_layout(new, self._layouts[tp]["ranks"])
-            for r in self.world.local_ranks:
-                self._weight_items(old, new, r, src, self._layouts[tp]["ranks"][r])
+        built = [self.spec.initial_tp] + sorted(self.prebuilt)
+        shared = {tp: self._shared_layout(Layout(tp, self.world.gpus), self._layouts[tp]["ranks"]) for tp in built}
+        for a in built:
+            for b in built:
+                if a == b:
+                    continue
+                old, new = Layout(a, self.world.gpus), Layout(b, self.world.gpus)
+                for r in self.world.local_ranks:
+                    self._weight_items(old, new, r, shared[a], self._layouts[b]["ranks"][r])
         if self.prebuilt:
             self._warm_switch_path()
         return time.perf_counter() - t0
