@@ -154,3 +154,14 @@ def test_bench_decision_layer_timing_runs_the_reference_path():
     import bench
     d = bench.decision_layer_timing(argparse.Namespace(model="qwen2.5-7b", l_max=8192, prompt_len=512, seed=4))
     assert d["evaluate_live_samples"] > 400 and d["evaluate_ms"] > 0 and d["run_stage_s"] > 0
+
+
+def test_table_backend_falls_back_to_the_quote_without_a_geometry():
+    """A reference preset's model (no executable geometry) is priced by the planner's quote."""
+    from paper_2605_23945_b200.config import build_scenario, load_config
+    from paper_2605_23945_b200.engine import build_profile
+    spec = build_scenario(load_config("paper_a40"), l_max=12288, seed=3)
+    tab = build_profile(spec)
+    rep = run(spec, tab, TableBackend(spec, tab))
+    sw = [s for nr in rep.node_reports for s in nr["switches"]]
+    assert sw and all(abs(s["breakdown"]["total"] - s["quoted_total"]) < 1e-12 for s in sw)
