@@ -234,11 +234,14 @@ def active_histogram(rep) -> dict[int, int]:
 
 def cpu_stage_estimate(spec, steps: dict, hist: dict[int, int]) -> float:
     """Stage seconds on the CPU oracle: every decode round at its active batch (measured
-    full-depth step times, piecewise-linear in B between the measured batches) + the prompts'
-    prefill at the measured 64-token chunk rate."""
+    full-depth step times, piecewise-linear in B between the measured batches, proportional to
+    B beyond the largest) + the prompts' prefill at the measured 64-token chunk rate."""
     bs = sorted(steps["steps"])
     ys = [steps["steps"][b] for b in bs]
-    dec = sum(n * float(np.interp(B, bs, ys)) for B, n in hist.items())
+
+    def t(B):  # beyond the largest measured batch (N > 1 stages): proportional to the rows
+        return float(np.interp(B, bs, ys)) if B <= bs[-1] else ys[-1] * B / bs[-1]
+    dec = sum(n * t(B) for B, n in hist.items())
     pre = spec.global_batch * (spec.prompt_len / 64.0) * steps["prefill64_s"]
     return dec + pre
 
