@@ -57,7 +57,10 @@ def test_oracle_prefill_equals_steps_bf16():
     last = a.prefill(prompt, 0)
     for t, tok in enumerate(prompt):
         ref = b.step([tok], [t], [0])[0]
-    assert float((last - ref).abs().max()) <= 1e-4
+    # bf16-rounded intermediates: the chunk's GEMMs and the per-position steps sum in a different
+    # order (and the BLAS kernel the host picks changes that order again), so an intermediate can
+    # land one bf16 ulp (2^-8 relative) apart; measured 1.4e-3 on logits of magnitude ~1.
+    assert float((last - ref).abs().max()) <= 1e-2
     for l in range(TINY["num_layers"]):
         for r in range(2):
             ka, va = a._kv(0, l, r)
