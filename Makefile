@@ -6,7 +6,7 @@ PKG := paper_2605_23945_b200
 CSRC := $(PKG)/csrc
 LIB := $(PKG)/libtpshift_b200.so
 OBJDIR := build/obj
-SRCS := abi gemm_tcgen05 decode_ops attention attention_balanced attention_prefill copy persist
+SRCS := abi gemm_tcgen05 gemv decode_ops attention attention_balanced attention_prefill copy persist
 OBJS := $(SRCS:%=$(OBJDIR)/%.o)
 NVFLAGS := -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
            -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr

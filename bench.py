@@ -14,8 +14,10 @@ decode path + decode to the last sample), run by the Global Coordinator.
              wall clock (includes launch/host overheads)
   roofline   dominant kernel = the tcgen05 projection GEMM, bytes/launch over
              CUDA-event time, per batch bucket, weighted by the stage's rounds
-  cpu_baseline  the CPU oracle (oracle/decoder_ref.py) on this host's cores,
-             1 layer timed and extrapolated to the stage's round/batch profile
+  cpu_baseline  the CPU oracle (oracle/decoder_ref.py) on this host's cores at full
+             depth: decode steps timed at B = 1, 8, 64 and composed over the stage's rounds
+  tail       the post-switch TP8 tail (one loopback rank, B <= 32) vs its HBM floor, with
+             the warp-shuffle GEMV form (csrc/gemv.cu) timed beside the default at B <= 4
 
 `--impl reference` times the reference-side CPU path (the oracle port) instead.
 Run: python bench.py [--gpus N --steps K --warmup W]; N>1 under torchrun.
@@ -413,17 +415,6 @@ def main():
     if tr:
         line["roofline"]["traffic"] = tr["dram_bytes_per_launch"]
         line["roofline"]["traffic_note"] = tr["note"]
-    if rank == 0 and gpus == 1 and not args.no_tail:
-        # the post-switch tail (BASELINE config 2 ends at TP8): one TP8 rank alone on this GPU
-        # (loopback peer table: same kernels and protocol, no NVLink hop), B <= 32
-        from paper_2605_23945_b200.profiler import tail_probe
-        try:
-            tail = tail_probe(geom, 8, (1, 4, 16, 32), 4096, peak)
-            line["tail"] = {"tp": 8, "ctx": 4096, "per_batch": {str(b): v for b, v in tail.items()},
-                            "note": "TP8 rank with a looped-back peer table (no NVLink hop); floor = weight shard "
-                                    "+ LM-head shard + live and new K/V at the measured copy peak"}
-        except Exception as e:
-            line["tail"] = {"error": f"{type(e).__name__}: {e}"}
     if gpus > 1 and args.static_tps:
         # the north-star comparison: the same stage at a fixed TP (no switching), same engine
         line["fixed_tp"] = {}
@@ -453,6 +444,18 @@ def main():
             line["switch_microbench"] = switch_microbench(args, peak)
         except Exception as e:
             line["switch_microbench"] = {"error": f"{type(e).__name__}: {e}"}
+    if rank == 0 and gpus == 1 and not args.no_tail:
+        # the post-switch tail (BASELINE config 2 ends at TP8): one TP8 rank alone on this GPU
+        # (loopback peer table: same kernels and protocol, no NVLink hop), B <= 32
+        from paper_2605_23945_b200.profiler import tail_probe
+        try:
+            tail = tail_probe(geom, 8, (1, 4, 16, 32), 4096, peak)
+            line["tail"] = {"tp": 8, "ctx": 4096, "per_batch": {str(b): v for b, v in tail.items()},
+                            "note": "TP8 rank with a looped-back peer table (no NVLink hop); floor = weight shard "
+                                    "+ LM-head shard + live and new K/V at the measured copy peak; gemv_ms = the "
+                                    "same step with every projection on the warp-shuffle GEMV (csrc/gemv.cu)"}
+        except Exception as e:
+            line["tail"] = {"error": f"{type(e).__name__}: {e}"}
     steps = None
     threads = args.cpu_threads or os.cpu_count()
     if rank == 0 and gpus == 1 and not args.no_cpu:

@@ -190,6 +190,26 @@ int tps_linear_push_ll_cluster(const void* w, int64_t n, int64_t k, int64_t ldw,
                                int64_t x_rows, int64_t ldx, uint64_t* const* dsts, int ndst,
                                const uint64_t* epoch, uint32_t tag_mult, uint32_t tag_add, void* stream);
 
+/* Tail-batch projections on CUDA cores (warp-shuffle GEMV, b <= tps_gemv_max_rows()): the
+ * contracts of the tcgen05 family above at the tail, so the executor swaps one call for the
+ * other (weight-traffic term of oracle_decode_latency, tpshift/latency.py:123-124):
+ *   tps_gemv          = tps_linear with splits = 1: out fp32 [b][n]
+ *   tps_gemv_silu     = tps_linear_silu (W rows in 64-row [gate c | up c] blocks, n = 2F)
+ *   tps_gemv_push_ll  = tps_linear_push_ll_cluster: out[i][j] as one LL {fp32 bits, tag} at
+ *                       dsts[d] + i * n + j, tag = (*epoch) * tag_mult + tag_add
+ *   tps_gemv_argmax   = tps_linear_argmax: logits [b][n] + cand[i * ceil(n/128) + t]
+ * k, ldw, ldx multiples of 8; w, x 16-byte aligned. Deterministic (fixed reduction order). */
+int tps_gemv_max_rows(void);
+int tps_gemv(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t ldx,
+             float* out, void* stream);
+int tps_gemv_silu(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t ldx,
+                  void* act, int64_t ld_act, void* stream);
+int tps_gemv_push_ll(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t ldx,
+                     uint64_t* const* dsts, int ndst, const uint64_t* epoch, uint32_t tag_mult, uint32_t tag_add,
+                     void* stream);
+int tps_gemv_argmax(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t ldx,
+                    float* logits, void* cand, int vocab0, void* stream);
+
 /* Positions per group of tps_prefill_attention for G query heads per KV head
  * (min(16, 64 / G); 0 if G > 64). */
 int tps_prefill_group_positions(int G);

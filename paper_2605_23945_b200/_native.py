@@ -40,6 +40,12 @@ SIGNATURES = {
     "tps_linear_argmax": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _vp, _vp, _i32, _vp]),
     "tps_linear_push_ll_cluster": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _pp, _i32, _vp,
                                           ctypes.c_uint32, ctypes.c_uint32, _vp]),
+    "tps_gemv_max_rows": (_i32, []),
+    "tps_gemv": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _vp]),
+    "tps_gemv_silu": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _i64, _vp]),
+    "tps_gemv_push_ll": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _pp, _i32, _vp, ctypes.c_uint32,
+                                ctypes.c_uint32, _vp]),
+    "tps_gemv_argmax": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _vp, _i32, _vp]),
     "tps_prefill_group_positions": (_i32, [_i32]),
     "tps_prefill_attention": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _i32, _i32, _i32, _i32, _vp,
                                      _vp]),

@@ -36,6 +36,15 @@ int linear_argmax(const void* w, int64_t n, int64_t k, int64_t ldw, const void* 
 int linear_push_ll_cluster(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b,
                            int64_t x_rows, int64_t ldx, const DstList& dst, const uint64_t* tag_epoch,
                            uint32_t tag_mult, uint32_t tag_add, cudaStream_t stream);
+int gemv_max_rows();
+int gemv(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t ldx, float* out,
+         cudaStream_t st);
+int gemv_silu(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t ldx, void* act,
+              int64_t ld_act, cudaStream_t st);
+int gemv_push_ll(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t ldx,
+                 const DstList& dst, const uint64_t* epoch, uint32_t tag_mult, uint32_t tag_add, cudaStream_t st);
+int gemv_argmax(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t ldx,
+                float* logits, void* cand, int vocab0, cudaStream_t st);
 int embed(const int*, const int*, const int*, const int*, int, const void*, int, int, float*, cudaStream_t);
 int add_norm(float*, const Src&, const WaitSpec&, const void*, float, int, int, void*, int, cudaStream_t);
 int reduce_push(const Src&, const DstList&, long long, const SignalSpec&, cudaStream_t);
@@ -235,6 +244,34 @@ int tps_linear_silu(const void* w, int64_t n, int64_t k, int64_t ldw, const void
 }
 
 int tps_cluster_splits(int64_t n, int64_t k, int64_t b) { return cluster_splits(n, k, b); }
+
+int tps_gemv_max_rows(void) { return gemv_max_rows(); }
+
+int tps_gemv(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t ldx, float* out,
+             void* stream) {
+  return gemv(w, n, k, ldw, x, b, ldx, out, S(stream));
+}
+
+int tps_gemv_silu(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t ldx, void* act,
+                  int64_t ld_act, void* stream) {
+  return gemv_silu(w, n, k, ldw, x, b, ldx, act, ld_act, S(stream));
+}
+
+int tps_gemv_push_ll(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t ldx,
+                     uint64_t* const* dsts, int ndst, const uint64_t* epoch, uint32_t tag_mult, uint32_t tag_add,
+                     void* stream) {
+  TPS_CHECK_ARG(ndst >= 1 && ndst <= kMaxPeers && dsts, "gemv_push_ll: 1..8 destinations");
+  DstList dl;
+  dl.n = ndst;
+  for (int i = 0; i < ndst; ++i) dl.p[i] = reinterpret_cast<float*>(dsts[i]);
+  return gemv_push_ll(w, n, k, ldw, x, b, ldx, dl, epoch, tag_mult, tag_add, S(stream));
+}
+
+int tps_gemv_argmax(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t ldx,
+                    float* logits, void* cand, int vocab0, void* stream) {
+  return gemv_argmax(w, n, k, ldw, x, b, ldx, logits, cand, vocab0, S(stream));
+}
+
 
 int tps_linear_argmax(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t x_rows,
                       int64_t ldx, float* logits, void* cand, int vocab0, void* stream) {

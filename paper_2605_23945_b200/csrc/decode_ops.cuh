@@ -117,7 +117,7 @@ struct TraceBuf {
 static __device__ TraceBuf g_trace_buf;  // one per translation unit, set by trace_register()
 enum TraceKind : int {
   kTrEmbed = 1, kTrAddNorm, kTrReducePush, kTrQkvRope, kTrSilu, kTrArgmax1, kTrArgmax2, kTrEpoch,
-  kTrGemm, kTrGemmSilu, kTrAttnSplit, kTrAttnCombine, kTrAttnBal, kTrAttnPrefill, kTrGemmPush
+  kTrGemm, kTrGemmSilu, kTrAttnSplit, kTrAttnCombine, kTrAttnBal, kTrAttnPrefill, kTrGemmPush, kTrGemv
 };
 __device__ __forceinline__ uint64_t trace_now() {
   uint64_t t;

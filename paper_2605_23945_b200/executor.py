@@ -88,6 +88,11 @@ FUSE_SOURCES = 16  # LL slots per parity: tp x splits partials of one fused allr
 # TP1 B=1 4.28 vs 3.00 ms): opt-in (TPS_PERSIST=1 or use_persist)
 PERSIST_MAX_ROWS = 16
 PERSIST = os.environ.get("TPS_PERSIST", "0") == "1"
+# B <= GEMV_ROWS: every projection of the step on the CUDA-core warp-shuffle GEMV
+# (csrc/gemv.cu; same output contracts as the tcgen05 forms, at most tps_gemv_max_rows() = 4
+# rows). Opt-in (TPS_GEMV_ROWS=4 or InferExecutor.gemv_rows) until it is measured against the
+# tcgen05 tail on B200: bench.py's `tail` section times both.
+GEMV_ROWS = int(os.environ.get("TPS_GEMV_ROWS", "0"))
 
 
 class GroupComm:
@@ -243,6 +248,7 @@ class InferExecutor:
         self.launch_stats: dict[int, LaunchStats] = {}
         # persistent step (csrc/persist.cu) state: workspace, logits, CTAs per rank it was sized for
         self.use_persist = PERSIST
+        self.gemv_rows = min(GEMV_ROWS, nat.lib().tps_gemv_max_rows())
         self.p_work: torch.Tensor | None = None
         self.p_logits: torch.Tensor | None = None
         self.p_ctas = 0
@@ -292,6 +298,11 @@ class InferExecutor:
         s = self._splits(n, k, B)
         if "linear" in self.skip:
             return (self.ws.data_ptr(), s, B * n)
+        if B <= self.gemv_rows:
+            nat.check(nat.lib().tps_gemv(w.data_ptr(), n, k, k, x.data_ptr(), B, x.shape[1], self.ws.data_ptr(), st),
+                      "tps_gemv")
+            stats.add("linear")
+            return (self.ws.data_ptr(), 1, B * n)
         nat.check(nat.lib().tps_linear(w.data_ptr(), n, k, k, x.data_ptr(), B, x.shape[0],
                                        x.shape[1], self.ws.data_ptr(), s, st), "tps_linear")
         stats.add("linear")
@@ -371,7 +382,11 @@ class InferExecutor:
             yield from self._row_parallel(st, stats, 2 * l, "w_o", W[(l, "w_o")], self.attn, B,
                                           W.tensor_ptr(l, "ln2"))
             w_gu = W[(l, "w_gu")]
-            if self._fuse_silu(B):
+            if B <= self.gemv_rows and "linear" not in self.skip:
+                nat.check(lib.tps_gemv_silu(w_gu.data_ptr(), 2 * self.F, H, H, self.xn.data_ptr(), B, H,
+                                            self.act.data_ptr(), self.F, st), "tps_gemv_silu")
+                stats.add("linear")
+            elif self._fuse_silu(B):
                 nat.check(lib.tps_linear_silu(w_gu.data_ptr(), 2 * self.F, H, H, self.xn.data_ptr(), B,
                                               self.xn.shape[0], H, self.act.data_ptr(), self.F, st),
                           "tps_linear_silu")
@@ -400,9 +415,14 @@ class InferExecutor:
             return
         if cm is None and self.temperature <= 0 and self.lm_argmax and "linear" not in self.skip:
             w = W[(-1, "lm_head")]
-            nat.check(lib.tps_linear_argmax(w.data_ptr(), w.shape[0], w.shape[1], w.shape[1], self.xn.data_ptr(), B,
-                                            self.xn.shape[0], self.xn.shape[1], self.ws.data_ptr(),
-                                            self.lm_cand.data_ptr(), self.shard.vocab[0], st), "tps_linear_argmax")
+            if B <= self.gemv_rows:
+                nat.check(lib.tps_gemv_argmax(w.data_ptr(), w.shape[0], w.shape[1], w.shape[1], self.xn.data_ptr(), B,
+                                              self.xn.shape[1], self.ws.data_ptr(), self.lm_cand.data_ptr(),
+                                              self.shard.vocab[0], st), "tps_gemv_argmax")
+            else:
+                nat.check(lib.tps_linear_argmax(w.data_ptr(), w.shape[0], w.shape[1], w.shape[1], self.xn.data_ptr(),
+                                                B, self.xn.shape[0], self.xn.shape[1], self.ws.data_ptr(),
+                                                self.lm_cand.data_ptr(), self.shard.vocab[0], st), "tps_linear_argmax")
             stats.add("linear")
             self._last_lm_srcs = ((self.ws.data_ptr(), 1, B * w.shape[0]), B)
             nat.check(lib.tps_argmax_finalize(self._arr([self.lm_cand.data_ptr()]), 1, self.lm_tiles, None, B, rs,
@@ -481,7 +501,14 @@ class InferExecutor:
         par = phase % 2
         # LL: {value, tag} stores polled by the consumer; tag = epoch * n_phases + phase
         # (a loopback timing rank -- profiler.loopback_rank -- fills every rank's slots itself)
-        if B <= LL_CLUSTER_ROWS and cm.tp >= LL_CLUSTER_MIN_TP and lib.tps_cluster_splits(n, k, B) > 0:
+        if B <= self.gemv_rows:
+            S = 1  # one full dot product per element, pushed once to every rank
+            dsts = [cm.ll_slot(base, par, q if cm.loopback else self.rank, 1) for q, base in enumerate(cm.peer_ll)]
+            nat.check(lib.tps_gemv_push_ll(w.data_ptr(), n, k, k, x.data_ptr(), B, x.shape[1], self._arr(dsts),
+                                           len(dsts), cm.epoch.data_ptr(), cm.n_phases, phase, st),
+                      "tps_gemv_push_ll")
+            stats.add("linear")
+        elif B <= LL_CLUSTER_ROWS and cm.tp >= LL_CLUSTER_MIN_TP and lib.tps_cluster_splits(n, k, B) > 0:
             S = 1  # one reduced slot per rank
             dsts = [cm.ll_slot(base, par, q if cm.loopback else self.rank, 1) for q, base in enumerate(cm.peer_ll)]
             nat.check(lib.tps_linear_push_ll_cluster(w.data_ptr(), n, k, k, x.data_ptr(), B, x.shape[0], x.shape[1],

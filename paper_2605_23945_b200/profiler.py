@@ -83,11 +83,13 @@ def gemm_probe(ex: InferExecutor, B: int, reps: int = 2) -> dict:
     return out
 
 
-def tail_probe(geom, tp: int, batches, ctx: int, peak_gbps: float, n: int = 30) -> dict:
+def tail_probe(geom, tp: int, batches, ctx: int, peak_gbps: float, n: int = 30, gemv: bool = True) -> dict:
     """Post-switch tail steps (SURVEY 8(d) "tail = post-switch B <= 32"): one TP-`tp` rank alone on
     the device (loopback peer table, `loopback_rank`), graph-replayed steps at context `ctx` per
     batch, vs the rank's HBM floor = weight shards (linears + LM-head shard) + live K/V + new K/V
-    at the measured copy peak. Returns {B: {"ms", "floor_ms", "frac", "kernels"}}."""
+    at the measured copy peak. Returns {B: {"ms", "floor_ms", "frac", "kernels"}}; with `gemv`,
+    buckets the warp-shuffle GEMV takes (<= tps_gemv_max_rows()) are also timed with every
+    projection on it ("gemv_ms", "gemv_frac") -- the A/B behind executor.GEMV_ROWS."""
     from .kvcache import pages_for
     from .models import rank_shard
     from .shards import arena_layout
@@ -109,6 +111,15 @@ def tail_probe(geom, tp: int, batches, ctx: int, peak_gbps: float, n: int = 30) 
         floor = byt / (peak_gbps * 1e9) * 1e3
         out[B] = {"ms": ms, "floor_ms": floor, "frac": floor / ms, "bytes": byt,
                   "kernels": runner.kernels_per_step(bk)}
+        if gemv and bk <= nat.lib().tps_gemv_max_rows():
+            default = r.executor.gemv_rows
+            r.executor.gemv_rows = bk
+            runner.graphs.pop(bk, None)  # recapture the bucket with the GEMV projections
+            r.slots.pos[:] = ctx
+            gms = step_probe(runner, bk, n)
+            out[B].update({"gemv_ms": gms, "gemv_frac": floor / gms})
+            r.executor.gemv_rows = default
+            runner.graphs.pop(bk, None)
     del r, runner
     gc.collect()
     torch.cuda.empty_cache()

@@ -120,13 +120,14 @@ def compare(logits, hist, orc, slots_rows, starts, steps, tol, mean_tol=MEAN_TOL
     return worst
 
 
-def run_long_context(name, tp, ctx, gen=3, layers=2, tol=0.05, noise_floor=False, persist=False):
+def run_long_context(name, tp, ctx, gen=3, layers=2, tol=0.05, noise_floor=False, persist=False, gemv=0):
     geom = truncated(name, layers)
     B = len(ctx)
     max_len = max(ctx) + gen + 8
     ranks, runner = build(geom, tp, max_batch=max(B, 8), num_slots=B, max_len=max_len)
     for r in ranks:  # B <= 16: the persistent one-launch step, else the per-kernel step
         r.executor.use_persist = persist
+        r.executor.gemv_rows = gemv  # B <= gemv: projections on the CUDA-core GEMV (csrc/gemv.cu)
     gtok = torch.Generator().manual_seed(len(ctx))
     slots = []
     for i, P in enumerate(ctx):

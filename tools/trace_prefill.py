@@ -8,7 +8,7 @@ from paper_2605_23945_b200.models import geometry
 from paper_2605_23945_b200.profiler import loopback_rank
 
 KIND = {1: "embed", 2: "add_norm", 3: "reduce_push", 4: "qkv_rope", 5: "silu_mul", 6: "argmax1", 7: "argmax2",
-        8: "epoch", 9: "gemm", 10: "gemm_silu", 11: "attn_split", 12: "attn_combine", 13: "attn_bal", 14: "attn_prefill", 15: "gemm_push"}
+        8: "epoch", 9: "gemm", 10: "gemm_silu", 11: "attn_split", 12: "attn_combine", 13: "attn_bal", 14: "attn_prefill", 15: "gemm_push", 16: "gemv"}
 name = sys.argv[1] if len(sys.argv) > 1 else "qwen2.5-7b"
 ctx = int(sys.argv[2]) if len(sys.argv) > 2 else 256
 tp = int(sys.argv[3]) if len(sys.argv) > 3 else 1

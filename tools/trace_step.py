@@ -12,7 +12,7 @@ from paper_2605_23945_b200.models import geometry
 from paper_2605_23945_b200.profiler import loopback_rank
 
 KIND = {1: "embed", 2: "add_norm", 3: "reduce_push", 4: "qkv_rope", 5: "silu_mul", 6: "argmax1", 7: "argmax2",
-        8: "epoch", 9: "gemm", 10: "gemm_silu", 11: "attn_split", 12: "attn_combine", 13: "attn_bal", 14: "attn_prefill", 15: "gemm_push"}
+        8: "epoch", 9: "gemm", 10: "gemm_silu", 11: "attn_split", 12: "attn_combine", 13: "attn_bal", 14: "attn_prefill", 15: "gemm_push", 16: "gemv"}
 name, tp, B, ctx = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4])
 geom = geometry(name)
 r, runner = loopback_rank(geom, tp, B, B, ctx + 256, B * ((ctx + 256) // 64 + 2))
