@@ -154,8 +154,12 @@ class GroupComm:
         return base + ((parity * FUSE_SOURCES + src_rank * splits) * FUSE_ROWS * self.hidden) * 8
 
     def reset(self) -> None:
+        # the epoch restarts at 1: clear the LL slots too, or a tag stored before the reset
+        # (epoch e, phase p) would satisfy the same (e, p) wait after it
         self.ctr.zero_()
         self.done.zero_()
+        self.ll.zero_()
+        self.am.zero_()
         self.epoch.fill_(1)
 
 
