@@ -248,6 +248,80 @@ def cpu_stage_estimate(spec, steps: dict, hist: dict[int, int]) -> float:
     return dec + pre
 
 
+def cpu_switch_copy(geom, samples: int, ctx: int, threads: int, reps: int = 3, verify: bool = False) -> dict:
+    """SURVEY 8(d) CPU baseline (ii) for the switch: BASELINE config 5's microbench switch
+    (TP1/DP2 -> TP2/DP1, `samples` live samples at context `ctx`) as host copies with torch on
+    this host's cores. Weights: the Switch Executor's own pull plan (`plan_weight_pulls`, the
+    canonical slices of tpshift/reshard.py:25-43) executed piece by piece as byte-slice copies
+    between host arenas (both old replicas hold identical bytes: one host arena stands for both).
+    KV: every sample's pages gathered from its old group's pool and scattered into the new
+    ranks' pools with the rank's KV heads ([2L][pages][n_kv][64][D] bf16, the engine's layout),
+    one torch index copy per (sample, target rank). Returns bytes, seconds and GB/s of each
+    part, median over `reps` passes (`verify`: also the host buffers, for the CPU test against
+    the canonical shards of oracle/reshard_ref.py)."""
+    from paper_2605_23945_b200.kvcache import PAGE, pages_for
+    from paper_2605_23945_b200.models import rank_shard
+    from paper_2605_23945_b200.shards import arena_layout
+    from paper_2605_23945_b200.switch_executor import Layout, plan_weight_pulls
+    torch.set_num_threads(threads)
+    old, new = Layout(1, 2), Layout(2, 2)
+    nsrc = arena_layout(geom, rank_shard(geom, 1, 0)).total_bytes
+    src = torch.randint(0, 256, (nsrc,), dtype=torch.uint8, generator=torch.Generator().manual_seed(1)) \
+        if verify else torch.ones(nsrc, dtype=torch.uint8)
+    plans = [plan_weight_pulls(geom, old, new, r).arrays() for r in range(2)]
+    dsts = [torch.zeros(arena_layout(geom, rank_shard(geom, 2, r)).total_bytes, dtype=torch.uint8)
+            for r in range(2)]
+    wbytes = int(sum(int(p[3].sum()) for p in plans))
+    t_ws = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        for (_, so, do, nb), dst in zip(plans, dsts):
+            for a, b, n in zip(so.tolist(), do.tolist(), nb.tolist()):
+                dst[b:b + n].copy_(src[a:a + n])
+        t_ws.append(time.perf_counter() - t0)
+    t_w = statistics.median(t_ws)
+    L, nkv, D = geom.num_layers, geom.n_kv, geom.head_dim
+    npg = pages_for(ctx)
+    per_group = -(-samples // 2)
+    g = torch.Generator().manual_seed(2)
+    pools = [torch.randint(-2 ** 15, 2 ** 15, (L, 2, per_group * npg, nkv, PAGE, D), dtype=torch.int16, generator=g)
+             for _ in range(2)]
+    hk = [rank_shard(geom, 2, r).kv_heads for r in range(2)]
+    new_pools = [torch.zeros((L, 2, samples * npg, b - a, PAGE, D), dtype=torch.int16) for a, b in hk]
+    kbytes = samples * L * 2 * npg * nkv * PAGE * D * 2
+    t_kvs = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        for i in range(samples):
+            old_g, j = i % 2, i // 2  # sample i ran in old DP group i % 2
+            sp = torch.arange(j * npg, (j + 1) * npg)
+            dp = torch.arange(i * npg, (i + 1) * npg)
+            for r, (a, b) in enumerate(hk):
+                new_pools[r][:, :, dp] = pools[old_g][:, :, sp, a:b]
+        t_kvs.append(time.perf_counter() - t0)
+    t_kv = statistics.median(t_kvs)
+    out = {"weights_bytes": wbytes, "weights_s": t_w, "weights_gbps": wbytes / t_w / 1e9,
+           "weight_pieces": int(sum(len(p[3]) for p in plans)), "kv_bytes": kbytes, "kv_s": t_kv,
+           "kv_gbps": kbytes / t_kv / 1e9, "gbps": (wbytes + kbytes) / (t_w + t_kv) / 1e9, "cores": threads,
+           "reps": reps}
+    if verify:
+        out["arenas"] = (src, dsts, plans, pools, new_pools, hk)
+    return out
+
+
+def cpu_switch_baseline(model: str, threads: int, layers: int = 4, samples: int = 16, ctx: int = 4096) -> dict:
+    """cpu_switch_copy on a bounded sample of config 5's microbench switch: the first `layers`
+    layers of the model (embedding, LM head and norms included); GB/s is per byte moved."""
+    import dataclasses as dc
+    from paper_2605_23945_b200.models import geometry
+    geom = dc.replace(geometry(model), num_layers=layers)
+    r = cpu_switch_copy(geom, samples, ctx, threads)
+    r["sample"] = (f"c5 switch TP1/DP2 -> TP2/DP1 of {model} truncated to {layers} layers (+ embedding / LM head), "
+                   f"{samples} samples at ctx {ctx}: the executor's weight pull plan as torch byte-slice copies "
+                   f"and KV page gather/scatter per (sample, rank), {threads} threads")
+    return r
+
+
 def decision_layer_timing(args) -> dict:
     """The reference's own CPU path, single-threaded Python (SURVEY 8(d) CPU baseline (i)):
     Algorithm 1 `evaluate` at B=512 (BASELINE config 2 on 8 GPUs, TP1/DP8, mid-stage) and one
@@ -482,6 +556,10 @@ def main():
             line["cpu_baseline"]["decision_layer"] = decision_layer_timing(args)
         except Exception as e:
             line["cpu_baseline"]["decision_layer"] = {"error": f"{type(e).__name__}: {e}"}
+        try:
+            line["cpu_baseline"]["switch"] = cpu_switch_baseline(args.model, threads)
+        except Exception as e:
+            line["cpu_baseline"]["switch"] = {"error": f"{type(e).__name__}: {e}"}
     if rank == 0:
         print(json.dumps(line), flush=True)
 
@@ -617,7 +695,8 @@ def reference_arm(args):
                    "model": args.model, "global_batch": spec.global_batch},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
                          "measured_steps_s": {str(b): t for b, t in steps["steps"].items()},
-                         "decision_layer": decision_layer_timing(args)},
+                         "decision_layer": decision_layer_timing(args),
+                         "switch": cpu_switch_baseline(args.model, threads)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
