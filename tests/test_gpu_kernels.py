@@ -380,12 +380,16 @@ def test_linear_push_ll_cluster(n, k, b, ndst):
                                              nat.ptr_array([t.data_ptr() for t in slots]), ndst, epoch.data_ptr(),
                                              3, 1, _stream()))
     torch.cuda.synchronize()
+    # directly against torch fp32 too (not only transitively through tps_linear)
+    fp32 = (x.float() @ w.float().T).cpu()
+    tol = 2e-3 * math.sqrt(k) * 0.05 * 4 + 1e-4
     for t in slots:
         u = t[:b].cpu()
         tags = (u >> 32) & 0xFFFFFFFF
         assert (tags == 5 * 3 + 1).all()
         vals = (u & 0xFFFFFFFF).to(torch.int32).view(torch.float32)
         assert torch.equal(vals, ref.cpu())
+        assert (vals - fp32).abs().max().item() <= tol
         assert (t[b:] == -1).all()
 
 
@@ -409,6 +413,8 @@ def test_linear_argmax_epilogue(V, k, b):
                                     cand.data_ptr(), vocab0, _stream()))
     torch.cuda.synchronize()
     assert torch.equal(logits, ref[0])
+    tol = 2e-3 * math.sqrt(k) * 0.05 * 4 + 1e-4  # and directly against torch fp32
+    assert (logits - x.float() @ w.float().T).abs().max().item() <= tol
     vals = cand[..., 0].view(torch.float32).cpu()
     idxs = cand[..., 1].cpu()
     lg = ref[0].cpu()
