@@ -450,7 +450,10 @@ def main():
                       "seconds": s["breakdown"]["total"], "release_to_resume_s": s.get("release_to_resume_s"),
                       "max_gpu_peer_bytes": s.get("max_gpu_peer_bytes"),
                       "max_gpu_local_bytes": s.get("max_gpu_local_bytes"),
-                      "peer_gbps_per_gpu": s.get("peer_gbps_per_gpu"), "host_switch_s": s.get("host_switch_s")}
+                      "peer_gbps_per_gpu": s.get("peer_gbps_per_gpu"), "host_switch_s": s.get("host_switch_s"),
+                      # the reference plan's volumes beside the executed bytes
+                      "reference_plan_bytes_per_rank": {"weights": s.get("weight_plan_per_rank_bytes"),
+                                                        "kv": (s.get("kv_plan") or {}).get("per_rank_bytes")}}
                      for s in switch],
         "switch_gbps": (sum(sw_gbps) / len(sw_gbps)) if sw_gbps else None,
         "switch_gbps_note": "max over GPUs of bytes pulled from peers / that GPU's barrier-release -> resume "
