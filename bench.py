@@ -44,6 +44,7 @@ sys.path.insert(0, HERE)
 
 METRIC = "rollout time to last sample (s) on 8xB200; switch reshard+KV-migrate GB/s"
 UNIT = "s"
+NOMINAL_HBM_GBPS = 8000.0  # B200 HBM3e nominal; SURVEY 8(d) asks for the fraction of both peaks
 
 
 def parse():
@@ -463,7 +464,8 @@ def main():
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None, "kernel": "gemm_swapab_kernel (tcgen05)",
-                     "peak_source": peak_src,
+                     "peak_source": peak_src, "nominal_peak": NOMINAL_HBM_GBPS,
+                     "frac_nominal": achieved / NOMINAL_HBM_GBPS,
                      "algorithmic_bytes_per_launch": g_bytes / g_launch, "launches_per_step": g_launch,
                      "split_partial_overhead_bytes_per_step": g_ovh,
                      "bytes_note": "algorithmic = weight shard + activations + one fp32 output row per batch row "

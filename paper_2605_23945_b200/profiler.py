@@ -110,6 +110,7 @@ def tail_probe(geom, tp: int, batches, ctx: int, peak_gbps: float, n: int = 30, 
         byt = w + B * (ctx + 1) * kv_tok
         floor = byt / (peak_gbps * 1e9) * 1e3
         out[B] = {"ms": ms, "floor_ms": floor, "frac": floor / ms, "bytes": byt,
+                  "gbps": byt / ms / 1e6, "frac_nominal_8tbps": byt / ms / 1e6 / 8000.0,
                   "kernels": runner.kernels_per_step(bk)}
         if gemv and bk <= nat.lib().tps_gemv_max_rows():
             default = r.executor.gemv_rows
