@@ -18,6 +18,7 @@ decode path + decode to the last sample), run by the Global Coordinator.
              depth: decode steps timed at B = 1, 8, 64 and composed over the stage's rounds
   tail       the post-switch TP8 tail (one loopback rank, B <= 32) vs its HBM floor, with
              the warp-shuffle GEMV form (csrc/gemv.cu) timed beside the default at B <= 4
+  gemv_stage the same stage with buckets of <= 4 rows on that GEMV (N=1, run last)
 
 `--impl reference` times the reference-side CPU path (the oracle port) instead.
 Run: python bench.py [--gpus N --steps K --warmup W]; N>1 under torchrun.
@@ -64,6 +65,8 @@ def parse():
     ap.add_argument("--static-tps", default="all",
                     help="N>1: also time the stage at these fixed TP degrees (default: every TP degree dividing N)")
     ap.add_argument("--no-tail", action="store_true")
+    ap.add_argument("--no-gemv-ab", action="store_true",
+                    help="N=1: skip the stage re-run with the tail buckets (<= 4 rows) on the warp-shuffle GEMV")
     ap.add_argument("--tp-list", default="", help="Algorithm 1 candidates (default: 1 and N, BASELINE config 2)")
     ap.add_argument("--initial-tp", type=int, default=1, help="starting TP degree (config 4 starts at TP2)")
     ap.add_argument("--cpu-threads", type=int, default=0)
@@ -565,8 +568,36 @@ def main():
             line["cpu_baseline"]["switch"] = cpu_switch_baseline(args.model, threads)
         except Exception as e:
             line["cpu_baseline"]["switch"] = {"error": f"{type(e).__name__}: {e}"}
+    if rank == 0 and gpus == 1 and not args.no_gemv_ab and not args.virtual:
+        # last (it rebuilds the backend): the same stage with every bucket of <= 4 rows on the
+        # warp-shuffle GEMV (csrc/gemv.cu) -- the stage-level A/B behind executor.GEMV_ROWS
+        try:
+            ex = be = None  # (drop this frame's handles on the first backend before rebuilding)
+            line["gemv_stage"] = gemv_stage_ab(spec, geom, world, table, coord)
+        except Exception as e:
+            line["gemv_stage"] = {"error": f"{type(e).__name__}: {e}"}
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def gemv_stage_ab(spec, geom, world, table, coord) -> dict:
+    from paper_2605_23945_b200 import executor as exmod
+    from paper_2605_23945_b200.coordinator import GlobalCoordinator
+    coord.backend = None
+    del coord
+    gc.collect()
+    torch.cuda.empty_cache()
+    old = exmod.GEMV_ROWS
+    exmod.GEMV_ROWS = 4
+    try:
+        c2 = GlobalCoordinator(spec, geom, world, seed=0, table=table)
+        c2.run()  # warm-up stage
+        rep, _ = c2.run()
+    finally:
+        exmod.GEMV_ROWS = old
+    return {"value": rep.generation_time, "unit": UNIT, "gemv_rows": 4,
+            "note": "the same stage (one warm-up, one timed) with buckets of <= 4 rows on the warp-shuffle GEMV; "
+                    "compare with `value`"}
 
 
 def stage_mean_context(spec) -> int:
