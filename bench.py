@@ -326,6 +326,35 @@ def cpu_switch_baseline(model: str, threads: int, layers: int = 4, samples: int 
     return r
 
 
+REF_INSTALL = os.path.join(HERE, "baseline", "_ref")  # the unmodified reference (pip --target, __graft_entry__.build)
+
+
+def reference_package():
+    """The unmodified reference package `tpshift` from baseline/_ref (installed from
+    /root/reference by __graft_entry__.build(); it travels to the GPU box), or None."""
+    if not os.path.isdir(os.path.join(REF_INSTALL, "tpshift")):
+        return None
+    if REF_INSTALL not in sys.path:
+        sys.path.insert(0, REF_INSTALL)
+    import tpshift
+    return tpshift
+
+
+def to_reference(T, x):
+    """Rebuild one of this package's decision-layer values (dataclasses of the reference's own
+    names and fields, restated bit-exactly) as the reference's type."""
+    if dataclasses.is_dataclass(x) and not isinstance(x, type):
+        cls = getattr(T, type(x).__name__)
+        return cls(**{f.name: to_reference(T, getattr(x, f.name)) for f in dataclasses.fields(x)})
+    if isinstance(x, tuple):
+        return tuple(to_reference(T, v) for v in x)
+    if isinstance(x, list):
+        return [to_reference(T, v) for v in x]
+    if isinstance(x, dict):
+        return {k: to_reference(T, v) for k, v in x.items()}
+    return x
+
+
 def decision_layer_timing(args) -> dict:
     """The reference's own CPU path, single-threaded Python (SURVEY 8(d) CPU baseline (i)):
     Algorithm 1 `evaluate` at B=512 (BASELINE config 2 on 8 GPUs, TP1/DP8, mid-stage) and one
@@ -360,9 +389,35 @@ def decision_layer_timing(args) -> dict:
     t0 = time.perf_counter()
     rep = sim_run(spec, table)
     run_s = time.perf_counter() - t0
-    return {"evaluate_ms": ev * 1e3, "evaluate_live_samples": live, "run_stage_s": run_s,
-            "run_stage": f"c2 on 8 GPUs: {spec.global_batch} samples, tp_list (1,2,4,8), "
-                         f"{rep.eval_count} evaluations", "cores": 1}
+    out = {"evaluate_ms": ev * 1e3, "evaluate_live_samples": live, "run_stage_s": run_s,
+           "run_stage": f"c2 on 8 GPUs: {spec.global_batch} samples, tp_list (1,2,4,8), "
+                        f"{rep.eval_count} evaluations", "cores": 1,
+           "impl": "restated (paper_2605_23945_b200 decision layer, bit-exact with tpshift)"}
+    T = reference_package()
+    if T is None:
+        out["reference_impl"] = {"unavailable": "baseline/_ref has no tpshift install"}
+        return out
+    # the same two calls through the UNMODIFIED reference (tpshift from baseline/_ref), same inputs
+    rspec, rtab = to_reference(T, spec), to_reference(T, table)
+    rpred = T.fit_predictor(rtab)  # the reference's own predictor fit of the same measured table
+    rargs = [to_reference(T, spec.controller), rpred] + [to_reference(T, a) for a in (pool, spec.switch, st, cur)]
+    rmod, rcl = to_reference(T, spec.model), to_reference(T, spec.cluster)
+    T.evaluate(*rargs, spec.l_max, l_gen, rmod, rcl)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        T.evaluate(*rargs, spec.l_max, l_gen, rmod, rcl)
+    rev = (time.perf_counter() - t0) / reps
+    t0 = time.perf_counter()
+    rrep = T.run(rspec, rtab)
+    rrun = time.perf_counter() - t0
+    dec, rdec = (evaluate(spec.controller, pred, pool, spec.switch, st, cur, spec.l_max, l_gen, spec.model,
+                          spec.cluster), T.evaluate(*rargs, spec.l_max, l_gen, rmod, rcl))
+    out["reference_impl"] = {"evaluate_ms": rev * 1e3, "run_stage_s": rrun, "cores": 1,
+                             "report_identical": rrep.to_json() == rep.to_json(),
+                             "decision_identical": (dec.action, repr(dec.t_cur), repr(dec.t_best)) ==
+                                                   (rdec.action, repr(rdec.t_cur), repr(rdec.t_best)),
+                             "source": "tpshift (unmodified reference) from baseline/_ref"}
+    return out
 
 
 def main():
