@@ -560,6 +560,12 @@ def main():
         for tp in fixed:
             if gpus % tp or not _tp_ok(geom, tp):
                 continue
+            # discard the previous backend: peers' mappings of its buffers are closed on every rank
+            # before any rank frees them (CUDA IPC), then the memory goes back to the device
+            torch.cuda.synchronize(dev)
+            world.barrier()
+            world.close_peers()
+            world.barrier()
             ex = coord = None
             gc.collect()  # executors / runners / comms form reference cycles
             torch.cuda.empty_cache()

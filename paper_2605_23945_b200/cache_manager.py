@@ -101,6 +101,17 @@ class World:
         return out
 
 
+    def close_peers(self) -> None:
+        """Unmap every peer buffer this process opened (tps_ipc_close) and forget the handles.
+        For discarding a whole backend: call it on every rank after the last kernel that touches
+        a peer buffer (device synchronised, then a barrier) and before any rank frees memory it
+        exported (another barrier) -- freeing an exported buffer that a peer still has mapped is
+        undefined in CUDA IPC, and its memory is not reclaimed while the mapping lives."""
+        for base in self._ipc_cache.values():
+            nat.check(nat.lib().tps_ipc_close(base), "ipc_close")
+        self._ipc_cache.clear()
+
+
 class CacheManager:
     """Per-layout communicator tables, created on first use and kept (grow-only pool)."""
 
