@@ -341,18 +341,9 @@ def reference_package():
 
 
 def to_reference(T, x):
-    """Rebuild one of this package's decision-layer values (dataclasses of the reference's own
-    names and fields, restated bit-exactly) as the reference's type."""
-    if dataclasses.is_dataclass(x) and not isinstance(x, type):
-        cls = getattr(T, type(x).__name__)
-        return cls(**{f.name: to_reference(T, getattr(x, f.name)) for f in dataclasses.fields(x)})
-    if isinstance(x, tuple):
-        return tuple(to_reference(T, v) for v in x)
-    if isinstance(x, list):
-        return [to_reference(T, v) for v in x]
-    if isinstance(x, dict):
-        return {k: to_reference(T, v) for k, v in x.items()}
-    return x
+    """This package's decision-layer value as the reference's type (interop.to_reference)."""
+    from paper_2605_23945_b200.interop import to_reference as conv
+    return conv(T, x)
 
 
 def decision_layer_timing(args) -> dict:
