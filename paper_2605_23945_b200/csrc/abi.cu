@@ -87,6 +87,7 @@ int trace_register_attention(uint64_t*, unsigned int*, unsigned int);
 int trace_register_attention_bal(uint64_t*, unsigned int*, unsigned int);
 int trace_register_gemm(uint64_t*, unsigned int*, unsigned int);
 int trace_register_attention_prefill(uint64_t*, unsigned int*, unsigned int);
+int trace_register_gemv(uint64_t*, unsigned int*, unsigned int);
 int barrier(uint64_t* const*, int, const uint64_t*, int, int, uint64_t, cudaStream_t);
 int ipc_get_handle(const void*, void*, int64_t*);
 int ipc_open(const void*, void**);
@@ -468,7 +469,7 @@ int tps_trace_enable(uint64_t* records, unsigned int* counter, unsigned int capa
   TPS_CHECK_ARG((records && counter) || (!records && !counter), "trace: records and counter together");
   if (trace_register_decode(records, counter, capacity) || trace_register_attention(records, counter, capacity) ||
       trace_register_attention_bal(records, counter, capacity) || trace_register_gemm(records, counter, capacity) ||
-      trace_register_attention_prefill(records, counter, capacity))
+      trace_register_attention_prefill(records, counter, capacity) || trace_register_gemv(records, counter, capacity))
     return fail(kCuda, "trace: cudaMemcpyToSymbol failed");
   return kOk;
 }

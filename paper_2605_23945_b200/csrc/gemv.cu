@@ -303,6 +303,8 @@ GvArgs gv_args(const void* w, int64_t n_out, int64_t k, int64_t ldw, const void*
 
 int gemv_max_rows() { return kGvMaxB; }
 
+int trace_register_gemv(uint64_t* p, unsigned int* c, unsigned int n) { return trace_register(p, c, n); }
+
 int gemv(const void* w, int64_t n, int64_t k, int64_t ldw, const void* x, int64_t b, int64_t ldx, float* out,
          cudaStream_t st) {
   if (int e = gv_check(w, n, k, ldw, x, b, ldx)) return e;
