@@ -176,3 +176,25 @@ def test_decode_on_gemv_matches_oracle(gemv_on, name, tp):
 def test_full_shapes_on_gemv_match_oracle(name, tp, ctx):
     from test_gpu_decode_fullshape import run_long_context
     run_long_context(name, tp, ctx=ctx, gemv=4)
+
+
+@pytest.mark.parametrize("name,tp", [("tiny", 2), ("mini-llama", 8)])
+def test_gemv_graph_replay_matches_eager(gemv_on, name, tp):
+    """The GEMV launches captured in a CUDA graph (as the bench and the stages run them) give the
+    eager step's tokens bit for bit."""
+    from paper_2605_23945_b200.group import admit, build_group
+    from paper_2605_23945_b200.models import geometry
+    geom = geometry(name)
+    outs = []
+    for graphs in (False, True):
+        ranks, runner = build_group(geom, tp, max_batch=8, num_slots=4, max_len=128, seed=3, use_graphs=graphs)
+        assert all(r.executor.gemv_rows == 4 for r in ranks)
+        slots = [admit(ranks, i, p, max_ctx=len(p) + 20) for i, p in enumerate(PROMPTS)]
+        runner.set_rows(2, slots)
+        runner.step(2, 1)  # eager warm-up step
+        if graphs:
+            runner.capture(2)
+        runner.step(2, 20)
+        torch.cuda.synchronize()
+        outs.append(ranks[0].slots.history[slots].cpu())
+    assert torch.equal(outs[0], outs[1])
