@@ -720,6 +720,21 @@ def traffic_record():
         return None
 
 
+def reference_plan_bytes(spec, tp_src: int, dp_src: int, tp_tgt: int, samples: int, ctx: int) -> dict:
+    """The reference's priced plans for the same switch (reported beside the executed
+    bytes): per-rank received bytes of plan_weight_reshard / plan_kv_migration
+    (tpshift/reshard.py:80-151, restated bit-exactly). The reference prices KV at the full hidden
+    width per token (2 H bytes per layer); the executor moves the GQA heads (2 n_kv D)."""
+    from paper_2605_23945_b200.reshard import ShardLayout, plan_kv_migration, plan_weight_reshard
+    from paper_2605_23945_b200.workload import Sample
+    H = spec.model.hidden_dim
+    w = plan_weight_reshard(spec.model, ShardLayout(tp=tp_src, dim=H), ShardLayout(tp=tp_tgt, dim=H))
+    live = [Sample(id=i, prompt_len=spec.prompt_len, target_response_len=spec.l_max,
+                   generated_len=ctx - spec.prompt_len, intra_dp_group=i % dp_src) for i in range(samples)]
+    kv = plan_kv_migration(live, spec.model, tp_src, dp_src, tp_tgt)
+    return {"weights": w.total_per_rank_bytes, "kv": kv.total_per_rank_bytes}
+
+
 def switch_microbench(args, hbm_peak):
     """BASELINE config 5 on one device: a real Switch Executor run TP1/DP2 -> TP2/DP1 of the
     bench model in a virtual 2-rank world (both ranks on this GPU, so every pull is an HBM
@@ -734,6 +749,7 @@ def switch_microbench(args, hbm_peak):
     r = switch_probe(spec, geom, World.virtual(2), 2, 16, 4096, copy_mode=1)
     gc.collect()
     torch.cuda.empty_cache()
+    ref_plan = reference_plan_bytes(spec, 1, 2, 2, 16, 4096)
     return {"config": f"c5: {args.model}, virtual TP1/DP2 -> TP2/DP1 on one B200, 16 samples at ctx 4096, "
                       f"TMA bulk copy engine",
             "weights_bytes": r["weights_bytes"], "kv_bytes": r["kv_bytes"], "copy_bytes": r["copy_bytes"],
@@ -743,7 +759,7 @@ def switch_microbench(args, hbm_peak):
             "switch_device_ms": r["switch_device_ms"], "release_to_resume_ms": r["release_to_resume_ms"],
             "max_gpu_peer_bytes": r["max_gpu_peer_bytes"], "max_gpu_local_bytes": r["max_gpu_local_bytes"],
             "host_switch_s": r["host_switch_s"], "host_plan_s": r["host_plan_s"],
-            "host_capture_s": r["host_capture_s"],
+            "host_capture_s": r["host_capture_s"], "reference_plan_bytes_per_rank": ref_plan,
             "note": "every rank on this GPU: a peer pull is an HBM copy; switch_device_ms runs from the first "
                     "rank's arrival at the opening barrier to the last rank's resume, host work included"}
 
