@@ -51,3 +51,18 @@ def test_cpu_switch_copy_is_the_canonical_reshard():
         for lay in (arena_layout(geom, rank_shard(geom, 2, q)) for q in range(2)))
     assert r["kv_bytes"] == samples * geom.num_layers * 2 * npg * geom.n_kv * 64 * geom.head_dim * 2
     assert r["weights_gbps"] > 0 and r["kv_gbps"] > 0
+
+
+def test_reference_plan_bytes_of_the_microbench_switch():
+    """bench.reference_plan_bytes = the reference's priced volumes (tpshift/reshard.py:80-151):
+    a TP1 -> TP2 weight reshard receives half of every layer; its KV plan counts the full hidden
+    width per token (2 H bytes per layer), not the GQA heads the executor moves."""
+    import argparse
+    import dataclasses
+    ns = argparse.Namespace(model="qwen2.5-7b", per_gpu_batch=8, l_max=8192, prompt_len=512, seed=4)
+    spec, geom = bench.build_spec(ns, 2)
+    spec = dataclasses.replace(spec, initial_tp=1, global_batch=16)
+    got = bench.reference_plan_bytes(spec, 1, 2, 2, 16, 4096)
+    L, H = geom.num_layers, geom.hidden
+    assert got["weights"] == L * geom.layer_param_bytes // 2
+    assert got["kv"] == L * 2 * 16 * 4096 * H * 2
