@@ -2,6 +2,11 @@
 set -x
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+# first contact under memcheck: an out-of-bounds access is reported by the instrumentation instead
+# of faulting the device (the kernel-level tests only; the step tests follow without the tool)
+timeout 900 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_gpu_tail_gemv.py -x -q \
+  -k "not full_shapes and not decode and not graph" > gpurun_out/memcheck_gemv.log 2>&1; tail -5 gpurun_out/memcheck_gemv.log
+grep -q "ERROR SUMMARY: 0 errors" gpurun_out/memcheck_gemv.log || { echo "memcheck not clean: stop"; exit 1; }
 timeout 900 python -m pytest tests/test_gpu_tail_gemv.py -x -q -k "not full_shapes" > gpurun_out/pytest_gemv.log 2>&1; tail -5 gpurun_out/pytest_gemv.log
 for g in 0 4; do echo "TPS_GEMV_ROWS=$g"; TPS_GEMV_ROWS=$g timeout 600 python tools/solo_step.py qwen2.5-7b 1,2,4,8 1,2,4 2048 2>&1 | grep step; done
 timeout 1800 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
